@@ -1,0 +1,229 @@
+/* pe.h — C-ABI of the B200 candidate-evaluation engine for automap
+ * (arxiv 2112.02958).  This header is the drop-in boundary: plain C types,
+ * caller-owned buffers, status codes instead of exceptions.
+ *
+ * Every entry point names the reference interface it replaces
+ * (REF = /root/reference/proj, SPEC = /root/reference/SPEC.md).  The same
+ * structs are used by the CPU parity oracle (oracle/), so a harness can call
+ * either implementation through one set of types.
+ *
+ * Threading: graphs are immutable after creation and may be shared.  One
+ * engine per device; an engine is not reentrant on one stream.
+ */
+#ifndef PE_H_
+#define PE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PE_MAX_AXES 4  /* mesh axes per program (REF mesh.h:38-48)          */
+#define PE_MAX_RANK 4  /* tensor rank bound kMaxRank (REF tensor.h:46)       */
+
+/* Library status codes; the C++ exception hierarchy of REF error.h:25-60
+ * maps onto these (the reference CLI maps them to exit codes 1/2/70,
+ * SPEC:730). */
+typedef enum pe_status {
+  PE_OK = 0,
+  PE_ERR_PARSE = 1,            /* ParseError(line, col)   error.h:28-39  */
+  PE_ERR_VALIDATION = 2,       /* ValidationError         error.h:43-46  */
+  PE_ERR_ILLEGAL = 3,          /* IllegalActionError      error.h:49-52  */
+  PE_ERR_INVALID_ARGUMENT = 4, /* bad pointer / size at the boundary     */
+  PE_ERR_CUDA = 5,             /* CUDA runtime failure                    */
+  PE_ERR_NO_DEVICE = 6,        /* no CUDA device: the engine never falls back to CPU */
+  PE_ERR_CAPACITY = 7,         /* a per-candidate arena bound was exceeded */
+  PE_ERR_INTERNAL = 70         /* InternalError           error.h:57-62  */
+} pe_status;
+
+typedef struct pe_error {
+  int32_t code;   /* pe_status */
+  int32_t line;   /* ParseError position, 1-based; 0 otherwise */
+  int32_t column;
+  char message[500];
+} pe_error;
+
+/* ---- actions (SPEC:484-487 `Action` = TileValue | InferRest | Stop) ---- */
+enum {
+  PE_ACT_TILE = 0,       /* apply_tile_action(value, dim, axis) then propagate
+                            (REF rewrite.cc:61-113, propagate.cc:459-482)      */
+  PE_ACT_TILE_GROUP = 1, /* the same on every member of a scope group, one
+                            propagate (grouping SPEC:568)            */
+  PE_ACT_INFER_REST = 2, /* infer_rest (REF propagate.cc:484-544) — reserved   */
+  PE_ACT_STOP = 3        /* terminal                                           */
+};
+
+typedef struct pe_action {
+  uint32_t value; /* value index (args [0,A), ops [A,A+N)) or group index */
+  uint8_t dim;
+  uint8_t axis;   /* mesh axis index in declaration order */
+  uint8_t kind;   /* PE_ACT_* */
+  uint8_t pad;
+} pe_action;
+
+/* ---- per-candidate result record ---- */
+enum {
+  PE_CAND_OK = 0,
+  PE_CAND_ILLEGAL = 1,  /* an action raised IllegalActionError; the state
+                           before it is scored, fail_step names the action  */
+  PE_CAND_INTERNAL = 2, /* InternalError / ValidationError inside propagate or
+                           lowering; no score                               */
+  PE_CAND_CAPACITY = 3  /* engine arena bound exceeded (engine only)        */
+};
+
+typedef struct pe_result {
+  int64_t peak_bytes;       /* peak_liveness            SPEC cost module    */
+  int64_t flops;            /* flop_count on local shapes                   */
+  int64_t reduction_bytes;  /* comm_cost: sum of all_reduce bytes           */
+  int64_t baseline_bytes;   /* max(1, replicated plan peak) used by reward  */
+  int64_t ar_bytes[PE_MAX_AXES]; /* collective_stats   REF spmd.cc:405-434 */
+  int64_t ag_bytes[PE_MAX_AXES];
+  int32_t ar_cnt[PE_MAX_AXES];
+  int32_t ag_cnt[PE_MAX_AXES];
+  int32_t sbc_cnt[PE_MAX_AXES];
+  int32_t n_spmd_ops;       /* ops in the lowered program (REF spmd.h:67)   */
+  int32_t n_stuck;          /* stuck nodes of the last propagate            */
+  int32_t n_steps;          /* decisions applied (reward's steps term)      */
+  int32_t status;           /* PE_CAND_*                                    */
+  int32_t fail_step;        /* index of the failing action, or -1           */
+  int32_t feasible;         /* peak <= memory budget                        */
+  int32_t reserved;
+  double runtime_s;         /* runtime_estimate                             */
+  double reward;            /* reward in [0,1]                              */
+} pe_result;
+
+/* Cost-model constants (SPEC cost module, defaults at SPEC "Default
+ * CostParams": 16 GiB, 1e14 flop/s, 1e11 B/s, 1e-6 s, w_mem 0.1, w_comm 1.0,
+ * w_steps 0.01). */
+typedef struct pe_cost_params {
+  int64_t memory_budget_bytes;
+  double flops_per_second;
+  double bytes_per_second;
+  double collective_latency_s;
+  double w_mem;
+  double w_comm;
+  double w_steps;
+} pe_cost_params;
+
+/* Search / rollout configuration (SPEC `SearchConfig`). */
+typedef struct pe_search_config {
+  uint32_t auto_axes_mask; /* bit i = mesh axis i may be searched          */
+  uint32_t max_decisions;  /* default 32                                   */
+  uint32_t group_scopes;   /* 1 = worklist entries are scope groups        */
+  uint32_t episodes;       /* MCTS budget                                  */
+  uint64_t seed;
+  double uct_c;            /* default 1.414                                */
+  uint32_t leaf_batch;     /* leaves evaluated per GPU launch              */
+  uint32_t reserved;
+} pe_search_config;
+
+void pe_default_cost_params(pe_cost_params* out);
+void pe_default_search_config(pe_search_config* out);
+
+/* ---- trace layout (parity; identical for engine and oracle) ----
+ * int32 words per candidate:
+ *   [0] words used (negative: buffer too small)
+ *   [1] n_args, then one spec word per SPMD argument (REF spmd.cc:370-391)
+ *   spec word of the returned value
+ *   n_stuck, then (op index, reason) pairs (REF propagate.h:28-38)
+ *   n_ops, then per SPMD op: head, local_bytes lo, hi, spec word of the op's
+ *   final registered DistType, operand buffer indices (arg i -> i, op j -> A+j)
+ * head = kind | (axis+1)<<8 | (dim+1)<<12 | n_operands<<16, kind = REF OpKind
+ * value (ir.h:31-62).  spec word = per dim (axis+1) in 4 bits (dims 0..3 in
+ * bits 0..15) | pending-sum axis mask << 16 | rank << 24.
+ */
+#define PE_TRACE_KIND_ALL_REDUCE 22
+#define PE_TRACE_KIND_ALL_GATHER 23
+#define PE_TRACE_KIND_SLICE_BY_COORD 24
+
+/* ---- graph: parse_program + graph compiler ---- */
+typedef struct pe_graph pe_graph;
+
+/* Replaces `Program parse_program(std::string_view)` (REF parser.h:28):
+ * parses + validates `.pir` text and compiles it into the engine's
+ * structure-of-arrays form.  Only untiled (base-dialect) programs are
+ * accepted as search roots. */
+pe_status pe_graph_create(const char* pir, size_t len, pe_graph** out,
+                          pe_error* err);
+void pe_graph_destroy(pe_graph* g);
+int32_t pe_graph_num_args(const pe_graph* g);
+int32_t pe_graph_num_ops(const pe_graph* g);
+int32_t pe_graph_num_axes(const pe_graph* g);
+int32_t pe_graph_num_operands(const pe_graph* g);
+int64_t pe_graph_axis_size(const pe_graph* g, int32_t axis);
+/* value index of `%name` (args first, then ops), -1 when absent */
+int32_t pe_graph_value_index(const pe_graph* g, const char* name);
+int32_t pe_graph_axis_index(const pe_graph* g, const char* name);
+/* value name into buf; returns length or -1 */
+int32_t pe_graph_value_name(const pe_graph* g, int32_t value, char* buf,
+                            int32_t cap);
+/* value rank and dims */
+int32_t pe_graph_value_shape(const pe_graph* g, int32_t value, int64_t* dims);
+/* scope groups (normalisation SPEC:568) */
+int32_t pe_graph_num_groups(const pe_graph* g);
+int32_t pe_graph_group_size(const pe_graph* g, int32_t group);
+int32_t pe_graph_group_member(const pe_graph* g, int32_t group, int32_t i);
+
+/* ---- engine: one per device ---- */
+typedef struct pe_engine pe_engine;
+
+/* Uploads the compiled graph to HBM and sizes the per-candidate arenas.
+ * Fails with PE_ERR_NO_DEVICE when no CUDA device is present — there is no
+ * CPU fallback. */
+pe_status pe_engine_create(const pe_graph* g, const pe_search_config* cfg,
+                           const pe_cost_params* cp, int32_t device,
+                           pe_engine** out, pe_error* err);
+void pe_engine_destroy(pe_engine* e);
+
+#define PE_MEM_DEVICE 1u /* all array arguments are device pointers      */
+#define PE_SYNC 2u       /* synchronize the stream before returning       */
+
+/* Batched evaluation: for each candidate c, apply
+ * acts[seq_off[c] .. seq_off[c+1]) from the untiled graph — each action is
+ * apply_tile_action (REF rewrite.cc:61) followed by propagate
+ * (REF propagate.cc:459) — then lower_to_spmd (REF spmd.cc:328),
+ * collective_stats (REF spmd.cc:405) and the SPEC cost model.  `trace` may be
+ * NULL; otherwise n_cand * trace_words int32 words.  `stream` is a
+ * cudaStream_t (NULL = legacy default stream). */
+pe_status pe_eval_batch(pe_engine* e, const pe_action* acts,
+                        const uint32_t* seq_off, uint32_t n_cand,
+                        pe_result* out, int32_t* trace, uint32_t trace_words,
+                        uint32_t flags, void* stream, pe_error* err);
+
+/* Leaf-parallel MCTS rollouts (SPEC mcts_search: "uniform-random rollout to
+ * terminal"): candidate c first applies its prefix, records the legal
+ * TileValue ordinals of that state in legal_out (bitmask of
+ * pe_engine_legal_words() uint64 words, may be NULL), then samples actions
+ * with the rollout policy (uniform, Stop weight 2 after the first decision,
+ * at most max_decisions) from a splitmix64 stream seeded with seeds[c], and
+ * scores the terminal state.  acts_out receives prefix + sampled actions
+ * (max_decisions per candidate), n_acts_out the count. */
+pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix,
+                           const uint32_t* prefix_off, const uint64_t* seeds,
+                           uint32_t n_cand, pe_action* acts_out,
+                           uint32_t* n_acts_out, pe_result* out,
+                           uint64_t* legal_out, uint32_t flags, void* stream,
+                           pe_error* err);
+
+/* Number of TileValue ordinals: worklist entries x PE_MAX_RANK x auto axes
+ * (ordinal = (entry*PE_MAX_RANK + dim)*n_auto + auto-axis rank). */
+uint32_t pe_engine_num_ordinals(const pe_engine* e);
+uint32_t pe_engine_legal_words(const pe_engine* e);
+/* decode an ordinal into an action */
+pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ordinal,
+                                   pe_action* out);
+/* replicated plan's peak liveness (reward baseline) */
+int64_t pe_engine_baseline_bytes(const pe_engine* e);
+/* bytes of the per-candidate arena, and candidate slots per launch */
+int64_t pe_engine_arena_bytes(const pe_engine* e);
+uint32_t pe_engine_slots(const pe_engine* e);
+/* kernel launches issued by this engine since creation */
+uint64_t pe_engine_launch_count(const pe_engine* e);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* PE_H_ */

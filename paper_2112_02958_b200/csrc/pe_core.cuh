@@ -1,0 +1,1448 @@
+// pe_core.cuh — per-candidate evaluation core of the engine.
+//
+// One candidate = one action sequence applied to the untiled graph, with
+// `propagate` after every action, then `lower_to_spmd`, `collective_stats`
+// and the SPEC cost model.  This file restates the reference's semantics
+// (REF = /root/reference/proj) over flat, bounded per-candidate arrays so it
+// runs inside a CUDA kernel with no allocation:
+//
+//   * the program is not copied per rewrite (REF rewrite.cc:78,
+//     propagate.cc:461): a candidate owns an arena of value slots, loop
+//     records and a top-level position table;
+//   * `propagate`'s restart-after-every-rewrite loop (REF propagate.cc:465-471)
+//     becomes ONE in-order forward sweep followed by ONE in-order backward
+//     sweep (SURVEY.md Appendix B.2 phase structure; the argument is in
+//     DESIGN.md §3.2), with `count_uses` (REF ir.cc:125-134) maintained
+//     incrementally instead of by whole-program walks;
+//   * lowering (REF spmd.cc:53-403, patch B) walks the same state in the
+//     rewritten op order and accumulates collective bytes, liveness and flops.
+//
+// Compiled for the device by nvcc (the product path).  tests/native builds
+// the same header with g++ purely as a test harness for differential fuzzing
+// against the oracle; the product library never contains a host copy.
+#pragma once
+#include <stdint.h>
+
+#include "pe.h"
+#include "pe_graph_view.h"
+#include "pe_rules.h"
+
+namespace pe {
+
+enum VKind : uint8_t {
+  VK_FREE = 0,
+  VK_ARG,     // function argument
+  VK_TOP,     // original base op still at top level
+  VK_LOOP,    // tile / sum loop result (REF ir.h kTile/kSum)
+  VK_ATOMIC,  // atomic wrap of an argument (REF rewrite.cc:115-137)
+  VK_SLICE,   // slice_axis in a loop body
+  VK_LOCAL,   // per-iteration copy of an original op inside a loop body
+  VK_DEAD     // erased (extended loop's old name, migrated producer)
+};
+
+enum LoopKind : uint8_t { LK_TILE = 0, LK_SUM = 1 };
+
+// stuck reasons (REF propagate.h:28-32)
+enum Reason : int32_t { R_INSUFFICIENT = 0, R_BLOCKED = 1, R_CONFLICT = 2, R_NONE = -1 };
+
+// ---------------------------------------------------------------- arena
+struct Caps {
+  int32_t V;   // value slots
+  int32_t L;   // loop records
+  int32_t FS;  // front stack (arg action loops + atomics)
+  int32_t EM;  // emitted SPMD ops
+  int32_t EO;  // emitted operand references
+};
+
+struct Layout {
+  Caps caps;
+  // byte offsets inside one candidate arena
+  uint64_t vk, vref, vaux, uses, slcnt, bnext, bprev, vpos;
+  uint64_t lo_buf, lo_spec, lo_acq, lo_g;
+  uint64_t opnd, adirect, aslice, awrapped, aspec0, alb0;
+  uint64_t lkind, laxis, ldim, lhead, ltail, lyield, ltype;
+  uint64_t pos, fs, stk, seen;
+  uint64_t em_head, em_ooff, em_lb, em_last, em_opnd, b_gb, b_lb, b_spec, delta;
+  uint64_t bytes;
+};
+
+struct Arena {
+  uint8_t* vk;
+  int32_t *vref, *vaux, *uses, *slcnt, *bnext, *bprev, *vpos;
+  int32_t* lo_buf;
+  uint32_t* lo_spec;
+  uint8_t* lo_acq;
+  int32_t* lo_g;
+  int32_t *opnd, *adirect, *aslice;
+  uint8_t* awrapped;
+  uint32_t* aspec0;
+  int64_t* alb0;
+  uint8_t *lkind, *laxis;
+  int8_t* ldim;
+  int32_t *lhead, *ltail, *lyield, *ltype;
+  int32_t *pos, *fs, *stk;
+  uint8_t* seen;
+  int32_t *em_head, *em_ooff;
+  int64_t* em_lb;
+  int32_t *em_last, *em_opnd;
+  int64_t *b_gb, *b_lb;
+  uint32_t* b_spec;
+  int64_t* delta;
+};
+
+PE_HD uint64_t align8(uint64_t x) { return (x + 7) & ~uint64_t(7); }
+
+// Host-side sizing.  Bounds are structural: every original
+// op is pulled or migrated at most once, every value is tiled at most once.
+inline Layout make_layout(const GraphView& g) {
+  Layout L{};
+  int32_t A = g.A, N = g.N, E = g.E;
+  int32_t K = A + N;               // action loops (each value tiled once)
+  int32_t S = E + K;               // slices
+  L.caps.V = A + N + N + S + K + A + 8;
+  L.caps.L = N + K + 4;
+  L.caps.FS = 2 * A + 4;
+  L.caps.EM = 3 * (N + S) + 2 * L.caps.L + A + 64;
+  L.caps.EO = E + 2 * L.caps.EM + 64;
+  uint64_t o = 0;
+  auto take = [&](uint64_t bytes) {
+    uint64_t at = o;
+    o = align8(o + bytes);
+    return at;
+  };
+  int64_t V = L.caps.V, Lc = L.caps.L, EM = L.caps.EM;
+  L.vk = take(V);
+  L.vref = take(4 * V);
+  L.vaux = take(4 * V);
+  L.uses = take(4 * V);
+  L.slcnt = take(4 * V);
+  L.bnext = take(4 * V);
+  L.bprev = take(4 * V);
+  L.vpos = take(4 * V);
+  L.lo_buf = take(4 * V);
+  L.lo_spec = take(4 * V);
+  L.lo_acq = take(V);
+  L.lo_g = take(16 * V);
+  L.opnd = take(4 * (int64_t)E + 4);
+  L.adirect = take(4 * (int64_t)A + 4);
+  L.aslice = take(4 * (int64_t)A + 4);
+  L.awrapped = take((int64_t)A + 4);
+  L.aspec0 = take(4 * (int64_t)A + 4);
+  L.alb0 = take(8 * (int64_t)A + 8);
+  L.lkind = take(Lc);
+  L.laxis = take(Lc);
+  L.ldim = take(Lc);
+  L.lhead = take(4 * Lc);
+  L.ltail = take(4 * Lc);
+  L.lyield = take(4 * Lc);
+  L.ltype = take(4 * Lc);
+  L.pos = take(8 * (int64_t)N + 8);
+  L.fs = take(4 * (int64_t)L.caps.FS);
+  L.stk = take(8 * (int64_t)N + 8);
+  L.seen = take((int64_t)N + 8);
+  L.em_head = take(4 * EM);
+  L.em_ooff = take(4 * EM + 4);
+  L.em_lb = take(8 * EM);
+  L.em_last = take(4 * EM);
+  L.em_opnd = take(4 * (int64_t)L.caps.EO);
+  L.b_gb = take(8 * (EM + A));
+  L.b_lb = take(8 * (EM + A));
+  L.b_spec = take(4 * (EM + A));
+  L.delta = take(8 * EM + 8);
+  L.bytes = align8(o);
+  return L;
+}
+
+PE_HD Arena carve(const Layout& L, uint8_t* base) {
+  Arena a;
+  a.vk = base + L.vk;
+  a.vref = (int32_t*)(base + L.vref);
+  a.vaux = (int32_t*)(base + L.vaux);
+  a.uses = (int32_t*)(base + L.uses);
+  a.slcnt = (int32_t*)(base + L.slcnt);
+  a.bnext = (int32_t*)(base + L.bnext);
+  a.bprev = (int32_t*)(base + L.bprev);
+  a.vpos = (int32_t*)(base + L.vpos);
+  a.lo_buf = (int32_t*)(base + L.lo_buf);
+  a.lo_spec = (uint32_t*)(base + L.lo_spec);
+  a.lo_acq = base + L.lo_acq;
+  a.lo_g = (int32_t*)(base + L.lo_g);
+  a.opnd = (int32_t*)(base + L.opnd);
+  a.adirect = (int32_t*)(base + L.adirect);
+  a.aslice = (int32_t*)(base + L.aslice);
+  a.awrapped = base + L.awrapped;
+  a.aspec0 = (uint32_t*)(base + L.aspec0);
+  a.alb0 = (int64_t*)(base + L.alb0);
+  a.lkind = base + L.lkind;
+  a.laxis = base + L.laxis;
+  a.ldim = (int8_t*)(base + L.ldim);
+  a.lhead = (int32_t*)(base + L.lhead);
+  a.ltail = (int32_t*)(base + L.ltail);
+  a.lyield = (int32_t*)(base + L.lyield);
+  a.ltype = (int32_t*)(base + L.ltype);
+  a.pos = (int32_t*)(base + L.pos);
+  a.fs = (int32_t*)(base + L.fs);
+  a.stk = (int32_t*)(base + L.stk);
+  a.seen = base + L.seen;
+  a.em_head = (int32_t*)(base + L.em_head);
+  a.em_ooff = (int32_t*)(base + L.em_ooff);
+  a.em_lb = (int64_t*)(base + L.em_lb);
+  a.em_last = (int32_t*)(base + L.em_last);
+  a.em_opnd = (int32_t*)(base + L.em_opnd);
+  a.b_gb = (int64_t*)(base + L.b_gb);
+  a.b_lb = (int64_t*)(base + L.b_lb);
+  a.b_spec = (uint32_t*)(base + L.b_spec);
+  a.delta = (int64_t*)(base + L.delta);
+  return a;
+}
+
+// IEEE double helpers with explicit rounding (no FMA contraction) so the
+// floating-point cost terms match the oracle bit-for-bit.
+#ifdef __CUDA_ARCH__
+PE_HD double dadd(double a, double b) { return __dadd_rn(a, b); }
+PE_HD double dmul(double a, double b) { return __dmul_rn(a, b); }
+PE_HD double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+#else
+PE_HD double dadd(double a, double b) { volatile double r = a + b; return r; }
+PE_HD double dmul(double a, double b) { volatile double r = a * b; return r; }
+PE_HD double ddiv(double a, double b) { volatile double r = a / b; return r; }
+#endif
+
+// Lowered view of one value (REF spmd.cc:42-51 `Lowered`): buffer, spec
+// word, acquired-in-loop mask (loops never nest, so acq is 0 or 1 per dim)
+// and global shape.
+struct Low {
+  int32_t buf;
+  uint32_t spec;
+  uint32_t acq;
+  int32_t g[kMaxRank];
+};
+
+struct Pull {
+  int32_t ok;
+  int32_t reason;
+  int32_t cls;    // class index local to the op
+  int32_t axis;
+  int32_t drive;  // value slot of the driving loop
+};
+
+struct Cand {
+  const GraphView& g;
+  const Caps caps;
+  Arena a;
+  int32_t nslots, nloops, nfs, nem, neo, nstk;
+  int32_t result_ref;
+  int32_t status;
+  int64_t flops;
+  int32_t result_buf;
+
+  PE_HD Cand(const GraphView& gv, const Layout& L, uint8_t* base)
+      : g(gv), caps(L.caps), a(carve(L, base)) {}
+
+  // ------------------------------------------------------------ helpers
+  PE_HD void fail(int32_t st) {
+    if (status == PE_CAND_OK || status == PE_CAND_ILLEGAL) status = st;
+  }
+  PE_HD bool bad() const { return status == PE_CAND_INTERNAL || status == PE_CAND_CAPACITY; }
+  PE_HD int32_t NV() const { return g.A + g.N; }
+  PE_HD int64_t asz(int32_t ax) const { return g.axis_size[ax]; }
+  PE_HD bool is_tile_loop(int32_t v) const {
+    return a.vk[v] == VK_LOOP && a.lkind[a.vref[v]] == LK_TILE;
+  }
+  // original value whose global shape a top-level value carries
+  PE_HD int32_t shape_src(int32_t v) const {
+    uint8_t k = a.vk[v];
+    if (k == VK_LOOP) return a.ltype[a.vref[v]];
+    if (k == VK_ATOMIC) return a.vref[v];
+    return v;  // ARG / TOP
+  }
+  PE_HD int32_t alloc_slot() {
+    if (nslots >= caps.V) {
+      fail(PE_CAND_CAPACITY);
+      return -1;
+    }
+    int32_t s = nslots++;
+    a.slcnt[s] = 0;
+    a.uses[s] = 0;
+    a.bnext[s] = -1;
+    a.bprev[s] = -1;
+    a.vpos[s] = 0;
+    return s;
+  }
+  PE_HD int32_t alloc_loop() {
+    if (nloops >= caps.L) {
+      fail(PE_CAND_CAPACITY);
+      return -1;
+    }
+    int32_t l = nloops++;
+    a.lhead[l] = -1;
+    a.ltail[l] = -1;
+    return l;
+  }
+  PE_HD void body_append(int32_t l, int32_t s) {
+    a.bnext[s] = -1;
+    a.bprev[s] = a.ltail[l];
+    if (a.ltail[l] >= 0) a.bnext[a.ltail[l]] = s;
+    else a.lhead[l] = s;
+    a.ltail[l] = s;
+  }
+  PE_HD void body_insert_before(int32_t l, int32_t at, int32_t s) {
+    int32_t p = a.bprev[at];
+    a.bprev[s] = p;
+    a.bnext[s] = at;
+    a.bprev[at] = s;
+    if (p >= 0) a.bnext[p] = s;
+    else a.lhead[l] = s;
+  }
+  PE_HD void set_pos(int32_t v, int32_t code) {
+    a.vpos[v] = code;
+    if (code >= 0) a.pos[code] = v;
+    else a.fs[-code - 1] = v;
+  }
+  PE_HD void push_front(int32_t v) {
+    if (nfs >= caps.FS) {
+      fail(PE_CAND_CAPACITY);
+      return;
+    }
+    set_pos(v, -(nfs + 1));
+    nfs++;
+  }
+  PE_HD void clear_pos(int32_t v) {
+    int32_t code = a.vpos[v];
+    if (code >= 0) a.pos[code] = -1;
+    else a.fs[-code - 1] = -1;
+  }
+  // REF rewrite.cc:27-38 replace_uses: every operand occurrence of an
+  // original value lives in one of its original operand slots.
+  PE_HD void replace_uses(int32_t v, int32_t t) {
+    for (int32_t i = g.user_off[v]; i < g.user_off[v + 1]; ++i) {
+      int32_t s = g.users[i];
+      if (a.opnd[s] == v) a.opnd[s] = t;
+    }
+    if (result_ref == v) result_ref = t;
+  }
+  PE_HD void slice_created(int32_t u, int32_t d, int32_t axis) {
+    a.slcnt[u]++;
+    if (u < g.A) {
+      int32_t pair = d | (axis << 3);
+      if (a.aslice[u] == -1) a.aslice[u] = pair;
+      else if (a.aslice[u] != pair) a.aslice[u] = -2;
+    }
+  }
+  PE_HD bool is_member(int32_t gc, int32_t k) const {
+    for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m)
+      if ((g.mem[m] >> 2) == k) return true;
+    return false;
+  }
+
+  // ------------------------------------------------------------ init
+  PE_HD void init() {
+    int32_t A = g.A, N = g.N;
+    for (int32_t v = 0; v < A; ++v) {
+      a.vk[v] = VK_ARG;
+      a.vref[v] = v;
+      a.uses[v] = g.init_uses[v];
+      a.slcnt[v] = 0;
+      a.adirect[v] = 0;
+      a.aslice[v] = -1;
+      a.awrapped[v] = 0;
+    }
+    for (int32_t o = 0; o < N; ++o) {
+      int32_t v = A + o;
+      a.vk[v] = VK_TOP;
+      a.vref[v] = o;
+      a.uses[v] = g.init_uses[v];
+      a.slcnt[v] = 0;
+      a.vpos[v] = 2 * o;
+      a.pos[2 * o] = v;
+      a.pos[2 * o + 1] = -1;
+    }
+    for (int32_t s = 0; s < g.E; ++s) a.opnd[s] = g.oopnd[s];
+    nslots = A + N;
+    nloops = 0;
+    nfs = 0;
+    nem = 0;
+    neo = 0;
+    nstk = 0;
+    result_ref = g.result;
+    status = PE_CAND_OK;
+    flops = 0;
+    result_buf = -1;
+  }
+
+  // ------------------------------------------------------------ actions
+  // carries_tiling (REF rewrite.cc:42-51) for an original value at top level
+  PE_HD bool carries(int32_t v) const {
+    if (a.vk[v] == VK_LOOP) return true;
+    if (a.slcnt[v] > 0) return true;
+    return v < g.A && a.awrapped[v];
+  }
+
+  // apply_tile_action (REF rewrite.cc:61-113).  Returns false when illegal
+  // (IllegalActionError); the state is untouched in that case.
+  PE_HD bool apply_tile(int32_t v, int32_t dim, int32_t axis) {
+    if (v < 0 || v >= NV()) return false;
+    uint8_t k = a.vk[v];
+    if (k != VK_ARG && k != VK_TOP && k != VK_LOOP) return false;  // erased: does not exist
+    if (axis < 0 || axis >= g.n_axes) return false;
+    if (dim < 0 || dim >= g.vrank[v]) return false;
+    if (g.shape(v)[dim] % asz(axis) != 0) return false;
+    if (carries(v)) return false;
+    int32_t l = alloc_loop();
+    int32_t ls = alloc_slot();
+    int32_t s = alloc_slot();
+    if (bad()) return false;
+    a.lkind[l] = LK_TILE;
+    a.laxis[l] = (uint8_t)axis;
+    a.ldim[l] = (int8_t)dim;
+    a.ltype[l] = v;
+    a.lyield[l] = s;
+    a.vk[ls] = VK_LOOP;
+    a.vref[ls] = l;
+    a.uses[ls] = a.uses[v];
+    a.vk[s] = VK_SLICE;
+    a.vref[s] = v;
+    a.vaux[s] = dim | (l << 3);
+    a.uses[s] = 1;  // the loop yield
+    body_append(l, s);
+    a.uses[v] = 1;  // the slice
+    slice_created(v, dim, axis);
+    replace_uses(v, ls);
+    if (v < g.A) push_front(ls);
+    else set_pos(ls, 2 * (v - g.A) + 1);
+    return !bad();
+  }
+
+  PE_HD bool apply_action(const pe_action& act) {
+    if (act.kind == PE_ACT_TILE) return apply_tile((int32_t)act.value, act.dim, act.axis);
+    if (act.kind == PE_ACT_TILE_GROUP) {
+      if ((int32_t)act.value >= g.n_groups) return false;
+      int32_t applied = 0;
+      for (int32_t i = g.grp_off[act.value]; i < g.grp_off[act.value + 1]; ++i) {
+        if (apply_tile(g.grp_mem[i], act.dim, act.axis)) ++applied;
+        if (bad()) return false;
+      }
+      return applied > 0;
+    }
+    return false;  // INFER_REST not supported by this engine version
+  }
+
+  // ------------------------------------------------------------ forward
+  // plan_pull (REF propagate.cc:92-144) for a top-level base op.
+  PE_HD Pull plan_pull(int32_t o) const {
+    Pull p;
+    p.ok = 0;
+    p.reason = R_NONE;
+    p.cls = -1;
+    p.axis = -1;
+    p.drive = -1;
+    int32_t base = g.oopnd_off[o], n = g.oopnd_off[o + 1] - base;
+    int32_t cbase = g.ocls_off[o];
+    for (int32_t k = 0; k < n; ++k) {
+      int32_t u = a.opnd[base + k];
+      if (!is_tile_loop(u)) continue;
+      int32_t L = a.vref[u];
+      int32_t c = g.slot_cls[(base + k) * 4 + a.ldim[L]];
+      if (c < 0 || g.cls_role[cbase + c] == kBlocked) {
+        p.reason = R_BLOCKED;
+        return p;
+      }
+      if (p.drive < 0) {
+        p.drive = u;
+        p.cls = c;
+        p.axis = a.laxis[L];
+      }
+    }
+    if (p.drive < 0) return p;
+    for (int32_t k = 0; k < n; ++k) {
+      int32_t u = a.opnd[base + k];
+      if (!is_tile_loop(u)) continue;
+      int32_t L = a.vref[u];
+      if (a.laxis[L] == p.axis && g.slot_cls[(base + k) * 4 + a.ldim[L]] != p.cls) {
+        p.reason = R_CONFLICT;
+        return p;
+      }
+    }
+    int64_t sz = asz(p.axis);
+    int32_t gc = cbase + p.cls;
+    for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
+      int32_t k = g.mem[m] >> 2, d = g.mem[m] & 3;
+      int32_t u = a.opnd[base + k];
+      if (g.shape(shape_src(u))[d] % sz != 0) {
+        p.reason = R_INSUFFICIENT;
+        return p;
+      }
+      if (is_tile_loop(u)) {
+        int32_t L = a.vref[u];
+        bool sa = a.laxis[L] == p.axis, sd = a.ldim[L] == d;
+        if (sa != sd) {
+          p.reason = R_CONFLICT;
+          return p;
+        }
+      }
+    }
+    p.ok = 1;
+    return p;
+  }
+
+  PE_HD bool has_tiled_operand(int32_t o) const {
+    for (int32_t s = g.oopnd_off[o]; s < g.oopnd_off[o + 1]; ++s)
+      if (is_tile_loop(a.opnd[s])) return true;
+    return false;
+  }
+
+  // The rewrite of REF propagate.cc:194-247 (extend a single-use tile loop,
+  // or a fresh tile / sum loop at X's slot) + build_sliced_consumer
+  // (:149-180, slices deduplicated per (operand, dim)).
+  PE_HD void pull(int32_t o, const Pull& p) {
+    int32_t base = g.oopnd_off[o], n = g.oopnd_off[o + 1] - base;
+    int32_t gc = g.ocls_off[o] + p.cls;
+    bool contracting = g.cls_role[gc] == kContract;
+    int32_t rd = g.cls_rdim[gc];
+    int32_t lv0 = p.drive;
+    bool extend = !contracting && a.uses[lv0] == 1;
+    int32_t f = alloc_slot();
+    int32_t l = extend ? a.vref[lv0] : alloc_loop();
+    if (bad()) return;
+    if (!extend) {
+      a.lkind[l] = contracting ? LK_SUM : LK_TILE;
+      a.laxis[l] = (uint8_t)p.axis;
+      a.ldim[l] = (int8_t)(contracting ? -1 : rd);
+    }
+    a.vk[f] = VK_LOCAL;
+    a.vref[f] = o;
+    a.vaux[f] = (contracting ? 0 : rd + 1) | (l << 3);
+    a.uses[f] = 1;  // yielded
+    // slice cache: members of one class reference at most its member count
+    int32_t cache_u[8], cache_d[8], cache_s[8];
+    int32_t nc = 0;
+    for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
+      int32_t k = g.mem[m] >> 2, d = g.mem[m] & 3;
+      int32_t ps = base + k;
+      int32_t u = a.opnd[ps];
+      if (extend && u == lv0) {
+        int32_t y = a.lyield[l];
+        a.opnd[ps] = y;
+        a.uses[lv0]--;
+        a.uses[y]++;
+        continue;
+      }
+      int32_t sl = -1;
+      for (int32_t c = 0; c < nc; ++c)
+        if (cache_u[c] == u && cache_d[c] == d) sl = cache_s[c];
+      if (sl < 0) {
+        // linear search fallback for very wide concatenates
+        for (int32_t q = g.cls_moff[gc]; q < m && sl < 0 && nc >= 8; ++q) {
+          int32_t k2 = g.mem[q] >> 2, d2 = g.mem[q] & 3;
+          int32_t s2 = a.opnd[base + k2];
+          if (d2 == d && a.vk[s2] == VK_SLICE && a.vref[s2] == u &&
+              (a.vaux[s2] >> 3) == l && (a.vaux[s2] & 7) == d)
+            sl = s2;
+        }
+      }
+      if (sl < 0) {
+        sl = alloc_slot();
+        if (bad()) return;
+        a.vk[sl] = VK_SLICE;
+        a.vref[sl] = u;
+        a.vaux[sl] = d | (l << 3);
+        body_append(l, sl);
+        a.uses[u]++;
+        slice_created(u, d, p.axis);
+        if (nc < 8) {
+          cache_u[nc] = u;
+          cache_d[nc] = d;
+          cache_s[nc] = sl;
+          nc++;
+        }
+      }
+      a.opnd[ps] = sl;
+      a.uses[u]--;
+      a.uses[sl]++;
+    }
+    for (int32_t k = 0; k < n; ++k) {
+      int32_t u = a.opnd[base + k];
+      if (a.vk[u] == VK_ARG && !is_member(gc, k)) a.adirect[u]++;
+    }
+    if (extend) a.uses[a.lyield[l]]--;  // old yield is no longer yielded
+    a.lyield[l] = f;
+    body_append(l, f);
+    a.ltype[l] = g.A + o;
+    if (extend) {
+      a.ldim[l] = (int8_t)rd;
+      clear_pos(lv0);
+      a.vk[lv0] = VK_DEAD;
+    }
+    int32_t xv = g.A + o;
+    a.vk[xv] = VK_LOOP;
+    a.vref[xv] = l;
+  }
+
+  PE_HD void forward() {
+    for (int32_t o = 0; o < g.N; ++o) {
+      if (a.vk[g.A + o] != VK_TOP) continue;
+      if (!has_tiled_operand(o)) continue;
+      if (g.orule_err[o]) {
+        fail(PE_CAND_INTERNAL);
+        return;
+      }
+      Pull p = plan_pull(o);
+      if (!p.ok) continue;
+      pull(o, p);
+      if (bad()) return;
+    }
+  }
+
+  // ------------------------------------------------------------ backward
+  // REF propagate.cc:284-375: migrate single-use producers of sliced values
+  // into the consuming loop, visiting loops and their body slices in order.
+  PE_HD void backward_loop(int32_t l) {
+    int32_t sz_axis = a.laxis[l];
+    int64_t sz = asz(sz_axis);
+    int32_t s = a.lhead[l];
+    while (s >= 0) {
+      int32_t next = a.bnext[s];
+      if (a.vk[s] == VK_SLICE) {
+        int32_t u = a.vref[s];
+        int32_t d = a.vaux[s] & 7;
+        if (a.vk[u] == VK_TOP && a.uses[u] == 1) {
+          int32_t P = a.vref[u];
+          uint8_t kind = g.okind[P];
+          int32_t pb = g.oopnd_off[P], pn = g.oopnd_off[P + 1] - pb;
+          bool simple = kind == kConstant ||
+                        (kind == kBroadcastInDim && !((g.omask[P] >> d) & 1));
+          bool go = true;
+          int32_t first_new = -1;
+          int32_t gc = -1;
+          if (!simple) {
+            if (g.orule_err[P]) {
+              fail(PE_CAND_INTERNAL);
+              return;
+            }
+            int32_t rc = g.op_rcls[P * 4 + d];
+            if (rc < 0) {
+              go = false;
+            } else {
+              gc = g.ocls_off[P] + rc;
+              for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
+                int32_t k = g.mem[m] >> 2, dd = g.mem[m] & 3;
+                int32_t w = a.opnd[pb + k];
+                if (g.shape(shape_src(w))[dd] % sz != 0) go = false;
+                if (is_tile_loop(w)) {
+                  int32_t L2 = a.vref[w];
+                  bool sa = a.laxis[L2] == sz_axis, sd = a.ldim[L2] == dd;
+                  if (sa != sd) go = false;
+                }
+              }
+            }
+          }
+          if (go) {
+            if (!simple) {
+              int32_t cache_u[8], cache_d[8], cache_s[8];
+              int32_t nc = 0;
+              for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
+                int32_t k = g.mem[m] >> 2, dd = g.mem[m] & 3;
+                int32_t w = a.opnd[pb + k];
+                int32_t sl = -1;
+                for (int32_t c = 0; c < nc; ++c)
+                  if (cache_u[c] == w && cache_d[c] == dd) sl = cache_s[c];
+                if (sl < 0 && nc >= 8) {
+                  for (int32_t q = g.cls_moff[gc]; q < m && sl < 0; ++q) {
+                    int32_t k2 = g.mem[q] >> 2, d2 = g.mem[q] & 3;
+                    int32_t s2 = a.opnd[pb + k2];
+                    if (d2 == dd && a.vk[s2] == VK_SLICE && a.vref[s2] == w &&
+                        (a.vaux[s2] >> 3) == l)
+                      sl = s2;
+                  }
+                }
+                if (sl < 0) {
+                  sl = alloc_slot();
+                  if (bad()) return;
+                  a.vk[sl] = VK_SLICE;
+                  a.vref[sl] = w;
+                  a.vaux[sl] = dd | (l << 3);
+                  body_insert_before(l, s, sl);
+                  a.uses[w]++;
+                  slice_created(w, dd, sz_axis);
+                  if (first_new < 0) first_new = sl;
+                  if (nc < 8) {
+                    cache_u[nc] = w;
+                    cache_d[nc] = dd;
+                    cache_s[nc] = sl;
+                    nc++;
+                  }
+                }
+                a.opnd[pb + k] = sl;
+                a.uses[w]--;
+                a.uses[sl]++;
+              }
+            }
+            for (int32_t k = 0; k < pn; ++k) {
+              int32_t w = a.opnd[pb + k];
+              if (a.vk[w] == VK_ARG && (simple || !is_member(gc, k))) a.adirect[w]++;
+            }
+            // the slice becomes P's per-iteration copy (it keeps S's name)
+            a.vk[s] = VK_LOCAL;
+            a.vref[s] = P;
+            a.vaux[s] = (d + 1) | (l << 3);
+            a.slcnt[u]--;
+            clear_pos(u);
+            a.vk[u] = VK_DEAD;
+            next = first_new >= 0 ? first_new : a.bnext[s];
+          }
+        }
+      }
+      s = next;
+    }
+  }
+
+  template <typename F>
+  PE_HD void for_top(F&& f) {
+    for (int32_t i = nfs - 1; i >= 0; --i) {
+      int32_t v = a.fs[i];
+      if (v >= 0) {
+        f(v);
+        if (bad()) return;
+      }
+    }
+    for (int32_t p = 0; p < 2 * g.N; ++p) {
+      int32_t v = a.pos[p];
+      if (v >= 0) {
+        f(v);
+        if (bad()) return;
+      }
+    }
+  }
+
+  PE_HD void backward() {
+    for_top([&](int32_t v) {
+      if (a.vk[v] == VK_LOOP) backward_loop(a.vref[v]);
+    });
+  }
+
+  // wrap_replicated_args (REF propagate.cc:385-408): arguments used directly
+  // inside a loop and never sliced are wrapped atomic, each at index 0.
+  PE_HD void wrap() {
+    for (int32_t x = 0; x < g.A; ++x) {
+      if (a.adirect[x] == 0 || a.slcnt[x] != 0 || a.awrapped[x]) continue;
+      int32_t t = alloc_slot();
+      if (bad()) return;
+      a.vk[t] = VK_ATOMIC;
+      a.vref[t] = x;
+      a.uses[t] = a.uses[x];
+      replace_uses(x, t);
+      a.uses[x] = 1;
+      a.awrapped[x] = 1;
+      push_front(t);
+      if (bad()) return;
+    }
+  }
+
+  PE_HD void propagate() {
+    forward();
+    if (bad()) return;
+    backward();
+    if (bad()) return;
+    wrap();
+  }
+
+  // stuck analysis (REF propagate.cc:412-454), dedup by op id in discovery
+  // order (:477-479).
+  PE_HD void add_stuck(int32_t o, int32_t r) {
+    if (a.seen[o]) return;
+    a.seen[o] = 1;
+    a.stk[2 * nstk] = o;
+    a.stk[2 * nstk + 1] = r;
+    nstk++;
+  }
+  PE_HD void analyze() {
+    for (int32_t o = 0; o < g.N; ++o) a.seen[o] = 0;
+    nstk = 0;
+    for_top([&](int32_t v) {
+      uint8_t k = a.vk[v];
+      if (k == VK_LOOP) {
+        int32_t l = a.vref[v];
+        for (int32_t s = a.lhead[l]; s >= 0; s = a.bnext[s]) {
+          if (a.vk[s] != VK_SLICE) continue;
+          int32_t u = a.vref[s], d = a.vaux[s] & 7;
+          if (a.vk[u] != VK_TOP) continue;
+          int32_t P = a.vref[u];
+          uint8_t kind = g.okind[P];
+          if (kind == kConstant) continue;
+          if (a.uses[u] != 1) continue;
+          if (kind == kBroadcastInDim && !((g.omask[P] >> d) & 1)) continue;
+          if (g.orule_err[P]) {
+            fail(PE_CAND_INTERNAL);
+            return;
+          }
+          if (g.op_rcls[P * 4 + d] < 0) add_stuck(P, R_BLOCKED);
+        }
+      } else if (k == VK_TOP) {
+        int32_t o = a.vref[v];
+        if (!has_tiled_operand(o)) return;
+        if (g.orule_err[o]) {
+          fail(PE_CAND_INTERNAL);
+          return;
+        }
+        Pull p = plan_pull(o);
+        if (p.ok) {
+          fail(PE_CAND_INTERNAL);  // "pull available after fixpoint"
+          return;
+        }
+        add_stuck(o, p.reason);
+      }
+    });
+  }
+
+  // ------------------------------------------------------------ lowering
+  PE_HD int32_t rank_of_spec(uint32_t spec) const { return (spec >> 24) & 7; }
+  PE_HD int64_t local_dim(const Low& w, int d) {
+    uint32_t ax1 = spec_axis(w.spec, d);
+    if (!ax1) return w.g[d];
+    int64_t s = asz(ax1 - 1);
+    if (w.g[d] % s != 0) {
+      fail(PE_CAND_INTERNAL);  // local_shape divisibility (REF mesh.cc:117-122)
+      return 1;
+    }
+    return w.g[d] / s;
+  }
+  PE_HD int64_t local_elems(const Low& w) {
+    int64_t e = 1;
+    int r = rank_of_spec(w.spec);
+    for (int d = 0; d < r; ++d) e *= local_dim(w, d);
+    return e;
+  }
+  PE_HD int64_t global_bytes(const Low& w) const {
+    int64_t e = 4;
+    int r = rank_of_spec(w.spec);
+    for (int d = 0; d < r; ++d) e *= w.g[d];
+    return e;
+  }
+  PE_HD Low load(int32_t v) const {
+    Low w;
+    w.buf = a.lo_buf[v];
+    w.spec = a.lo_spec[v];
+    w.acq = a.lo_acq[v];
+    for (int d = 0; d < kMaxRank; ++d) w.g[d] = a.lo_g[4 * v + d];
+    return w;
+  }
+  PE_HD void store(int32_t v, const Low& w) {
+    a.lo_buf[v] = w.buf;
+    a.lo_spec[v] = w.spec;
+    a.lo_acq[v] = (uint8_t)w.acq;
+    for (int d = 0; d < kMaxRank; ++d) a.lo_g[4 * v + d] = w.g[d];
+  }
+  PE_HD void register_type(int32_t buf, const Low& w) {
+    a.b_gb[buf] = global_bytes(w);
+    a.b_lb[buf] = 4 * local_elems(w);
+    a.b_spec[buf] = w.spec;
+  }
+  // opens an SPMD op; operands appended with add_operand
+  PE_HD int32_t new_op(int32_t kind, int32_t axis, int32_t dim, int32_t nopnd) {
+    if (nem >= caps.EM || neo + nopnd > caps.EO) {
+      fail(PE_CAND_CAPACITY);
+      return -1;
+    }
+    int32_t j = nem++;
+    a.em_head[j] = kind | ((axis + 1) << 8) | ((dim + 1) << 12) | (nopnd << 16);
+    a.em_ooff[j] = neo;
+    a.em_last[j] = j;
+    return j;
+  }
+  PE_HD void add_operand(int32_t j, int32_t buf) {
+    a.em_opnd[neo++] = buf;
+    if (buf >= g.A) {
+      int32_t jj = buf - g.A;
+      if (a.em_last[jj] < j) a.em_last[jj] = j;
+    }
+  }
+  PE_HD int32_t pending_front(uint32_t spec) const {
+    uint32_t pm = spec_pending(spec);
+    int32_t best = -1;
+    for (int32_t ax = 0; ax < g.n_axes; ++ax)
+      if ((pm >> ax) & 1)
+        if (best < 0 || g.axis_name_rank[ax] < g.axis_name_rank[best]) best = ax;
+    return best;
+  }
+  // emit_gather (REF spmd.cc:85-99): updates the record in place
+  PE_HD void emit_gather(Low& w, int d) {
+    int32_t ax = (int32_t)spec_axis(w.spec, d) - 1;
+    int32_t j = new_op(kAllGather, ax, d, 1);
+    if (j < 0) return;
+    add_operand(j, w.buf);
+    w.spec = spec_set_axis(w.spec, d, 0);
+    w.acq &= ~(1u << d);
+    a.em_lb[j] = 4 * local_elems(w);
+    w.buf = g.A + j;
+    register_type(w.buf, w);
+  }
+  // emit_all_reduce (REF spmd.cc:102-114)
+  PE_HD void emit_all_reduce(Low& w, int32_t ax) {
+    int32_t j = new_op(kAllReduce, ax, -1, 1);
+    if (j < 0) return;
+    add_operand(j, w.buf);
+    w.spec &= ~(1u << (16 + ax));
+    a.em_lb[j] = 4 * local_elems(w);
+    w.buf = g.A + j;
+    register_type(w.buf, w);
+  }
+  // materialize_for_direct_use (REF spmd.cc:119-129); loop_axis = -1 at top
+  PE_HD void materialize(int32_t v, int32_t loop_axis) {
+    Low w = load(v);
+    int r = rank_of_spec(w.spec);
+    for (int d = 0; d < r; ++d) {
+      uint32_t ax1 = spec_axis(w.spec, d);
+      if (!ax1) continue;
+      bool live = loop_axis >= 0 && (int32_t)ax1 - 1 == loop_axis && ((w.acq >> d) & 1);
+      if (!live) emit_gather(w, d);
+      if (bad()) return;
+    }
+    while (spec_pending(w.spec)) {
+      emit_all_reduce(w, pending_front(w.spec));
+      if (bad()) return;
+    }
+    store(v, w);
+  }
+
+  // lower_base (REF spmd.cc:256-323 with patch B) for a top-level op
+  // (l = -1) or a per-iteration copy in loop l.
+  PE_HD void lower_base(int32_t v, int32_t o, int32_t l) {
+    int32_t base = g.oopnd_off[o], n = g.oopnd_off[o + 1] - base;
+    int32_t lax = l >= 0 ? (int32_t)a.laxis[l] : -1;
+    uint8_t kind = g.okind[o];
+    for (int32_t k = 0; k < n; ++k) {
+      materialize(a.opnd[base + k], lax);
+      if (bad()) return;
+    }
+    Low r;
+    int32_t xv = g.A + o;
+    int rank = g.vrank[xv];
+    for (int d = 0; d < kMaxRank; ++d) r.g[d] = g.shape(xv)[d];
+    if (l >= 0) {
+      int32_t dd = (a.vaux[v] & 7) - 1;
+      if (dd >= 0) r.g[dd] = (int32_t)(r.g[dd] / asz(lax));
+    }
+    r.spec = (uint32_t)rank << 24;
+    r.acq = 0;
+    r.buf = -1;
+    for (int32_t k = 0; k < n; ++k) r.spec |= spec_pending(a.lo_spec[a.opnd[base + k]]) << 16;
+    if (kind != kConstant) {
+      for (int32_t k = 0; k < n; ++k) {
+        Low w = load(a.opnd[base + k]);
+        int wr = rank_of_spec(w.spec);
+        bool any = false;
+        for (int d = 0; d < wr; ++d) any |= spec_axis(w.spec, d) != 0;
+        if (!any) continue;
+        ReshapeRule rr;
+        if (kind == kReshape) {
+          int64_t in[kMaxRank];
+          for (int d = 0; d < wr; ++d) in[d] = local_dim(w, d);
+          rr = reshape_rule(in, wr, r.g, rank);
+          if (rr.error) {
+            fail(PE_CAND_INTERNAL);
+            return;
+          }
+        }
+        for (int d = 0; d < wr; ++d) {
+          uint32_t ax1 = spec_axis(w.spec, d);
+          if (!ax1) continue;
+          int role, rdim;
+          if (kind == kReshape) {
+            int c = rr.cls_of_dim[d];
+            if (c < 0) {
+              fail(PE_CAND_INTERNAL);
+              return;
+            }
+            role = rr.role[c];
+            rdim = rr.rdim[c];
+          } else {
+            int c = g.slot_cls[(base + k) * 4 + d];
+            if (c < 0) {
+              fail(PE_CAND_INTERNAL);
+              return;
+            }
+            role = g.cls_role[g.ocls_off[o] + c];
+            rdim = g.cls_rdim[g.ocls_off[o] + c];
+          }
+          if (role == kPass) {
+            uint32_t cur = spec_axis(r.spec, rdim);
+            if (cur && cur != ax1) {
+              fail(PE_CAND_INTERNAL);
+              return;
+            }
+            r.spec = spec_set_axis(r.spec, rdim, ax1);
+            r.acq = (r.acq & ~(1u << rdim)) | (((w.acq >> d) & 1) << rdim);
+          } else if (role == kBlocked) {
+            fail(PE_CAND_INTERNAL);
+            return;
+          }
+        }
+      }
+    }
+    for (int d = 0; d < rank; ++d) {
+      uint32_t ax1 = spec_axis(r.spec, d);
+      if (ax1) r.g[d] = (int32_t)(r.g[d] * asz(ax1 - 1));
+    }
+    int32_t j = new_op(kind, -1, -1, n);
+    if (j < 0) return;
+    for (int32_t k = 0; k < n; ++k) add_operand(j, a.lo_buf[a.opnd[base + k]]);
+    int64_t out_elems = local_elems(r);
+    a.em_lb[j] = 4 * out_elems;
+    // flops on LOCAL operand shapes
+    switch (kind) {
+      case kDot: {
+        Low lw = load(a.opnd[base]);
+        Low rw = load(a.opnd[base + 1]);
+        int64_t f = 2 * local_elems(lw);
+        int rr2 = rank_of_spec(rw.spec);
+        for (int d = 0; d < rr2; ++d)
+          if ((g.omask[o] >> d) & 1) f *= local_dim(rw, d);
+        flops += f;
+        break;
+      }
+      case kAdd: case kSub: case kMul: case kDiv: case kMaximum:
+      case kNeg: case kExp: case kTanh: case kRsqrt:
+        flops += out_elems;
+        break;
+      case kReduceSum: case kReduceMax:
+        flops += local_elems(load(a.opnd[base]));
+        break;
+      default:
+        break;
+    }
+    r.buf = g.A + j;
+    register_type(r.buf, r);
+    store(v, r);
+  }
+
+  // lower_slice_axis (REF spmd.cc:206-254)
+  PE_HD void lower_slice(int32_t s, int32_t l) {
+    int32_t lax = a.laxis[l];
+    int32_t u = a.vref[s];
+    int d = a.vaux[s] & 7;
+    Low src = load(u);
+    if ((int32_t)spec_axis(src.spec, d) == lax + 1) {
+      Low r = src;
+      r.acq |= 1u << d;
+      store(s, r);
+      return;
+    }
+    if (spec_axis(src.spec, d) != 0) {
+      emit_gather(src, d);
+      if (bad()) return;
+    }
+    int rk = rank_of_spec(src.spec);
+    for (int d2 = 0; d2 < rk; ++d2) {
+      if ((int32_t)spec_axis(src.spec, d2) != lax + 1) continue;
+      if ((src.acq >> d2) & 1) {
+        fail(PE_CAND_INTERNAL);
+        return;
+      }
+      emit_gather(src, d2);
+      if (bad()) return;
+    }
+    store(u, src);
+    int32_t j = new_op(kSliceByCoord, lax, d, 1);
+    if (j < 0) return;
+    add_operand(j, src.buf);
+    Low r = src;
+    r.spec = spec_set_axis(r.spec, d, (uint32_t)(lax + 1));
+    r.acq |= 1u << d;
+    a.em_lb[j] = 4 * local_elems(r);
+    r.buf = g.A + j;
+    register_type(r.buf, r);
+    store(s, r);
+  }
+
+  PE_HD bool has_axis(uint32_t spec, int32_t ax) const {
+    if ((spec_pending(spec) >> ax) & 1) return true;
+    int r = rank_of_spec(spec);
+    for (int d = 0; d < r; ++d)
+      if ((int32_t)spec_axis(spec, d) == ax + 1) return true;
+    return false;
+  }
+
+  // lower_loop (REF spmd.cc:157-204)
+  PE_HD void lower_loop(int32_t v) {
+    int32_t l = a.vref[v];
+    int32_t lax = a.laxis[l];
+    for (int32_t s = a.lhead[l]; s >= 0; s = a.bnext[s]) {
+      if (a.vk[s] == VK_SLICE) lower_slice(s, l);
+      else lower_base(s, a.vref[s], l);
+      if (bad()) return;
+    }
+    Low yv = load(a.lyield[l]);
+    int32_t lt = a.ltype[l];
+    if (a.lkind[l] == LK_TILE) {
+      if (spec_pending(yv.spec)) {
+        fail(PE_CAND_INTERNAL);
+        return;
+      }
+      Low r = yv;
+      int dim = a.ldim[l];
+      uint32_t have = spec_axis(r.spec, dim);
+      if ((int32_t)have == lax + 1) {
+        r.acq &= ~(1u << dim);
+      } else if (have == 0 && !has_axis(r.spec, lax)) {
+        r.spec = spec_set_axis(r.spec, dim, (uint32_t)(lax + 1));
+        r.acq &= ~(1u << dim);
+      } else {
+        fail(PE_CAND_INTERNAL);
+        return;
+      }
+      for (int d = 0; d < kMaxRank; ++d) r.g[d] = g.shape(lt)[d];
+      int rk = rank_of_spec(r.spec);
+      for (int d = 0; d < rk; ++d)
+        if (local_dim(r, d) != local_dim(yv, d)) {
+          fail(PE_CAND_INTERNAL);
+          return;
+        }
+      if (bad()) return;
+      store(v, r);
+      register_type(r.buf, r);
+    } else {
+      Low w = yv;
+      w.spec |= 1u << (16 + lax);
+      int rk = rank_of_spec(w.spec);
+      for (int d = 0; d < rk; ++d)
+        if ((int32_t)spec_axis(w.spec, d) == lax + 1) {
+          w.spec = spec_set_axis(w.spec, d, 0);
+          w.acq &= ~(1u << d);
+        }
+      for (int d = 0; d < kMaxRank; ++d) w.g[d] = g.shape(lt)[d];
+      register_type(w.buf, w);
+      emit_all_reduce(w, lax);
+      if (bad()) return;
+      store(v, w);
+    }
+  }
+
+  // lower_to_spmd (REF spmd.cc:328-403)
+  PE_HD void lower() {
+    nem = 0;
+    neo = 0;
+    flops = 0;
+    for (int32_t x = 0; x < g.A; ++x) {
+      Low w;
+      int rank = g.vrank[x];
+      for (int d = 0; d < kMaxRank; ++d) w.g[d] = g.shape(x)[d];
+      w.spec = (uint32_t)rank << 24;
+      w.acq = 0;
+      w.buf = x;
+      int32_t direct = a.uses[x] - a.slcnt[x] - (result_ref == x ? 1 : 0);
+      if (direct == 0 && a.aslice[x] >= 0) {
+        int d = a.aslice[x] & 7, ax = a.aslice[x] >> 3;
+        if (w.g[d] % asz(ax) == 0) w.spec = spec_set_axis(w.spec, d, (uint32_t)(ax + 1));
+      }
+      store(x, w);
+      register_type(x, w);
+      a.aspec0[x] = w.spec;
+      a.alb0[x] = 4 * local_elems(w);
+    }
+    for_top([&](int32_t v) {
+      uint8_t k = a.vk[v];
+      if (k == VK_TOP) {
+        lower_base(v, a.vref[v], -1);
+      } else if (k == VK_ATOMIC) {
+        Low w = load(a.vref[v]);
+        int r = rank_of_spec(w.spec);
+        bool rep = spec_pending(w.spec) == 0;
+        for (int d = 0; d < r; ++d) rep = rep && spec_axis(w.spec, d) == 0;
+        if (!rep) {
+          fail(PE_CAND_INTERNAL);
+          return;
+        }
+        store(v, w);
+      } else if (k == VK_LOOP) {
+        lower_loop(v);
+      }
+    });
+    if (bad()) return;
+    Low res = load(result_ref);
+    while (spec_pending(res.spec)) {
+      emit_all_reduce(res, pending_front(res.spec));
+      if (bad()) return;
+    }
+    store(result_ref, res);
+    result_buf = res.buf;
+  }
+
+  // ------------------------------------------------------------ scoring
+  PE_HD void score(const pe_cost_params& cp, int64_t baseline, int32_t steps,
+                   pe_result& r) {
+    for (int x = 0; x < PE_MAX_AXES; ++x) {
+      r.ar_bytes[x] = 0;
+      r.ag_bytes[x] = 0;
+      r.ar_cnt[x] = 0;
+      r.ag_cnt[x] = 0;
+      r.sbc_cnt[x] = 0;
+    }
+    // collective_stats (REF spmd.cc:405-434) over final registered types
+    for (int32_t j = 0; j < nem; ++j) {
+      int32_t h = a.em_head[j];
+      int32_t kind = h & 0xFF, ax = ((h >> 8) & 0xF) - 1;
+      if (kind == kAllReduce) {
+        int32_t b = a.em_opnd[a.em_ooff[j]];
+        r.ar_cnt[ax]++;
+        r.ar_bytes[ax] += a.b_gb[b];
+      } else if (kind == kAllGather) {
+        int32_t b = a.em_opnd[a.em_ooff[j]];
+        r.ag_cnt[ax]++;
+        r.ag_bytes[ax] += a.b_lb[b] * (asz(ax) - 1);
+      } else if (kind == kSliceByCoord) {
+        r.sbc_cnt[ax]++;
+      }
+    }
+    // peak liveness
+    int64_t base = 0;
+    for (int32_t x = 0; x < g.A; ++x) base += a.alb0[x];
+    if (result_buf >= g.A) a.em_last[result_buf - g.A] = nem - 1;
+    for (int32_t j = 0; j <= nem; ++j) a.delta[j] = 0;
+    for (int32_t j = 0; j < nem; ++j) {
+      a.delta[j] += a.em_lb[j];
+      a.delta[a.em_last[j] + 1] -= a.em_lb[j];
+    }
+    int64_t run = 0, best = 0;
+    for (int32_t j = 0; j < nem; ++j) {
+      run += a.delta[j];
+      if (run > best) best = run;
+    }
+    r.peak_bytes = base + best;
+    r.flops = flops;
+    r.n_spmd_ops = nem;
+    r.n_steps = steps;
+    int64_t ar = 0, ag = 0, arc = 0, agc = 0;
+    for (int x = 0; x < PE_MAX_AXES; ++x) {
+      ar += r.ar_bytes[x];
+      ag += r.ag_bytes[x];
+      arc += r.ar_cnt[x];
+      agc += r.ag_cnt[x];
+    }
+    r.reduction_bytes = ar;
+    r.baseline_bytes = baseline;
+    double rt = ddiv((double)flops, cp.flops_per_second);
+    rt = dadd(rt, ddiv((double)(ar + ag), cp.bytes_per_second));
+    rt = dadd(rt, dmul(cp.collective_latency_s, (double)(arc + agc)));
+    r.runtime_s = rt;
+    r.feasible = r.peak_bytes <= cp.memory_budget_bytes ? 1 : 0;
+    if (!r.feasible) {
+      r.reward = 0.0;
+    } else {
+      double d = 1.0;
+      d = dadd(d, dmul(cp.w_comm, ddiv((double)ar, (double)baseline)));
+      d = dadd(d, dmul(cp.w_mem, ddiv((double)r.peak_bytes, (double)cp.memory_budget_bytes)));
+      d = dadd(d, dmul(cp.w_steps, (double)steps));
+      r.reward = ddiv(1.0, d);
+    }
+  }
+
+  // parity trace (pe.h layout)
+  PE_HD void write_trace(int32_t* t, uint32_t cap) {
+    uint32_t n = 1;
+    bool over = false;
+    auto put = [&](int64_t v) {
+      if (n < cap) t[n] = (int32_t)v;
+      else over = true;
+      ++n;
+    };
+    put(g.A);
+    for (int32_t x = 0; x < g.A; ++x) put(a.aspec0[x]);
+    put(a.b_spec[result_buf]);
+    put(nstk);
+    for (int32_t i = 0; i < nstk; ++i) {
+      put(a.stk[2 * i]);
+      put(a.stk[2 * i + 1]);
+    }
+    put(nem);
+    for (int32_t j = 0; j < nem; ++j) {
+      int32_t h = a.em_head[j];
+      put(h);
+      put(a.em_lb[j] & 0xffffffff);
+      put(a.em_lb[j] >> 32);
+      put(a.b_spec[g.A + j]);
+      int32_t no = (h >> 16) & 0xFFFF;
+      for (int32_t q = 0; q < no; ++q) put(a.em_opnd[a.em_ooff[j] + q]);
+    }
+    if (cap > 0) t[0] = over ? -(int32_t)n : (int32_t)n;
+  }
+
+  // ------------------------------------------------------------ drivers
+  PE_HD void finish(const pe_cost_params& cp, int64_t baseline, int32_t steps,
+                    bool propagated, pe_result& r, int32_t* trace, uint32_t trace_words) {
+    if (!bad() && propagated) analyze();
+    if (!bad()) lower();
+    if (bad()) {
+      int32_t st = status;
+      for (int x = 0; x < PE_MAX_AXES; ++x) {
+        r.ar_bytes[x] = r.ag_bytes[x] = 0;
+        r.ar_cnt[x] = r.ag_cnt[x] = r.sbc_cnt[x] = 0;
+      }
+      r.peak_bytes = r.flops = r.reduction_bytes = r.baseline_bytes = 0;
+      r.n_spmd_ops = 0;
+      r.n_stuck = 0;
+      r.feasible = 0;
+      r.runtime_s = 0;
+      r.reward = 0;
+      r.n_steps = steps;
+      r.status = st;
+      r.fail_step = steps;
+      if (trace && trace_words) trace[0] = 0;
+      return;
+    }
+    int32_t fs = r.fail_step;
+    score(cp, baseline, steps, r);
+    r.n_stuck = propagated ? nstk : 0;
+    r.status = status;
+    r.fail_step = fs;
+    if (trace && trace_words) write_trace(trace, trace_words);
+  }
+
+  PE_HD void eval(const pe_action* acts, int32_t n, const pe_cost_params& cp,
+                  int64_t baseline, pe_result& r, int32_t* trace, uint32_t trace_words) {
+    init();
+    r.fail_step = -1;
+    r.reserved = 0;
+    int32_t steps = 0;
+    bool propagated = false;
+    for (int32_t k = 0; k < n; ++k) {
+      if (acts[k].kind == PE_ACT_STOP) break;
+      bool ok = apply_action(acts[k]);
+      if (bad()) break;
+      if (!ok) {
+        status = PE_CAND_ILLEGAL;
+        r.fail_step = k;
+        break;
+      }
+      propagate();
+      propagated = true;
+      if (bad()) break;
+      ++steps;
+    }
+    finish(cp, baseline, steps, propagated, r, trace, trace_words);
+  }
+
+  // ------------------------------------------------------------ rollouts
+  PE_HD bool member_legal(int32_t m, int32_t d, int32_t ax) const {
+    if (d >= g.vrank[m]) return false;
+    if (g.shape(m)[d] % asz(ax) != 0) return false;
+    return !(a.slcnt[m] > 0 || a.awrapped[m]);
+  }
+  PE_HD bool ordinal_legal(int32_t e, int32_t d, int32_t ax) const {
+    for (int32_t i = g.ent_off[e]; i < g.ent_off[e + 1]; ++i)
+      if (member_legal(g.ent_mem[i], d, ax)) return true;
+    return false;
+  }
+  PE_HD int32_t count_legal() const {
+    int32_t c = 0;
+    for (int32_t e = 0; e < g.n_entries; ++e)
+      for (int32_t d = 0; d < kMaxRank; ++d)
+        for (int32_t ai = 0; ai < g.n_auto; ++ai)
+          if (ordinal_legal(e, d, g.auto_axes[ai])) ++c;
+    return c;
+  }
+  PE_HD pe_action ordinal_action(int32_t ord) const {
+    pe_action x;
+    int32_t na = g.n_auto;
+    int32_t ai = ord % na, d = (ord / na) % kMaxRank, e = ord / na / kMaxRank;
+    x.axis = (uint8_t)g.auto_axes[ai];
+    x.dim = (uint8_t)d;
+    x.pad = 0;
+    if (g.entries_are_groups) {
+      x.kind = PE_ACT_TILE_GROUP;
+      x.value = (uint32_t)e;
+    } else {
+      x.kind = PE_ACT_TILE;
+      x.value = (uint32_t)g.ent_mem[g.ent_off[e]];
+    }
+    return x;
+  }
+  // the pick-th legal ordinal
+  PE_HD int32_t nth_legal(int32_t pick) const {
+    int32_t c = 0;
+    for (int32_t e = 0; e < g.n_entries; ++e)
+      for (int32_t d = 0; d < kMaxRank; ++d)
+        for (int32_t ai = 0; ai < g.n_auto; ++ai)
+          if (ordinal_legal(e, d, g.auto_axes[ai])) {
+            if (c == pick) return (e * kMaxRank + d) * g.n_auto + ai;
+            ++c;
+          }
+    return -1;
+  }
+  PE_HD static uint64_t splitmix(uint64_t& st) {
+    st += 0x9E3779B97F4A7C15ull;
+    uint64_t z = st;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+
+  PE_HD void rollout(const pe_action* prefix, int32_t np, uint64_t seed, int32_t maxd,
+                     const pe_cost_params& cp, int64_t baseline, pe_action* acts_out,
+                     uint32_t* n_out, pe_result& r, uint64_t* legal_out, int32_t legal_words) {
+    init();
+    r.fail_step = -1;
+    r.reserved = 0;
+    int32_t steps = 0, nacts = 0;
+    bool propagated = false, terminal = false;
+    if (legal_out)
+      for (int32_t w = 0; w < legal_words; ++w) legal_out[w] = 0;
+    for (int32_t k = 0; k < np; ++k) {
+      if (prefix[k].kind == PE_ACT_STOP) {
+        terminal = true;
+        break;
+      }
+      bool ok = apply_action(prefix[k]);
+      if (bad()) break;
+      if (!ok) {
+        status = PE_CAND_ILLEGAL;
+        r.fail_step = k;
+        terminal = true;
+        break;
+      }
+      propagate();
+      propagated = true;
+      if (bad()) break;
+      if (nacts < maxd) acts_out[nacts] = prefix[k];
+      ++nacts;
+      ++steps;
+    }
+    if (!bad() && status == PE_CAND_OK) {
+      if (legal_out) {
+        for (int32_t e = 0; e < g.n_entries; ++e)
+          for (int32_t d = 0; d < kMaxRank; ++d)
+            for (int32_t ai = 0; ai < g.n_auto; ++ai)
+              if (ordinal_legal(e, d, g.auto_axes[ai])) {
+                int32_t o = (e * kMaxRank + d) * g.n_auto + ai;
+                legal_out[o >> 6] |= 1ull << (o & 63);
+              }
+      }
+      uint64_t st = seed;
+      while (!terminal) {
+        if (steps >= maxd) break;
+        int32_t nl = count_legal();
+        if (nl == 0) break;
+        uint64_t ws = steps >= 1 ? 2 : 1;
+        uint64_t pick = splitmix(st) % ((uint64_t)nl + ws);
+        if (pick >= (uint64_t)nl) break;
+        pe_action x = ordinal_action(nth_legal((int32_t)pick));
+        bool ok = apply_action(x);
+        if (bad()) break;
+        if (!ok) {
+          status = PE_CAND_ILLEGAL;
+          r.fail_step = nacts;
+          break;
+        }
+        propagate();
+        propagated = true;
+        if (bad()) break;
+        if (nacts < maxd) acts_out[nacts] = x;
+        ++nacts;
+        ++steps;
+      }
+    }
+    *n_out = (uint32_t)(nacts < maxd ? nacts : maxd);
+    finish(cp, baseline, steps, propagated, r, nullptr, 0);
+  }
+};
+
+}  // namespace pe

@@ -1,0 +1,527 @@
+// pe_engine.cu — CUDA engine and C-ABI (include/pe.h) for batched candidate
+// evaluation on B200 (sm_100a).
+//
+// Device layout:
+//   * the compiled graph (pe::GraphView tables) lives once in HBM;
+//   * every in-flight candidate owns one arena (pe::Layout) in HBM, reused
+//     across the candidates that slot processes;
+//   * kernels: pe_eval_kernel (explicit action sequences) and
+//     pe_rollout_kernel (MCTS leaf rollouts), one thread per candidate,
+//     candidates claimed from a global work counter so long rollouts do not
+//     stall a static partition.
+// There is no CPU fallback: without a device every entry point fails with
+// PE_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "pe.h"
+#include "pe_core.cuh"
+#include "pe_graph.h"
+
+struct pe_graph {
+  pe::HostGraph g;
+};
+
+struct pe_engine {
+  const pe_graph* graph = nullptr;
+  int device = 0;
+  pe_search_config cfg{};
+  pe_cost_params cp{};
+  pe::GraphView dview{};  // device pointers
+  pe::Layout layout{};
+  uint8_t* d_graph = nullptr;
+  uint8_t* d_arena = nullptr;
+  uint32_t slots = 0;
+  unsigned int* d_counter = nullptr;
+  int64_t baseline = 1;
+  uint32_t n_ordinals = 0;
+  std::vector<int32_t> auto_axes;
+  std::vector<int32_t> ent_off, ent_mem;
+  uint64_t launches = 0;
+  int sm_count = 148;
+  // staging for host-pointer calls
+  uint8_t* d_io = nullptr;
+  size_t io_cap = 0;
+};
+
+namespace {
+
+void set_err(pe_error* err, int code, const std::string& msg, int line = 0, int col = 0) {
+  if (!err) return;
+  err->code = code;
+  err->line = line;
+  err->column = col;
+  std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
+}
+
+bool cuda_ok(cudaError_t e, pe_error* err, const char* what) {
+  if (e == cudaSuccess) return true;
+  set_err(err, PE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return false;
+}
+
+__global__ void pe_eval_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
+                               unsigned int* counter, const pe_action* acts,
+                               const uint32_t* off, uint32_t n, pe_cost_params cp,
+                               int64_t baseline, pe_result* out, int32_t* trace,
+                               uint32_t trace_words) {
+  uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= slots) return;
+  pe::Cand c(g, L, arena + (uint64_t)slot * L.bytes);
+  for (;;) {
+    uint32_t i = atomicAdd(counter, 1u);
+    if (i >= n) break;
+    pe_result r;
+    c.eval(acts + off[i], (int32_t)(off[i + 1] - off[i]), cp, baseline, r,
+           trace ? trace + (uint64_t)i * trace_words : nullptr, trace_words);
+    out[i] = r;
+  }
+}
+
+__global__ void pe_rollout_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
+                                  unsigned int* counter, const pe_action* prefix,
+                                  const uint32_t* poff, const uint64_t* seeds, uint32_t n,
+                                  int32_t maxd, pe_cost_params cp, int64_t baseline,
+                                  pe_action* acts_out, uint32_t* n_out, pe_result* out,
+                                  uint64_t* legal_out, int32_t legal_words) {
+  uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= slots) return;
+  pe::Cand c(g, L, arena + (uint64_t)slot * L.bytes);
+  for (;;) {
+    uint32_t i = atomicAdd(counter, 1u);
+    if (i >= n) break;
+    pe_result r;
+    c.rollout(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, cp, baseline,
+              acts_out + (uint64_t)i * maxd, n_out + i, r,
+              legal_out ? legal_out + (uint64_t)i * legal_words : nullptr, legal_words);
+    out[i] = r;
+  }
+}
+
+constexpr int kBlock = 128;
+
+// Append a host vector to the device image; returns its offset.
+template <typename T>
+size_t stage(std::vector<uint8_t>& img, const std::vector<T>& v) {
+  size_t at = (img.size() + 15) & ~size_t(15);
+  img.resize(at + std::max<size_t>(v.size() * sizeof(T), 16));
+  if (!v.empty()) std::memcpy(img.data() + at, v.data(), v.size() * sizeof(T));
+  return at;
+}
+
+bool ensure_io(pe_engine* e, size_t bytes, pe_error* err) {
+  if (bytes <= e->io_cap) return true;
+  if (e->d_io) cudaFree(e->d_io);
+  e->d_io = nullptr;
+  e->io_cap = 0;
+  size_t cap = std::max<size_t>(bytes, 1 << 20);
+  if (!cuda_ok(cudaMalloc(&e->d_io, cap), err, "cudaMalloc(io)")) return false;
+  e->io_cap = cap;
+  return true;
+}
+
+uint32_t launch_slots(const pe_engine* e, uint32_t n) { return std::min<uint32_t>(e->slots, n); }
+
+}  // namespace
+
+extern "C" {
+
+void pe_default_cost_params(pe_cost_params* out) {
+  out->memory_budget_bytes = 16ll << 30;
+  out->flops_per_second = 1e14;
+  out->bytes_per_second = 1e11;
+  out->collective_latency_s = 1e-6;
+  out->w_mem = 0.1;
+  out->w_comm = 1.0;
+  out->w_steps = 0.01;
+}
+
+void pe_default_search_config(pe_search_config* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->auto_axes_mask = 0xffffffffu;
+  out->max_decisions = 32;
+  out->group_scopes = 1;
+  out->episodes = 500;
+  out->seed = 0;
+  out->uct_c = 1.414;
+  out->leaf_batch = 256;
+}
+
+// ------------------------------------------------------------------ graph
+pe_status pe_graph_create(const char* pir, size_t len, pe_graph** out, pe_error* err) {
+  if (!pir || !out) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  pe_graph* g = new (std::nothrow) pe_graph();
+  if (!g) {
+    set_err(err, PE_ERR_INTERNAL, "out of memory");
+    return PE_ERR_INTERNAL;
+  }
+  pe::LoadError le;
+  if (!pe::load_graph(pir, len, g->g, le)) {
+    set_err(err, le.code, le.message, le.line, le.column);
+    delete g;
+    return (pe_status)le.code;
+  }
+  *out = g;
+  if (err) err->code = PE_OK;
+  return PE_OK;
+}
+
+void pe_graph_destroy(pe_graph* g) { delete g; }
+int32_t pe_graph_num_args(const pe_graph* g) { return (int32_t)g->g.args.size(); }
+int32_t pe_graph_num_ops(const pe_graph* g) { return (int32_t)g->g.ops.size(); }
+int32_t pe_graph_num_axes(const pe_graph* g) { return (int32_t)g->g.axis_names.size(); }
+int32_t pe_graph_num_operands(const pe_graph* g) { return (int32_t)g->g.oopnd.size(); }
+int64_t pe_graph_axis_size(const pe_graph* g, int32_t axis) {
+  if (axis < 0 || axis >= (int32_t)g->g.axis_sizes.size()) return -1;
+  return g->g.axis_sizes[axis];
+}
+int32_t pe_graph_value_index(const pe_graph* g, const char* name) {
+  return name ? g->g.value_index(name) : -1;
+}
+int32_t pe_graph_axis_index(const pe_graph* g, const char* name) {
+  return name ? g->g.axis_index(name) : -1;
+}
+int32_t pe_graph_value_name(const pe_graph* g, int32_t v, char* buf, int32_t cap) {
+  if (v < 0 || v >= g->g.num_values()) return -1;
+  const std::string& s =
+      v < (int32_t)g->g.args.size() ? g->g.args[v].id : g->g.ops[v - g->g.args.size()].id;
+  if (buf && cap > 0) std::snprintf(buf, cap, "%s", s.c_str());
+  return (int32_t)s.size();
+}
+int32_t pe_graph_value_shape(const pe_graph* g, int32_t v, int64_t* dims) {
+  if (v < 0 || v >= g->g.num_values()) return -1;
+  const auto& s = g->g.value_shape(v);
+  for (size_t d = 0; d < s.size() && dims; ++d) dims[d] = s[d];
+  return (int32_t)s.size();
+}
+int32_t pe_graph_num_groups(const pe_graph* g) { return (int32_t)g->g.groups.size(); }
+int32_t pe_graph_group_size(const pe_graph* g, int32_t grp) {
+  if (grp < 0 || grp >= (int32_t)g->g.groups.size()) return -1;
+  return (int32_t)g->g.groups[grp].size();
+}
+int32_t pe_graph_group_member(const pe_graph* g, int32_t grp, int32_t i) {
+  if (grp < 0 || grp >= (int32_t)g->g.groups.size()) return -1;
+  if (i < 0 || i >= (int32_t)g->g.groups[grp].size()) return -1;
+  return g->g.groups[grp][i];
+}
+
+// ------------------------------------------------------------------ engine
+pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
+                           const pe_cost_params* cp, int32_t device, pe_engine** out,
+                           pe_error* err) {
+  if (!graph || !out) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_err(err, PE_ERR_NO_DEVICE, "no CUDA device: the engine has no CPU fallback");
+    return PE_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= ndev) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "device index out of range");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  if (!cuda_ok(cudaSetDevice(device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+  pe_engine* e = new pe_engine();
+  e->graph = graph;
+  e->device = device;
+  pe_default_search_config(&e->cfg);
+  pe_default_cost_params(&e->cp);
+  if (cfg) e->cfg = *cfg;
+  if (cp) e->cp = *cp;
+  if (e->cfg.max_decisions == 0) e->cfg.max_decisions = 32;
+  cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, device);
+  const pe::HostGraph& g = graph->g;
+  int32_t A = (int32_t)g.args.size();
+  for (int32_t a = 0; a < (int32_t)g.axis_names.size(); ++a)
+    if (e->cfg.auto_axes_mask & (1u << a)) e->auto_axes.push_back(a);
+  // worklist entries (SPEC build_worklist: arguments, optionally grouped)
+  e->ent_off.push_back(0);
+  if (e->cfg.group_scopes) {
+    for (const auto& grp : g.groups) {
+      for (int32_t m : grp) e->ent_mem.push_back(m);
+      e->ent_off.push_back((int32_t)e->ent_mem.size());
+    }
+  } else {
+    for (int32_t a = 0; a < A; ++a) {
+      e->ent_mem.push_back(a);
+      e->ent_off.push_back((int32_t)e->ent_mem.size());
+    }
+  }
+  std::vector<int32_t> grp_off{0}, grp_mem;
+  for (const auto& grp : g.groups) {
+    for (int32_t m : grp) grp_mem.push_back(m);
+    grp_off.push_back((int32_t)grp_mem.size());
+  }
+  int32_t n_entries = (int32_t)e->ent_off.size() - 1;
+  e->n_ordinals = (uint32_t)(n_entries * pe::kMaxRank * (int32_t)e->auto_axes.size());
+
+  // device image of the graph tables
+  std::vector<uint8_t> img;
+  size_t o_vshape = stage(img, g.vshape), o_vrank = stage(img, g.vrank);
+  size_t o_okind = stage(img, g.okind), o_omask = stage(img, g.omask);
+  size_t o_ooff = stage(img, g.oopnd_off), o_oopnd = stage(img, g.oopnd);
+  size_t o_slotop = stage(img, g.slot_op), o_rerr = stage(img, g.orule_err);
+  size_t o_cls = stage(img, g.ocls_off), o_crole = stage(img, g.cls_role);
+  size_t o_crdim = stage(img, g.cls_rdim), o_cmoff = stage(img, g.cls_moff);
+  size_t o_mem = stage(img, g.mem), o_scls = stage(img, g.slot_cls);
+  size_t o_rcls = stage(img, g.op_rcls), o_uoff = stage(img, g.user_off);
+  size_t o_users = stage(img, g.users), o_iu = stage(img, g.init_uses);
+  size_t o_eoff = stage(img, e->ent_off), o_emem = stage(img, e->ent_mem);
+  size_t o_goff = stage(img, grp_off), o_gmem = stage(img, grp_mem);
+  if (!cuda_ok(cudaMalloc(&e->d_graph, img.size()), err, "cudaMalloc(graph)") ||
+      !cuda_ok(cudaMemcpy(e->d_graph, img.data(), img.size(), cudaMemcpyHostToDevice), err,
+               "cudaMemcpy(graph)")) {
+    pe_engine_destroy(e);
+    return PE_ERR_CUDA;
+  }
+  pe::GraphView v = g.host_view();
+  uint8_t* b = e->d_graph;
+  v.vshape = (const int32_t*)(b + o_vshape);
+  v.vrank = b + o_vrank;
+  v.okind = b + o_okind;
+  v.omask = b + o_omask;
+  v.oopnd_off = (const int32_t*)(b + o_ooff);
+  v.oopnd = (const int32_t*)(b + o_oopnd);
+  v.slot_op = (const int32_t*)(b + o_slotop);
+  v.orule_err = b + o_rerr;
+  v.ocls_off = (const int32_t*)(b + o_cls);
+  v.cls_role = b + o_crole;
+  v.cls_rdim = (const int8_t*)(b + o_crdim);
+  v.cls_moff = (const int32_t*)(b + o_cmoff);
+  v.mem = (const uint16_t*)(b + o_mem);
+  v.slot_cls = (const int16_t*)(b + o_scls);
+  v.op_rcls = (const int16_t*)(b + o_rcls);
+  v.user_off = (const int32_t*)(b + o_uoff);
+  v.users = (const int32_t*)(b + o_users);
+  v.init_uses = (const int32_t*)(b + o_iu);
+  v.n_entries = n_entries;
+  v.n_auto = (int32_t)e->auto_axes.size();
+  for (int i = 0; i < pe::kMaxAxes; ++i)
+    v.auto_axes[i] = i < v.n_auto ? e->auto_axes[i] : 0;
+  v.entries_are_groups = e->cfg.group_scopes ? 1 : 0;
+  v.ent_off = (const int32_t*)(b + o_eoff);
+  v.ent_mem = (const int32_t*)(b + o_emem);
+  v.n_groups = (int32_t)g.groups.size();
+  v.grp_off = (const int32_t*)(b + o_goff);
+  v.grp_mem = (const int32_t*)(b + o_gmem);
+  e->dview = v;
+
+  // per-candidate arenas: one per thread slot, bounded by an HBM budget
+  e->layout = pe::make_layout(v);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  size_t budget = std::min<size_t>(free_b / 2, (size_t)24 << 30);
+  uint64_t want = (uint64_t)e->sm_count * 256;  // resident threads worth of slots
+  uint64_t fit = budget / std::max<uint64_t>(e->layout.bytes, 1);
+  e->slots = (uint32_t)std::max<uint64_t>(1, std::min(want, fit));
+  if (!cuda_ok(cudaMalloc(&e->d_arena, (size_t)e->slots * e->layout.bytes), err,
+               "cudaMalloc(arena)") ||
+      !cuda_ok(cudaMalloc(&e->d_counter, sizeof(unsigned int)), err, "cudaMalloc(counter)")) {
+    pe_engine_destroy(e);
+    return PE_ERR_CUDA;
+  }
+  // replicated plan's peak (reward baseline)
+  {
+    uint32_t off[2] = {0, 0};
+    pe_result r;
+    e->baseline = 1;
+    pe_status st = pe_eval_batch(e, nullptr, off, 1, &r, nullptr, 0, PE_SYNC, nullptr, err);
+    if (st != PE_OK) {
+      pe_engine_destroy(e);
+      return st;
+    }
+    if (r.status != PE_CAND_OK) {
+      set_err(err, PE_ERR_INTERNAL, "replicated plan failed to lower");
+      pe_engine_destroy(e);
+      return PE_ERR_INTERNAL;
+    }
+    e->baseline = std::max<int64_t>(1, r.peak_bytes);
+  }
+  *out = e;
+  if (err) err->code = PE_OK;
+  return PE_OK;
+}
+
+void pe_engine_destroy(pe_engine* e) {
+  if (!e) return;
+  if (e->d_graph) cudaFree(e->d_graph);
+  if (e->d_arena) cudaFree(e->d_arena);
+  if (e->d_counter) cudaFree(e->d_counter);
+  if (e->d_io) cudaFree(e->d_io);
+  delete e;
+}
+
+uint32_t pe_engine_num_ordinals(const pe_engine* e) { return e->n_ordinals; }
+uint32_t pe_engine_legal_words(const pe_engine* e) { return (e->n_ordinals + 63) / 64; }
+int64_t pe_engine_baseline_bytes(const pe_engine* e) { return e->baseline; }
+int64_t pe_engine_arena_bytes(const pe_engine* e) { return (int64_t)e->layout.bytes; }
+uint32_t pe_engine_slots(const pe_engine* e) { return e->slots; }
+uint64_t pe_engine_launch_count(const pe_engine* e) { return e->launches; }
+
+pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* out) {
+  if (!out || ord >= e->n_ordinals) return PE_ERR_INVALID_ARGUMENT;
+  uint32_t na = (uint32_t)e->auto_axes.size();
+  uint32_t ai = ord % na, d = (ord / na) % pe::kMaxRank, ent = ord / na / pe::kMaxRank;
+  out->axis = (uint8_t)e->auto_axes[ai];
+  out->dim = (uint8_t)d;
+  out->pad = 0;
+  if (e->cfg.group_scopes) {
+    out->kind = PE_ACT_TILE_GROUP;
+    out->value = ent;
+  } else {
+    out->kind = PE_ACT_TILE;
+    out->value = (uint32_t)e->ent_mem[e->ent_off[ent]];
+  }
+  return PE_OK;
+}
+
+pe_status pe_eval_batch(pe_engine* e, const pe_action* acts, const uint32_t* seq_off,
+                        uint32_t n, pe_result* out, int32_t* trace, uint32_t trace_words,
+                        uint32_t flags, void* stream, pe_error* err) {
+  if (!e || !seq_off || !out) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  if (n == 0) return PE_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+  const pe_action* d_acts = acts;
+  const uint32_t* d_off = seq_off;
+  pe_result* d_out = out;
+  int32_t* d_trace = trace;
+  if (!(flags & PE_MEM_DEVICE)) {
+    uint32_t n_acts = seq_off[n];
+    size_t b_acts = ((size_t)n_acts * sizeof(pe_action) + 255) & ~size_t(255);
+    size_t b_off = ((size_t)(n + 1) * 4 + 255) & ~size_t(255);
+    size_t b_out = ((size_t)n * sizeof(pe_result) + 255) & ~size_t(255);
+    size_t b_tr = trace ? (size_t)n * trace_words * 4 : 0;
+    if (!ensure_io(e, b_acts + b_off + b_out + b_tr + 256, err)) return PE_ERR_CUDA;
+    uint8_t* p = e->d_io;
+    d_acts = (const pe_action*)p;
+    d_off = (const uint32_t*)(p + b_acts);
+    d_out = (pe_result*)(p + b_acts + b_off);
+    d_trace = trace ? (int32_t*)(p + b_acts + b_off + b_out) : nullptr;
+    if (n_acts && !cuda_ok(cudaMemcpyAsync((void*)d_acts, acts, (size_t)n_acts * sizeof(pe_action),
+                                           cudaMemcpyHostToDevice, st), err, "H2D acts"))
+      return PE_ERR_CUDA;
+    if (!cuda_ok(cudaMemcpyAsync((void*)d_off, seq_off, (size_t)(n + 1) * 4,
+                                 cudaMemcpyHostToDevice, st), err, "H2D offsets"))
+      return PE_ERR_CUDA;
+  }
+  if (!cuda_ok(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned int), st), err, "memset"))
+    return PE_ERR_CUDA;
+  uint32_t slots = launch_slots(e, n);
+  pe_eval_kernel<<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+      e->dview, e->layout, e->d_arena, slots, e->d_counter, d_acts, d_off, n, e->cp,
+      e->baseline, d_out, d_trace, trace_words);
+  e->launches++;
+  if (!cuda_ok(cudaGetLastError(), err, "pe_eval_kernel launch")) return PE_ERR_CUDA;
+  if (!(flags & PE_MEM_DEVICE)) {
+    if (!cuda_ok(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(pe_result),
+                                 cudaMemcpyDeviceToHost, st), err, "D2H results"))
+      return PE_ERR_CUDA;
+    if (trace && !cuda_ok(cudaMemcpyAsync(trace, d_trace, (size_t)n * trace_words * 4,
+                                          cudaMemcpyDeviceToHost, st), err, "D2H trace"))
+      return PE_ERR_CUDA;
+    if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
+  } else if (flags & PE_SYNC) {
+    if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
+  }
+  return PE_OK;
+}
+
+pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t* prefix_off,
+                           const uint64_t* seeds, uint32_t n, pe_action* acts_out,
+                           uint32_t* n_acts_out, pe_result* out, uint64_t* legal_out,
+                           uint32_t flags, void* stream, pe_error* err) {
+  if (!e || !prefix_off || !seeds || !acts_out || !n_acts_out || !out) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  if (n == 0) return PE_OK;
+  if (e->auto_axes.empty()) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "no auto axes selected");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+  int32_t maxd = (int32_t)e->cfg.max_decisions;
+  int32_t lw = (int32_t)pe_engine_legal_words(e);
+  const pe_action* d_prefix = prefix;
+  const uint32_t* d_poff = prefix_off;
+  const uint64_t* d_seeds = seeds;
+  pe_action* d_acts = acts_out;
+  uint32_t* d_nacts = n_acts_out;
+  pe_result* d_out = out;
+  uint64_t* d_legal = legal_out;
+  if (!(flags & PE_MEM_DEVICE)) {
+    uint32_t np = prefix_off[n];
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    size_t b_pre = al((size_t)np * sizeof(pe_action) + 8), b_poff = al((size_t)(n + 1) * 4);
+    size_t b_seed = al((size_t)n * 8), b_acts = al((size_t)n * maxd * sizeof(pe_action));
+    size_t b_nacts = al((size_t)n * 4), b_out = al((size_t)n * sizeof(pe_result));
+    size_t b_legal = legal_out ? al((size_t)n * lw * 8) : 0;
+    if (!ensure_io(e, b_pre + b_poff + b_seed + b_acts + b_nacts + b_out + b_legal, err))
+      return PE_ERR_CUDA;
+    uint8_t* p = e->d_io;
+    d_prefix = (const pe_action*)p;
+    p += b_pre;
+    d_poff = (const uint32_t*)p;
+    p += b_poff;
+    d_seeds = (const uint64_t*)p;
+    p += b_seed;
+    d_acts = (pe_action*)p;
+    p += b_acts;
+    d_nacts = (uint32_t*)p;
+    p += b_nacts;
+    d_out = (pe_result*)p;
+    p += b_out;
+    d_legal = legal_out ? (uint64_t*)p : nullptr;
+    if (np && !cuda_ok(cudaMemcpyAsync((void*)d_prefix, prefix, (size_t)np * sizeof(pe_action),
+                                       cudaMemcpyHostToDevice, st), err, "H2D prefix"))
+      return PE_ERR_CUDA;
+    if (!cuda_ok(cudaMemcpyAsync((void*)d_poff, prefix_off, (size_t)(n + 1) * 4,
+                                 cudaMemcpyHostToDevice, st), err, "H2D prefix_off") ||
+        !cuda_ok(cudaMemcpyAsync((void*)d_seeds, seeds, (size_t)n * 8, cudaMemcpyHostToDevice,
+                                 st), err, "H2D seeds"))
+      return PE_ERR_CUDA;
+  }
+  if (!cuda_ok(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned int), st), err, "memset"))
+    return PE_ERR_CUDA;
+  uint32_t slots = launch_slots(e, n);
+  pe_rollout_kernel<<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+      e->dview, e->layout, e->d_arena, slots, e->d_counter, d_prefix, d_poff, d_seeds, n, maxd,
+      e->cp, e->baseline, d_acts, d_nacts, d_out, d_legal, lw);
+  e->launches++;
+  if (!cuda_ok(cudaGetLastError(), err, "pe_rollout_kernel launch")) return PE_ERR_CUDA;
+  if (!(flags & PE_MEM_DEVICE)) {
+    bool ok = cuda_ok(cudaMemcpyAsync(acts_out, d_acts, (size_t)n * maxd * sizeof(pe_action),
+                                      cudaMemcpyDeviceToHost, st), err, "D2H acts") &&
+              cuda_ok(cudaMemcpyAsync(n_acts_out, d_nacts, (size_t)n * 4,
+                                      cudaMemcpyDeviceToHost, st), err, "D2H n_acts") &&
+              cuda_ok(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(pe_result),
+                                      cudaMemcpyDeviceToHost, st), err, "D2H results");
+    if (ok && legal_out)
+      ok = cuda_ok(cudaMemcpyAsync(legal_out, d_legal, (size_t)n * lw * 8,
+                                   cudaMemcpyDeviceToHost, st), err, "D2H legal");
+    if (!ok) return PE_ERR_CUDA;
+    if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
+  } else if (flags & PE_SYNC) {
+    if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
+  }
+  return PE_OK;
+}
+
+}  // extern "C"

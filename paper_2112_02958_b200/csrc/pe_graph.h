@@ -1,0 +1,86 @@
+// pe_graph.h — host graph loader + compiler (the boundary's `parse_program`).
+//
+// Parses the reference's `.pir` text format (SPEC tensor_ir "External
+// Interfaces"; REF parser.cc), validates it with the reference's shape
+// rules (REF validate.cc:161-225), and compiles it into the SoA tables of
+// pe::GraphView.  Host-only C++; no exceptions cross the C-ABI.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "pe_graph_view.h"
+
+namespace pe {
+
+struct HostOp {
+  std::string id;
+  Kind kind = kAdd;
+  std::vector<int32_t> operands;  // value indices
+  std::vector<int64_t> shape;     // result type
+  std::string scope;
+  std::vector<int> lhs_batch, rhs_batch, lhs_contract, rhs_contract;
+  std::vector<int> dims;  // reduce dims / transpose perm / broadcast map
+  std::vector<int64_t> start, limit;
+  int dim = -1;
+  double value = 0.;
+};
+
+struct HostArg {
+  std::string id;
+  std::vector<int64_t> shape;
+  std::string scope;
+};
+
+struct HostClass {
+  Role role;
+  int rdim;
+  std::vector<std::pair<int, int>> members;  // (operand, dim)
+};
+
+struct HostGraph {
+  std::string name;
+  std::vector<std::string> axis_names;
+  std::vector<int64_t> axis_sizes;
+  std::vector<HostArg> args;
+  std::vector<HostOp> ops;
+  int32_t result = -1;
+
+  // compiled tables (see GraphView)
+  std::vector<int32_t> vshape;
+  std::vector<uint8_t> vrank;
+  std::vector<uint8_t> okind, omask, orule_err;
+  std::vector<int32_t> oopnd_off, oopnd, slot_op;
+  std::vector<int32_t> ocls_off;
+  std::vector<uint8_t> cls_role;
+  std::vector<int8_t> cls_rdim;
+  std::vector<int32_t> cls_moff;
+  std::vector<uint16_t> mem;
+  std::vector<int16_t> slot_cls, op_rcls;
+  std::vector<int32_t> user_off, users, init_uses;
+  std::vector<std::vector<int32_t>> groups;  // scope groups
+
+  int32_t num_values() const { return (int32_t)(args.size() + ops.size()); }
+  int32_t value_index(const std::string& name) const;
+  int32_t axis_index(const std::string& name) const;
+  const std::vector<int64_t>& value_shape(int32_t v) const {
+    return v < (int32_t)args.size() ? args[v].shape : ops[v - args.size()].shape;
+  }
+  // GraphView over the host vectors (worklist fields left empty)
+  GraphView host_view() const;
+};
+
+struct LoadError {
+  int code = 0;  // pe_status
+  int line = 0, column = 0;
+  std::string message;
+};
+
+// Parse + validate + compile.  Returns false and fills `err` on failure.
+bool load_graph(const char* text, size_t len, HostGraph& g, LoadError& err);
+
+// SPEC:568 scope normalisation used for grouping.
+std::string normalize_scope(const std::string& s);
+
+}  // namespace pe

@@ -1,0 +1,97 @@
+// pe_graph_view.h — the compiled, read-only graph as the kernels see it.
+//
+// Structure-of-arrays CSR resident in HBM (one copy per device, shared by all
+// candidates).  Built once per program by the host graph compiler
+// (pe_graph.cc) from the `.pir` text; it replaces the reference's AoS
+// `Program` / `Operation` structs (REF ir.h:84-131) and the per-call rule
+// instantiation of `rule_for` (REF registry.cc:123-206): every op's
+// propagation rule is precomputed for its global operand shapes.
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define PE_HD __host__ __device__ __forceinline__
+#else
+#define PE_HD inline
+#endif
+
+namespace pe {
+
+// REF OpKind numbering (ir.h:31-62); only base kinds appear in a root graph.
+enum Kind : uint8_t {
+  kConstant = 0, kAdd, kSub, kMul, kDiv, kNeg, kExp, kTanh, kRsqrt, kMaximum,
+  kDot, kReduceSum, kReduceMax, kTranspose, kReshape, kBroadcastInDim, kSlice,
+  kConcatenate,
+  kNumBaseKinds = 18,
+  kAllReduce = 22, kAllGather = 23, kSliceByCoord = 24
+};
+
+// DimRole (REF registry.h:27-38)
+enum Role : uint8_t { kPass = 0, kContract = 1, kBlocked = 2 };
+
+constexpr int kMaxRank = 4;
+constexpr int kMaxAxes = 4;
+
+struct GraphView {
+  int32_t A;        // arguments
+  int32_t N;        // ops (top level, topologically ordered)
+  int32_t E;        // operand slots
+  int32_t n_axes;
+  int64_t axis_size[kMaxAxes];
+  // rank of each axis name in lexicographic order: ShardingSpec::pending_sum
+  // is kept sorted by NAME (REF mesh.cc:74-77), so `pending_sum.front()` is
+  // the axis with the smallest name rank.
+  int32_t axis_name_rank[kMaxAxes];
+  int32_t result;   // returned value index
+
+  // values [A+N]: args first, then op results
+  const int32_t* vshape;  // [(A+N)*4] dims, 0-padded
+  const uint8_t* vrank;   // [A+N]
+
+  // ops [N]
+  const uint8_t* okind;      // Kind
+  const uint8_t* omask;      // dot: rhs free-dim mask; broadcast: mapped result-dim mask
+  const int32_t* oopnd_off;  // [N+1] into oopnd / slot arrays
+  const int32_t* oopnd;      // [E] original operand value index
+  const int32_t* slot_op;    // [E] op owning operand slot
+  const uint8_t* orule_err;  // [N] rule_for would throw (reshape factorisation)
+
+  // propagation rules, per op: classes [ocls_off[o], ocls_off[o+1])
+  const int32_t* ocls_off;   // [N+1]
+  const uint8_t* cls_role;   // [C]
+  const int8_t* cls_rdim;    // [C] result dim (pass-through) or -1
+  const int32_t* cls_moff;   // [C+1] member range into mem
+  const uint16_t* mem;       // member = operand << 2 | dim
+  const int16_t* slot_cls;   // [E*4] (operand slot, dim) -> class index local to op, -1
+  const int16_t* op_rcls;    // [N*4] result dim -> pass-through class (local) or -1
+
+  // users CSR: value -> operand slots that originally read it
+  const int32_t* user_off;   // [A+N+1]
+  const int32_t* users;      // operand slot indices
+
+  const int32_t* init_uses;  // [A+N] count_uses on the root (REF ir.cc:125-134)
+
+  // worklist entries (scope groups or single arguments) for rollouts
+  int32_t n_entries;
+  int32_t n_auto;
+  int32_t auto_axes[kMaxAxes];
+  int32_t entries_are_groups;
+  const int32_t* ent_off;    // [n_entries+1]
+  const int32_t* ent_mem;    // arg indices
+  // scope groups (for PE_ACT_TILE_GROUP)
+  int32_t n_groups;
+  const int32_t* grp_off;    // [n_groups+1]
+  const int32_t* grp_mem;
+
+  PE_HD const int32_t* shape(int32_t v) const { return vshape + 4 * v; }
+};
+
+// spec word (pe.h trace layout): per dim (axis+1) in 4 bits, pending mask
+// << 16, rank << 24
+PE_HD uint32_t spec_axis(uint32_t spec, int d) { return (spec >> (4 * d)) & 0xFu; }
+PE_HD uint32_t spec_set_axis(uint32_t spec, int d, uint32_t ax1) {
+  return (spec & ~(0xFu << (4 * d))) | (ax1 << (4 * d));
+}
+PE_HD uint32_t spec_pending(uint32_t spec) { return (spec >> 16) & 0xFu; }
+
+}  // namespace pe

@@ -1,0 +1,235 @@
+"""Host-side mirror of the reference interface for the candidate-evaluation
+path, over the C-ABI of include/pe.h.
+
+Reference API (REF = /root/reference/proj)        this module
+------------------------------------------------   ---------------------------
+parse_program(text)          parser.h:28           Graph(text)
+apply_tile_action(p,v,d,ax)  rewrite.h:33-34       action tuples (value, dim, axis)
+propagate(p)                 propagate.h:54        } applied after every action
+lower_to_spmd(p)             spmd.h:67             } inside Engine.eval_batch,
+collective_stats(sp)         spmd.h:87             } batched on the GPU
+peak_liveness/comm_cost/runtime_estimate/reward    (SPEC cost module)
+MCTS rollouts                (SPEC mcts_search)    Engine.rollout_batch
+Errors: Error/ParseError/ValidationError/IllegalActionError/InternalError
+(error.h:25-60) are raised with the same names; per-candidate
+IllegalActionError/InternalError become a status in the result record.
+
+The engine is GPU-only: constructing an Engine without a CUDA device raises
+NoDeviceError — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import capi
+from .capi import PeAction, PeError, PeResult
+
+
+class Error(RuntimeError):
+    pass
+
+
+class ParseError(Error):
+    def __init__(self, msg, line=0, column=0):
+        super().__init__(msg)
+        self.line = line
+        self.column = column
+
+
+class ValidationError(Error):
+    pass
+
+
+class IllegalActionError(Error):
+    pass
+
+
+class InternalError(Error):
+    pass
+
+
+class NoDeviceError(Error):
+    pass
+
+
+def _raise(rc: int, err: PeError):
+    msg = err.message.decode(errors="replace")
+    if rc == capi.PE_ERR_PARSE:
+        raise ParseError(msg, err.line, err.column)
+    if rc == capi.PE_ERR_VALIDATION:
+        raise ValidationError(msg)
+    if rc == capi.PE_ERR_ILLEGAL:
+        raise IllegalActionError(msg)
+    if rc == capi.PE_ERR_NO_DEVICE:
+        raise NoDeviceError(msg)
+    if rc == capi.PE_ERR_INTERNAL:
+        raise InternalError(msg)
+    raise Error(f"pe error {rc}: {msg}")
+
+
+class Graph:
+    """A parsed, validated and compiled program (parse_program)."""
+
+    def __init__(self, text: str):
+        self.lib = capi.load()
+        self.text = text
+        b = text.encode()
+        h = C.c_void_p()
+        err = PeError()
+        rc = self.lib.pe_graph_create(b, len(b), C.byref(h), C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        self.h = h
+        L = self.lib
+        self.n_args = L.pe_graph_num_args(h)
+        self.n_ops = L.pe_graph_num_ops(h)
+        self.n_axes = L.pe_graph_num_axes(h)
+        buf = C.create_string_buffer(1024)
+        self.names = []
+        self.shapes = []
+        dims = (C.c_int64 * 4)()
+        for v in range(self.n_args + self.n_ops):
+            L.pe_graph_value_name(h, v, buf, 1024)
+            self.names.append(buf.value.decode())
+            r = L.pe_graph_value_shape(h, v, dims)
+            self.shapes.append([dims[i] for i in range(r)])
+        self.axis_sizes = [L.pe_graph_axis_size(h, a) for a in range(self.n_axes)]
+        self.groups = [[L.pe_graph_group_member(h, g, i) for i in range(L.pe_graph_group_size(h, g))]
+                       for g in range(L.pe_graph_num_groups(h))]
+        self._index = {n: i for i, n in enumerate(self.names)}
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.lib.pe_graph_destroy(h)
+            self.h = None
+
+    def value_index(self, name: str) -> int:
+        return self._index[name]
+
+    def axis_index(self, name: str) -> int:
+        i = self.lib.pe_graph_axis_index(self.h, name.encode())
+        if i < 0:
+            raise IllegalActionError(f'axis "{name}" is not declared')
+        return i
+
+    def group_of(self, arg: int) -> int:
+        for g, m in enumerate(self.groups):
+            if arg in m:
+                return g
+        raise KeyError(arg)
+
+    def action(self, value, dim: int, axis, group: bool = False) -> PeAction:
+        v = value if isinstance(value, int) else self.value_index(value)
+        ax = axis if isinstance(axis, int) else self.axis_index(axis)
+        if group:
+            return PeAction(self.group_of(v), dim, ax, capi.PE_ACT_TILE_GROUP, 0)
+        return PeAction(v, dim, ax, capi.PE_ACT_TILE, 0)
+
+    def actions(self, seq, group: bool = False):
+        return [self.action(*a, group=group) if not isinstance(a, PeAction) else a for a in seq]
+
+
+class Engine:
+    """Per-device batched candidate evaluator."""
+
+    def __init__(self, graph: Graph, device: int = 0, cfg=None, cost=None):
+        self.lib = graph.lib
+        self.graph = graph
+        self.cfg = cfg if cfg is not None else capi.default_search_config()
+        self.cost = cost if cost is not None else capi.default_cost_params()
+        h = C.c_void_p()
+        err = PeError()
+        rc = self.lib.pe_engine_create(graph.h, C.byref(self.cfg), C.byref(self.cost), device,
+                                       C.byref(h), C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        self.h = h
+        self.device = device
+        self.n_ordinals = self.lib.pe_engine_num_ordinals(h)
+        self.legal_words = self.lib.pe_engine_legal_words(h)
+        self.baseline_bytes = self.lib.pe_engine_baseline_bytes(h)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.lib.pe_engine_destroy(h)
+            self.h = None
+
+    def launch_count(self) -> int:
+        return int(self.lib.pe_engine_launch_count(self.h))
+
+    def arena_bytes(self) -> int:
+        return int(self.lib.pe_engine_arena_bytes(self.h))
+
+    def slots(self) -> int:
+        return int(self.lib.pe_engine_slots(self.h))
+
+    def ordinal_action(self, ordinal: int) -> PeAction:
+        a = PeAction()
+        rc = self.lib.pe_engine_ordinal_action(self.h, ordinal, C.byref(a))
+        if rc:
+            raise IndexError(ordinal)
+        return a
+
+    # ---- host-buffer entry points (the e2e path) ----
+    def eval_batch(self, seqs, trace_words: int = 0):
+        acts, off = capi.actions_array(seqs)
+        n = len(seqs)
+        out = (PeResult * n)()
+        tr = (C.c_int32 * (n * trace_words))() if trace_words else None
+        err = PeError()
+        rc = self.lib.pe_eval_batch(self.h, acts, off, n, out, tr, trace_words, 0, None,
+                                    C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        res = list(out)
+        if trace_words:
+            return res, [list(tr[i * trace_words:(i + 1) * trace_words]) for i in range(n)]
+        return res
+
+    def rollout_batch(self, prefixes, seeds, legal: bool = False):
+        acts, off = capi.actions_array(prefixes)
+        n = len(prefixes)
+        maxd = self.cfg.max_decisions
+        sd = (C.c_uint64 * n)(*seeds)
+        aout = (PeAction * (n * maxd))()
+        nout = (C.c_uint32 * n)()
+        out = (PeResult * n)()
+        lg = (C.c_uint64 * (n * self.legal_words))() if legal else None
+        err = PeError()
+        rc = self.lib.pe_rollout_batch(self.h, acts, off, sd, n, aout, nout, out, lg, 0, None,
+                                       C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        seqs = [[(aout[i * maxd + k].value, aout[i * maxd + k].dim, aout[i * maxd + k].axis,
+                  aout[i * maxd + k].kind) for k in range(nout[i])] for i in range(n)]
+        lgl = None
+        if legal:
+            lgl = [list(lg[i * self.legal_words:(i + 1) * self.legal_words]) for i in range(n)]
+        return list(out), seqs, lgl
+
+    # ---- device-buffer entry points (inputs already resident in HBM) ----
+    def rollout_batch_device(self, prefix_ptr, poff_ptr, seeds_ptr, n, acts_out_ptr,
+                             nacts_out_ptr, out_ptr, legal_ptr=None, stream=None, sync=False):
+        err = PeError()
+        flags = capi.PE_MEM_DEVICE | (capi.PE_SYNC if sync else 0)
+        rc = self.lib.pe_rollout_batch(self.h, prefix_ptr, poff_ptr, seeds_ptr, n, acts_out_ptr,
+                                       nacts_out_ptr, out_ptr, legal_ptr, flags, stream,
+                                       C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+
+    def eval_batch_device(self, acts_ptr, off_ptr, n, out_ptr, stream=None, sync=False):
+        err = PeError()
+        flags = capi.PE_MEM_DEVICE | (capi.PE_SYNC if sync else 0)
+        rc = self.lib.pe_eval_batch(self.h, acts_ptr, off_ptr, n, out_ptr, None, 0, flags, stream,
+                                    C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+
+
+def describe(r: PeResult) -> str:
+    return (f"status={r.status} peak={r.peak_bytes} ar={list(r.ar_cnt)}/{list(r.ar_bytes)} "
+            f"ag={list(r.ag_cnt)}/{list(r.ag_bytes)} sbc={list(r.sbc_cnt)} steps={r.n_steps} "
+            f"stuck={r.n_stuck} ops={r.n_spmd_ops} runtime={r.runtime_s:.6g} reward={r.reward:.9f}")

@@ -1,0 +1,138 @@
+// pe_host_harness.cc — TEST HARNESS ONLY.
+//
+// Compiles the engine's per-candidate core (paper_2112_02958_b200/csrc/
+// pe_core.cuh) with g++ so the CPU test suite can differential-fuzz the
+// rewrite automaton against the oracle (the patched reference) on thousands
+// of programs without a GPU.  The product library (libpe_b200.so) is built
+// by nvcc only and contains no host copy of the core; this harness is never
+// loaded by the product path.  GPU parity tests (tests/test_gpu_parity.py)
+// check the device build against the same oracle.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "pe.h"
+#include "pe_core.cuh"
+#include "pe_graph.h"
+
+namespace {
+
+struct Harness {
+  pe::HostGraph g;
+  pe::GraphView v;
+  pe::Layout L;
+  std::vector<int32_t> ent_off, ent_mem, grp_off, grp_mem;
+  std::vector<int32_t> auto_axes;
+  std::vector<uint8_t> arena;
+  pe_search_config cfg;
+  pe_cost_params cp;
+  int64_t baseline = 1;
+};
+
+void defaults(pe_search_config* c, pe_cost_params* p) {
+  std::memset(c, 0, sizeof(*c));
+  c->auto_axes_mask = 0xffffffffu;
+  c->max_decisions = 32;
+  c->group_scopes = 1;
+  c->uct_c = 1.414;
+  p->memory_budget_bytes = 16ll << 30;
+  p->flops_per_second = 1e14;
+  p->bytes_per_second = 1e11;
+  p->collective_latency_s = 1e-6;
+  p->w_mem = 0.1;
+  p->w_comm = 1.0;
+  p->w_steps = 0.01;
+}
+
+int setup(Harness& h, const char* pir, size_t len, const pe_search_config* cfg,
+          const pe_cost_params* cp, char* err, size_t errcap) {
+  pe::LoadError le;
+  if (!pe::load_graph(pir, len, h.g, le)) {
+    if (err) std::snprintf(err, errcap, "%s", le.message.c_str());
+    return le.code;
+  }
+  defaults(&h.cfg, &h.cp);
+  if (cfg) h.cfg = *cfg;
+  if (cp) h.cp = *cp;
+  h.v = h.g.host_view();
+  for (int a = 0; a < (int)h.g.axis_names.size(); ++a)
+    if (h.cfg.auto_axes_mask & (1u << a)) h.auto_axes.push_back(a);
+  h.ent_off.push_back(0);
+  h.grp_off.push_back(0);
+  for (const auto& grp : h.g.groups) {
+    for (int m : grp) h.grp_mem.push_back(m);
+    h.grp_off.push_back((int32_t)h.grp_mem.size());
+  }
+  if (h.cfg.group_scopes) {
+    h.ent_off = h.grp_off;
+    h.ent_mem = h.grp_mem;
+  } else {
+    for (int a = 0; a < (int)h.g.args.size(); ++a) {
+      h.ent_mem.push_back(a);
+      h.ent_off.push_back((int32_t)h.ent_mem.size());
+    }
+  }
+  h.v.n_entries = (int32_t)h.ent_off.size() - 1;
+  h.v.n_auto = (int32_t)h.auto_axes.size();
+  for (int i = 0; i < pe::kMaxAxes; ++i)
+    h.v.auto_axes[i] = i < h.v.n_auto ? h.auto_axes[i] : 0;
+  h.v.entries_are_groups = h.cfg.group_scopes ? 1 : 0;
+  h.v.ent_off = h.ent_off.data();
+  h.v.ent_mem = h.ent_mem.data();
+  h.v.n_groups = (int32_t)h.g.groups.size();
+  h.v.grp_off = h.grp_off.data();
+  h.v.grp_mem = h.grp_mem.data();
+  h.L = pe::make_layout(h.v);
+  h.arena.assign(h.L.bytes, 0);
+  pe::Cand c(h.v, h.L, h.arena.data());
+  pe_result r;
+  c.eval(nullptr, 0, h.cp, 1, r, nullptr, 0);
+  h.baseline = std::max<int64_t>(1, r.peak_bytes);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int harness_eval_batch(const char* pir, size_t len, const pe_search_config* cfg,
+                       const pe_cost_params* cp, const pe_action* acts, const uint32_t* off,
+                       uint32_t n, pe_result* out, int32_t* trace, uint32_t trace_words,
+                       char* err, size_t errcap) {
+  Harness h;
+  int rc = setup(h, pir, len, cfg, cp, err, errcap);
+  if (rc) return rc;
+  pe::Cand c(h.v, h.L, h.arena.data());
+  for (uint32_t i = 0; i < n; ++i)
+    c.eval(acts + off[i], (int32_t)(off[i + 1] - off[i]), h.cp, h.baseline, out[i],
+           trace ? trace + (size_t)i * trace_words : nullptr, trace_words);
+  return 0;
+}
+
+int harness_rollout_batch(const char* pir, size_t len, const pe_search_config* cfg,
+                          const pe_cost_params* cp, const pe_action* prefix,
+                          const uint32_t* poff, const uint64_t* seeds, uint32_t n,
+                          pe_action* acts_out, uint32_t* n_out, pe_result* out,
+                          uint64_t* legal_out, char* err, size_t errcap) {
+  Harness h;
+  int rc = setup(h, pir, len, cfg, cp, err, errcap);
+  if (rc) return rc;
+  pe::Cand c(h.v, h.L, h.arena.data());
+  int32_t maxd = (int32_t)h.cfg.max_decisions;
+  int32_t nord = h.v.n_entries * pe::kMaxRank * h.v.n_auto;
+  int32_t lw = (nord + 63) / 64;
+  for (uint32_t i = 0; i < n; ++i)
+    c.rollout(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, h.cp,
+              h.baseline, acts_out + (size_t)i * maxd, n_out + i, out[i],
+              legal_out ? legal_out + (size_t)i * lw : nullptr, lw);
+  return 0;
+}
+
+int64_t harness_arena_bytes(const char* pir, size_t len) {
+  Harness h;
+  char err[256];
+  if (setup(h, pir, len, nullptr, nullptr, err, sizeof(err))) return -1;
+  return (int64_t)h.L.bytes;
+}
+
+}  // extern "C"
