@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""bench.py — partition candidates evaluated / s on B200.
+
+Workload (BASELINE.json configs[2], the north_star's "24-layer transformer
+graph"): the 24-layer GPT-2-medium-shaped forward graph (d=1024, H=16,
+F=4096, S=1024, B=8; 1032 ops, 145 arguments) on the 2-axis mesh
+[batch=4, model=2], scope-grouped worklist, auto axes {batch, model}.  A
+candidate = one MCTS rollout from the root under the SPEC rollout policy
+(uniform over legal TileValue actions, Stop weight 2 after the first
+decision, <= 32 decisions), each action followed by propagate, then
+lower_to_spmd + collective_stats + cost model + reward.  One step = one
+launch over a batch of candidates with fresh seeds.
+
+  python bench.py [--gpus N --steps K --warmup W]        engine (this repo)
+  python bench.py --impl reference ...                    reference CPU path
+
+Under torchrun every rank evaluates its own candidate stream (seeds offset by
+rank; weak scaling, no data-path collective); timing is max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "partition candidates evaluated/sec"
+UNIT = "candidates/s"
+WORKLOAD = "gpt2-medium-24L rollouts, mesh [batch=4, model=2], grouped worklist"
+
+
+def _config(batch, extra=None):
+    c = {"workload": WORKLOAD, "graph": "24-layer GPT-2-medium forward (1032 ops, 145 args)",
+         "mesh": "[batch=4, model=2]", "candidates_per_step": batch,
+         "candidate": "SPEC rollout from root: uniform legal TileValue, Stop w=2 after 1st, <=32",
+         "auto_axes": ["batch", "model"], "group_scopes": True}
+    if extra:
+        c.update(extra)
+    return c
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, device=0):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            backend = "nccl"
+            import torch
+            if not torch.cuda.is_available():
+                backend = "gloo"
+            dist.init_process_group(backend)
+        return dist, dist.get_rank(), ws
+    return None, 0, 1
+
+
+def _max_over_ranks(dist, x: float, device=None) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_reference(text, n_cand, seed0, threads):
+    """The reference's own CPU path (oracle/_ref: patched REF propagate /
+    lower_to_spmd / collective_stats + SPEC cost/rollout restatement) on
+    `threads` host cores.  Returns (cand/s, seconds)."""
+    import helpers as H
+    from paper_2112_02958_b200 import capi
+    cfg = capi.default_search_config(group_scopes=1)
+    t0 = time.perf_counter()
+    H.rollout_batch("oracle", text, [[]] * n_cand, [seed0 + i for i in range(n_cand)], cfg,
+                    threads=threads)
+    dt = time.perf_counter() - t0
+    return n_cand / dt, dt
+
+
+def run_reference(args):
+    dist, rank, ws = _dist()
+    if rank != 0:
+        return 0
+    from paper_2112_02958_b200 import modelgen
+    text = modelgen.config_program(3)
+    threads = os.cpu_count() or 1
+    per_step = 2 * threads  # ~1-3 s of CPU work per step on this path
+    for w in range(args.warmup):
+        cpu_reference(text, per_step, 10_000_000 + w * per_step, threads)
+    total = 0.0
+    n = 0
+    for s in range(args.steps):
+        _, dt = cpu_reference(text, per_step, 20_000_000 + s * per_step, threads)
+        total += dt
+        n += per_step
+    v = n / total
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": _config(per_step, {"parallelism": f"{threads} host threads"}),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{args.steps} x {per_step} rollouts of the bench workload"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------- engine
+def run_engine(args):
+    import ctypes as C
+
+    import torch
+
+    from paper_2112_02958_b200 import capi, engine, modelgen
+
+    dist, rank, ws = _dist()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    text = modelgen.config_program(3)
+    cfg = capi.default_search_config(group_scopes=1)
+    g = engine.Graph(text)
+    eng = engine.Engine(g, device=local, cfg=cfg)
+    B = args.batch
+    K, W = args.steps, args.warmup
+    maxd = cfg.max_decisions
+    lib = g.lib
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+
+    # inputs resident in HBM before timing: per-step seeds, empty prefixes
+    base = 1_000_003 * (rank + 1)
+    seeds = (torch.arange((K + W) * B, dtype=torch.int64, device=dev) + base).view(K + W, B)
+    poff = torch.zeros(B + 1, dtype=torch.int32, device=dev)
+    prefix = torch.zeros(2, dtype=torch.int64, device=dev)
+    acts_out = torch.empty(B * maxd * 8, dtype=torch.uint8, device=dev)
+    nacts = torch.empty(B, dtype=torch.int32, device=dev)
+    res = torch.empty(B * C.sizeof(capi.PeResult), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(i):
+        eng.rollout_batch_device(prefix.data_ptr(), poff.data_ptr(), seeds[i].data_ptr(), B,
+                                 acts_out.data_ptr(), nacts.data_ptr(), res.data_ptr(),
+                                 stream=sp)
+
+    for i in range(W):
+        flush.zero_()
+        step(K + i)
+    torch.cuda.synchronize(dev)
+    launches0 = eng.launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(K):
+            flush.zero_()  # L2 flushed between timed iterations (outside the events)
+            starts[i].record(stream)
+            step(i)
+            stops[i].record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    launches = eng.launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, stops)]
+    total_ms = _max_over_ranks(dist, sum(step_ms), dev)
+    value = ws * K * B / (total_ms / 1e3)
+
+    # sanity: every candidate evaluated OK
+    host = res.view(B, C.sizeof(capi.PeResult)).cpu().numpy()
+    results = [capi.PeResult.from_buffer_copy(host[i].tobytes()) for i in range(B)]
+    bad = sum(r.status != 0 for r in results)
+    mean_steps = sum(r.n_steps for r in results) / B
+    mean_ops = sum(r.n_spmd_ops for r in results) / B
+
+    # e2e: the public C-ABI with HOST buffers (pinned), copies inside the region
+    pin_seeds = torch.empty(B, dtype=torch.int64).pin_memory()
+    pin_poff = torch.zeros(B + 1, dtype=torch.int32).pin_memory()
+    pin_acts = torch.empty(B * maxd * 8, dtype=torch.uint8).pin_memory()
+    pin_nacts = torch.empty(B, dtype=torch.int32).pin_memory()
+    pin_res = torch.empty(B * C.sizeof(capi.PeResult), dtype=torch.uint8).pin_memory()
+    err = capi.PeError()
+    h2d = pin_seeds.numel() * 8 + pin_poff.numel() * 4
+    d2h = pin_acts.numel() + pin_nacts.numel() * 4 + pin_res.numel()
+    e2e_k = max(1, min(K, 5))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for i in range(e2e_k):
+        pin_seeds.copy_(torch.arange(B, dtype=torch.int64) + base + 7_000_000 * (i + 1))
+        rc = lib.pe_rollout_batch(eng.h, None, C.c_void_p(pin_poff.data_ptr()),
+                                  C.c_void_p(pin_seeds.data_ptr()), B, C.c_void_p(pin_acts.data_ptr()),
+                                  C.c_void_p(pin_nacts.data_ptr()), C.c_void_p(pin_res.data_ptr()),
+                                  None, 0, sp, C.byref(err))
+        assert rc == 0, err.message
+        _ = pin_res[:8].numpy().tobytes()  # host read of the step's result
+    e2e_s = _max_over_ranks(dist, time.perf_counter() - t0, dev)
+    e2e = ws * e2e_k * B / e2e_s
+
+    # roofline: algorithmic bytes per candidate
+    A, N = g.n_args, g.n_ops
+    s_graph = eng.graph_bytes()
+    s_state = 8 * (A + N)
+    s_io = C.sizeof(capi.PeResult) + 8 * maxd + 4 + 8 + 4
+    b_cand = s_graph + 2 * s_state + s_io
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    kern_s = sum(step_ms) / 1e3 / K
+    achieved = b_cand * B / kern_s / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("bytes_per_launch_per_candidate")
+            traffic = traffic * B if traffic else None
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import helpers as H
+        if os.path.exists(H.ORACLE_SO):
+            threads = os.cpu_count() or 1
+            n_cpu = 8 * threads
+            v_cpu, dt = cpu_reference(text, n_cpu, 30_000_000, threads)
+            cpu = {"value": v_cpu, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{n_cpu} rollouts of the bench workload ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
+                "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+                "config": _config(B, {"parallelism": f"candidate-parallel x{ws}",
+                                      "l2": "256 MB flush between timed steps",
+                                      "mean_decisions": round(mean_steps, 3),
+                                      "mean_spmd_ops": round(mean_ops, 1),
+                                      "arena_bytes": eng.arena_bytes(), "slots": eng.slots(),
+                                      "failed_candidates": bad}),
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches,
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "algorithmic_bytes_per_candidate": b_cand,
+                             "kernel": "pe_rollout_kernel",
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+                "cpu_baseline": cpu,
+                "clocks": clk.summary()}
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=65536)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_engine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

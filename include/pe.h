@@ -219,6 +219,8 @@ int64_t pe_engine_baseline_bytes(const pe_engine* e);
 /* bytes of the per-candidate arena, and candidate slots per launch */
 int64_t pe_engine_arena_bytes(const pe_engine* e);
 uint32_t pe_engine_slots(const pe_engine* e);
+/* bytes of the compiled graph image resident in HBM */
+int64_t pe_engine_graph_bytes(const pe_engine* e);
 /* kernel launches issued by this engine since creation */
 uint64_t pe_engine_launch_count(const pe_engine* e);
 

@@ -126,6 +126,7 @@ SIGNATURES = {
     "pe_engine_arena_bytes": (C.c_int64, [_P]),
     "pe_engine_slots": (C.c_uint32, [_P]),
     "pe_engine_launch_count": (C.c_uint64, [_P]),
+    "pe_engine_graph_bytes": (C.c_int64, [_P]),
 }
 
 HERE = os.path.dirname(os.path.abspath(__file__))

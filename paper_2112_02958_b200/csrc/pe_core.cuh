@@ -92,18 +92,41 @@ struct Arena {
 
 PE_HD uint64_t align8(uint64_t x) { return (x + 7) & ~uint64_t(7); }
 
-// Host-side sizing.  Bounds are structural: every original
-// op is pulled or migrated at most once, every value is tiled at most once.
-inline Layout make_layout(const GraphView& g) {
+inline Layout relayout(const GraphView& g, const Caps& caps);
+
+// Host-side sizing.  The FULL layout's bounds are
+// structural: every original op is pulled or migrated at most once, every
+// value is tiled at most once.  The TIGHT layout is sized from measured
+// high-water marks (slots ~ N+E, SPMD ops ~ 1.45 N on the 24-layer graph)
+// with headroom; a candidate that overflows it reports PE_CAND_CAPACITY and
+// is re-evaluated in a full-size arena by the retry kernel, so the tight
+// layout changes memory footprint, never results.
+inline Layout make_layout(const GraphView& g, bool tight = false) {
   Layout L{};
   int32_t A = g.A, N = g.N, E = g.E;
   int32_t K = A + N;               // action loops (each value tiled once)
   int32_t S = E + K;               // slices
-  L.caps.V = A + N + N + S + K + A + 8;
-  L.caps.L = N + K + 4;
-  L.caps.FS = 2 * A + 4;
-  L.caps.EM = 3 * (N + S) + 2 * L.caps.L + A + 64;
-  L.caps.EO = E + 2 * L.caps.EM + 64;
+  if (tight) {
+    L.caps.V = A + 2 * N + E + 64;
+    L.caps.L = N + 64;
+    L.caps.FS = 2 * A + 4;
+    L.caps.EM = (3 * (N + A)) / 2 + 256;
+    L.caps.EO = E + L.caps.EM + 256;
+  } else {
+    L.caps.V = A + N + N + S + K + A + 8;
+    L.caps.L = N + K + 4;
+    L.caps.FS = 2 * A + 4;
+    L.caps.EM = 3 * (N + S) + 2 * L.caps.L + A + 64;
+    L.caps.EO = E + 2 * L.caps.EM + 64;
+  }
+  return relayout(g, L.caps);
+}
+
+// Byte offsets of every per-candidate array for the given capacities.
+inline Layout relayout(const GraphView& g, const Caps& caps) {
+  Layout L{};
+  L.caps = caps;
+  int32_t A = g.A, N = g.N, E = g.E;
   uint64_t o = 0;
   auto take = [&](uint64_t bytes) {
     uint64_t at = o;
@@ -235,9 +258,28 @@ struct Cand {
   int32_t status;
   int64_t flops;
   int32_t result_buf;
+#if defined(PE_PHASE_TIMERS) && defined(__CUDA_ARCH__)
+  // profiling build only: clock64 cycles per phase
+  // 0 init 1 apply 2 forward 3 backward 4 wrap 5 legal 6 analyze 7 lower 8 score
+  long long ph[9];
+  long long t_last;
+  __device__ void tick_start() { t_last = clock64(); }
+  __device__ void tick(int k) {
+    long long t = clock64();
+    ph[k] += t - t_last;
+    t_last = t;
+  }
+#else
+  PE_HD void tick_start() {}
+  PE_HD void tick(int) {}
+#endif
 
   PE_HD Cand(const GraphView& gv, const Layout& L, uint8_t* base)
-      : g(gv), caps(L.caps), a(carve(L, base)) {}
+      : g(gv), caps(L.caps), a(carve(L, base)) {
+#if defined(PE_PHASE_TIMERS) && defined(__CUDA_ARCH__)
+    for (int k = 0; k < 9; ++k) ph[k] = 0;
+#endif
+  }
 
   // ------------------------------------------------------------ helpers
   PE_HD void fail(int32_t st) {
@@ -739,11 +781,15 @@ struct Cand {
   }
 
   PE_HD void propagate() {
+    tick(1);
     forward();
+    tick(2);
     if (bad()) return;
     backward();
+    tick(3);
     if (bad()) return;
     wrap();
+    tick(4);
   }
 
   // stuck analysis (REF propagate.cc:412-454), dedup by op id in discovery
@@ -1269,8 +1315,11 @@ struct Cand {
   // ------------------------------------------------------------ drivers
   PE_HD void finish(const pe_cost_params& cp, int64_t baseline, int32_t steps,
                     bool propagated, pe_result& r, int32_t* trace, uint32_t trace_words) {
+    tick(5);
     if (!bad() && propagated) analyze();
+    tick(6);
     if (!bad()) lower();
+    tick(7);
     if (bad()) {
       int32_t st = status;
       for (int x = 0; x < PE_MAX_AXES; ++x) {
@@ -1295,11 +1344,14 @@ struct Cand {
     r.status = status;
     r.fail_step = fs;
     if (trace && trace_words) write_trace(trace, trace_words);
+    tick(8);
   }
 
   PE_HD void eval(const pe_action* acts, int32_t n, const pe_cost_params& cp,
                   int64_t baseline, pe_result& r, int32_t* trace, uint32_t trace_words) {
+    tick_start();
     init();
+    tick(0);
     r.fail_step = -1;
     r.reserved = 0;
     int32_t steps = 0;
@@ -1379,7 +1431,9 @@ struct Cand {
   PE_HD void rollout(const pe_action* prefix, int32_t np, uint64_t seed, int32_t maxd,
                      const pe_cost_params& cp, int64_t baseline, pe_action* acts_out,
                      uint32_t* n_out, pe_result& r, uint64_t* legal_out, int32_t legal_words) {
+    tick_start();
     init();
+    tick(0);
     r.fail_step = -1;
     r.reserved = 0;
     int32_t steps = 0, nacts = 0;
@@ -1419,12 +1473,14 @@ struct Cand {
       uint64_t st = seed;
       while (!terminal) {
         if (steps >= maxd) break;
+        tick(4);
         int32_t nl = count_legal();
         if (nl == 0) break;
         uint64_t ws = steps >= 1 ? 2 : 1;
         uint64_t pick = splitmix(st) % ((uint64_t)nl + ws);
         if (pick >= (uint64_t)nl) break;
         pe_action x = ordinal_action(nth_legal((int32_t)pick));
+        tick(5);
         bool ok = apply_action(x);
         if (bad()) break;
         if (!ok) {

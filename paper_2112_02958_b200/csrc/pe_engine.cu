@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -34,16 +35,19 @@ struct pe_engine {
   pe_search_config cfg{};
   pe_cost_params cp{};
   pe::GraphView dview{};  // device pointers
-  pe::Layout layout{};
+  pe::Layout layout{};      // tight arenas (main pass)
+  pe::Layout big_layout{};  // full-size arenas (retry pass)
   uint8_t* d_graph = nullptr;
   uint8_t* d_arena = nullptr;
+  uint8_t* d_big_arena = nullptr;
   uint32_t slots = 0;
-  unsigned int* d_counter = nullptr;
+  uint32_t big_slots = 0;
   int64_t baseline = 1;
   uint32_t n_ordinals = 0;
   std::vector<int32_t> auto_axes;
   std::vector<int32_t> ent_off, ent_mem;
   uint64_t launches = 0;
+  int64_t graph_bytes = 0;
   int sm_count = 148;
   // staging for host-pointer calls
   uint8_t* d_io = nullptr;
@@ -66,17 +70,29 @@ bool cuda_ok(cudaError_t e, pe_error* err, const char* what) {
   return false;
 }
 
-__global__ void pe_eval_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
-                               unsigned int* counter, const pe_action* acts,
-                               const uint32_t* off, uint32_t n, pe_cost_params cp,
-                               int64_t baseline, pe_result* out, int32_t* trace,
-                               uint32_t trace_words) {
+constexpr int kBlock = 128;
+constexpr int kMinBlocks = 4;  // 16 warps / SM: caps registers at 128 per thread
+
+#ifdef PE_PHASE_TIMERS
+// profiling build only (tools/phase_profile.py): summed clock64 per phase
+__device__ unsigned long long g_phase_cycles[9];
+#endif
+
+// One thread per candidate.  Candidates are assigned statically (i = slot,
+// slot + slots, ...) so the 32 lanes of a warp start their candidates
+// together and stay in similar phases of the sweep (SIMT efficiency).
+// RETRY launches re-evaluate, in full-size arenas, exactly the candidates
+// whose tight arena overflowed (status PE_CAND_CAPACITY).
+template <bool RETRY>
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
+pe_eval_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
+               const pe_action* acts, const uint32_t* off, uint32_t n, pe_cost_params cp,
+               int64_t baseline, pe_result* out, int32_t* trace, uint32_t trace_words) {
   uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)slot * L.bytes);
-  for (;;) {
-    uint32_t i = atomicAdd(counter, 1u);
-    if (i >= n) break;
+  for (uint32_t i = slot; i < n; i += slots) {
+    if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
     c.eval(acts + off[i], (int32_t)(off[i + 1] - off[i]), cp, baseline, r,
            trace ? trace + (uint64_t)i * trace_words : nullptr, trace_words);
@@ -84,27 +100,28 @@ __global__ void pe_eval_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, ui
   }
 }
 
-__global__ void pe_rollout_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
-                                  unsigned int* counter, const pe_action* prefix,
-                                  const uint32_t* poff, const uint64_t* seeds, uint32_t n,
-                                  int32_t maxd, pe_cost_params cp, int64_t baseline,
-                                  pe_action* acts_out, uint32_t* n_out, pe_result* out,
-                                  uint64_t* legal_out, int32_t legal_words) {
+template <bool RETRY>
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
+pe_rollout_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
+                  const pe_action* prefix, const uint32_t* poff, const uint64_t* seeds,
+                  uint32_t n, int32_t maxd, pe_cost_params cp, int64_t baseline,
+                  pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
+                  int32_t legal_words) {
   uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)slot * L.bytes);
-  for (;;) {
-    uint32_t i = atomicAdd(counter, 1u);
-    if (i >= n) break;
+  for (uint32_t i = slot; i < n; i += slots) {
+    if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
     c.rollout(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, cp, baseline,
               acts_out + (uint64_t)i * maxd, n_out + i, r,
               legal_out ? legal_out + (uint64_t)i * legal_words : nullptr, legal_words);
     out[i] = r;
   }
+#ifdef PE_PHASE_TIMERS
+  for (int k = 0; k < 9; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)c.ph[k]);
+#endif
 }
-
-constexpr int kBlock = 128;
 
 // Append a host vector to the device image; returns its offset.
 template <typename T>
@@ -286,6 +303,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
     pe_engine_destroy(e);
     return PE_ERR_CUDA;
   }
+  e->graph_bytes = (int64_t)img.size();
   pe::GraphView v = g.host_view();
   uint8_t* b = e->d_graph;
   v.vshape = (const int32_t*)(b + o_vshape);
@@ -319,16 +337,30 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   e->dview = v;
 
   // per-candidate arenas: one per thread slot, bounded by an HBM budget
-  e->layout = pe::make_layout(v);
+  e->layout = pe::make_layout(v, /*tight=*/true);
+  e->big_layout = pe::make_layout(v, /*tight=*/false);
+  if (const char* dbg = std::getenv("PE_DEBUG_TIGHT_EM_CAP")) {
+    // test hook: shrink the tight arena so candidates overflow and take the
+    // retry path (tests/test_gpu_parity.py::test_capacity_retry_path)
+    pe::Caps c = e->layout.caps;
+    c.EM = std::max(4, std::atoi(dbg));
+    e->layout = pe::relayout(v, c);
+  }
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  size_t budget = std::min<size_t>(free_b / 2, (size_t)24 << 30);
-  uint64_t want = (uint64_t)e->sm_count * 256;  // resident threads worth of slots
-  uint64_t fit = budget / std::max<uint64_t>(e->layout.bytes, 1);
+  size_t budget = std::min<size_t>(free_b / 2, (size_t)48 << 30);
+  // one resident thread per slot: kMinBlocks blocks of kBlock threads per SM
+  uint64_t want = (uint64_t)e->sm_count * kBlock * kMinBlocks;
+  e->big_slots = (uint32_t)std::min<uint64_t>(
+      (uint64_t)e->sm_count * 8,
+      std::max<uint64_t>(1, (budget / 8) / std::max<uint64_t>(e->big_layout.bytes, 1)));
+  uint64_t fit = (budget - (uint64_t)e->big_slots * e->big_layout.bytes) /
+                 std::max<uint64_t>(e->layout.bytes, 1);
   e->slots = (uint32_t)std::max<uint64_t>(1, std::min(want, fit));
   if (!cuda_ok(cudaMalloc(&e->d_arena, (size_t)e->slots * e->layout.bytes), err,
                "cudaMalloc(arena)") ||
-      !cuda_ok(cudaMalloc(&e->d_counter, sizeof(unsigned int)), err, "cudaMalloc(counter)")) {
+      !cuda_ok(cudaMalloc(&e->d_big_arena, (size_t)e->big_slots * e->big_layout.bytes), err,
+               "cudaMalloc(big arena)")) {
     pe_engine_destroy(e);
     return PE_ERR_CUDA;
   }
@@ -358,7 +390,7 @@ void pe_engine_destroy(pe_engine* e) {
   if (!e) return;
   if (e->d_graph) cudaFree(e->d_graph);
   if (e->d_arena) cudaFree(e->d_arena);
-  if (e->d_counter) cudaFree(e->d_counter);
+  if (e->d_big_arena) cudaFree(e->d_big_arena);
   if (e->d_io) cudaFree(e->d_io);
   delete e;
 }
@@ -369,6 +401,7 @@ int64_t pe_engine_baseline_bytes(const pe_engine* e) { return e->baseline; }
 int64_t pe_engine_arena_bytes(const pe_engine* e) { return (int64_t)e->layout.bytes; }
 uint32_t pe_engine_slots(const pe_engine* e) { return e->slots; }
 uint64_t pe_engine_launch_count(const pe_engine* e) { return e->launches; }
+int64_t pe_engine_graph_bytes(const pe_engine* e) { return e->graph_bytes; }
 
 pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* out) {
   if (!out || ord >= e->n_ordinals) return PE_ERR_INVALID_ARGUMENT;
@@ -420,13 +453,15 @@ pe_status pe_eval_batch(pe_engine* e, const pe_action* acts, const uint32_t* seq
                                  cudaMemcpyHostToDevice, st), err, "H2D offsets"))
       return PE_ERR_CUDA;
   }
-  if (!cuda_ok(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned int), st), err, "memset"))
-    return PE_ERR_CUDA;
   uint32_t slots = launch_slots(e, n);
-  pe_eval_kernel<<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
-      e->dview, e->layout, e->d_arena, slots, e->d_counter, d_acts, d_off, n, e->cp,
-      e->baseline, d_out, d_trace, trace_words);
-  e->launches++;
+  pe_eval_kernel<false><<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+      e->dview, e->layout, e->d_arena, slots, d_acts, d_off, n, e->cp, e->baseline, d_out,
+      d_trace, trace_words);
+  uint32_t bs = std::min<uint32_t>(e->big_slots, n);
+  pe_eval_kernel<true><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+      e->dview, e->big_layout, e->d_big_arena, bs, d_acts, d_off, n, e->cp, e->baseline, d_out,
+      d_trace, trace_words);
+  e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "pe_eval_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {
     if (!cuda_ok(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(pe_result),
@@ -498,13 +533,15 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
                                  st), err, "H2D seeds"))
       return PE_ERR_CUDA;
   }
-  if (!cuda_ok(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned int), st), err, "memset"))
-    return PE_ERR_CUDA;
   uint32_t slots = launch_slots(e, n);
-  pe_rollout_kernel<<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
-      e->dview, e->layout, e->d_arena, slots, e->d_counter, d_prefix, d_poff, d_seeds, n, maxd,
-      e->cp, e->baseline, d_acts, d_nacts, d_out, d_legal, lw);
-  e->launches++;
+  pe_rollout_kernel<false><<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+      e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff, d_seeds, n, maxd, e->cp,
+      e->baseline, d_acts, d_nacts, d_out, d_legal, lw);
+  uint32_t bs = std::min<uint32_t>(e->big_slots, n);
+  pe_rollout_kernel<true><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+      e->dview, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff, d_seeds, n, maxd, e->cp,
+      e->baseline, d_acts, d_nacts, d_out, d_legal, lw);
+  e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "pe_rollout_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {
     bool ok = cuda_ok(cudaMemcpyAsync(acts_out, d_acts, (size_t)n * maxd * sizeof(pe_action),
@@ -525,3 +562,15 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
 }
 
 }  // extern "C"
+
+#ifdef PE_PHASE_TIMERS
+extern "C" int pe_debug_phase_cycles(unsigned long long* out9, int reset) {
+  if (cudaMemcpyFromSymbol(out9, g_phase_cycles, sizeof(unsigned long long) * 9) != cudaSuccess)
+    return 1;
+  if (reset) {
+    unsigned long long z[9] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -159,6 +159,9 @@ class Engine:
     def launch_count(self) -> int:
         return int(self.lib.pe_engine_launch_count(self.h))
 
+    def graph_bytes(self) -> int:
+        return int(self.lib.pe_engine_graph_bytes(self.h))
+
     def arena_bytes(self) -> int:
         return int(self.lib.pe_engine_arena_bytes(self.h))
 

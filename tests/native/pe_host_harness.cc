@@ -128,6 +128,30 @@ int harness_rollout_batch(const char* pir, size_t len, const pe_search_config* c
   return 0;
 }
 
+// High-water marks of the arena counters over a batch of rollouts, relative
+// to the graph size: {slots - (A+N), loops, front stack, spmd ops, operands}.
+int harness_highwater(const char* pir, size_t len, const pe_search_config* cfg,
+                      const uint64_t* seeds, uint32_t n, int64_t* out5) {
+  Harness h;
+  char err[256];
+  if (setup(h, pir, len, cfg, nullptr, err, sizeof(err))) return 1;
+  pe::Cand c(h.v, h.L, h.arena.data());
+  int32_t maxd = (int32_t)h.cfg.max_decisions;
+  std::vector<pe_action> acts(maxd);
+  for (int k = 0; k < 5; ++k) out5[k] = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    uint32_t na;
+    pe_result r;
+    c.rollout(nullptr, 0, seeds[i], maxd, h.cp, h.baseline, acts.data(), &na, r, nullptr, 0);
+    out5[0] = std::max<int64_t>(out5[0], c.nslots - (h.v.A + h.v.N));
+    out5[1] = std::max<int64_t>(out5[1], c.nloops);
+    out5[2] = std::max<int64_t>(out5[2], c.nfs);
+    out5[3] = std::max<int64_t>(out5[3], c.nem);
+    out5[4] = std::max<int64_t>(out5[4], c.neo);
+  }
+  return 0;
+}
+
 int64_t harness_arena_bytes(const char* pir, size_t len) {
   Harness h;
   char err[256];

@@ -99,3 +99,18 @@ def test_gpt2_medium_grouped_megatron_dp(oracle_lib):
     r = res[0]
     assert r.ar_cnt[1] == 48 and r.ar_bytes[1] == 1610612736
     assert r.ag_cnt[0] == 48 and r.ag_bytes[0] == 1207959552
+
+
+def test_capacity_retry_path(oracle_lib, monkeypatch):
+    # force the tight arena to overflow: every candidate must take the retry
+    # kernel (full-size arena) and still match the oracle exactly
+    monkeypatch.setenv("PE_DEBUG_TIGHT_EM_CAP", "8")
+    text = modelgen.config_program(2)
+    cfg = capi.default_search_config(group_scopes=1)
+    eng = _engine(text, cfg)
+    n = 256
+    res, seqs, _ = eng.rollout_batch([[]] * n, list(range(n)))
+    ref, rseqs, _ = H.rollout_batch("oracle", text, [[]] * n, list(range(n)), cfg)
+    assert seqs == rseqs
+    assert all(r.status == 0 for r in res)
+    assert all(not H.compare_results(a, b) for a, b in zip(res, ref))

@@ -13,3 +13,13 @@ for cfgno in (2, 3):
         torch.cuda.synchronize()
         t=time.time(); res, seqs, _ = eng.rollout_batch([[]]*n, seeds); dt=time.time()-t
         print(f"  n={n} {n/dt:.0f} cand/s  ({dt*1e3:.1f} ms)  mean steps {sum(r.n_steps for r in res)/n:.2f} status0 {sum(r.status==0 for r in res)}")
+import helpers as H
+text = modelgen.config_program(3)
+cfg = capi.default_search_config(group_scopes=1)
+n=32
+t=time.time(); H.rollout_batch("oracle", text, [[]]*n, list(range(n)), cfg, threads=os.cpu_count()); dt=time.time()-t
+print(f"oracle cfg3 {os.cpu_count()} threads: {n/dt:.2f} cand/s")
+text = modelgen.config_program(2)
+n=512
+t=time.time(); H.rollout_batch("oracle", text, [[]]*n, list(range(n)), cfg, threads=os.cpu_count()); dt=time.time()-t
+print(f"oracle cfg2 {os.cpu_count()} threads: {n/dt:.2f} cand/s")
