@@ -54,43 +54,65 @@ struct Caps {
   int32_t EO;  // emitted operand references
 };
 
+// Per-candidate arena, packed as 32-byte records so that the fields a sweep
+// touches together share one sector:
+//   VRec[V]     value slot:  vk, vref, vaux, uses, slcnt, body links, position
+//   LowRec[V]   lowered view (REF spmd.cc:42 `Lowered`): buffer, spec, acq, shape
+//   ArgRec[A]   per argument: direct-in-loop count, slice demand, atomic flag
+//   LoopRec[L]  tile / sum loop: kind, axis, dim, body list, yield, result type
+//   EmRec[EM+1] emitted SPMD op: head, operand offset, last use, local bytes
+//   BRec[A+EM]  final registered DistType of every SPMD buffer (bytes, spec)
+// plus flat int arrays (operands, top-level positions, stuck list).
+template <typename T, int STRIDE>
+struct Field {
+  uint8_t* p;
+  PE_HD T& operator[](int64_t i) const { return *reinterpret_cast<T*>(p + i * STRIDE); }
+};
+
+constexpr int kRec = 32;
+constexpr int kEmRec = 64;
+
 struct Layout {
   Caps caps;
   // byte offsets inside one candidate arena
-  uint64_t vk, vref, vaux, uses, slcnt, bnext, bprev, vpos;
-  uint64_t lo_buf, lo_spec, lo_acq, lo_g;
-  uint64_t opnd, adirect, aslice, awrapped, aspec0, alb0;
-  uint64_t lkind, laxis, ldim, lhead, ltail, lyield, ltype;
-  uint64_t pos, fs, stk, seen;
-  uint64_t em_head, em_ooff, em_lb, em_last, em_opnd, b_gb, b_lb, b_spec, delta;
+  uint64_t vrec, lrec, arec, looprec, emrec;
+  uint64_t opnd, pos, fs, stk, seen, em_opnd, carry, lg;
   uint64_t bytes;
 };
 
 struct Arena {
-  uint8_t* vk;
-  int32_t *vref, *vaux, *uses, *slcnt, *bnext, *bprev, *vpos;
-  int32_t* lo_buf;
-  uint32_t* lo_spec;
-  uint8_t* lo_acq;
-  int32_t* lo_g;
-  int32_t *opnd, *adirect, *aslice;
-  uint8_t* awrapped;
-  uint32_t* aspec0;
-  int64_t* alb0;
-  uint8_t *lkind, *laxis;
-  int8_t* ldim;
-  int32_t *lhead, *ltail, *lyield, *ltype;
-  int32_t *pos, *fs, *stk;
+  // VRec
+  Field<uint8_t, kRec> vk;
+  Field<int32_t, kRec> vref, vaux, uses, slcnt, bnext, bprev, vpos;
+  // LowRec
+  uint8_t* lo_base;
+  Field<int32_t, kRec> lo_buf;
+  Field<uint32_t, kRec> lo_spec;
+  Field<uint8_t, kRec> lo_acq;
+  // ArgRec (64 B)
+  Field<int32_t, 2 * kRec> adirect, aslice;
+  Field<uint8_t, 2 * kRec> awrapped;
+  Field<uint32_t, 2 * kRec> aspec0;
+  Field<int64_t, 2 * kRec> alb0;
+  // LoopRec
+  Field<uint8_t, kRec> lkind, laxis;
+  Field<int8_t, kRec> ldim;
+  Field<int32_t, kRec> lhead, ltail, lyield, ltype;
+  // EmRec
+  Field<int64_t, 2 * kRec> arg_gb, arg_lb;
+  Field<uint32_t, 2 * kRec> arg_spec;
+  // EmRec (64 B): emitted op + final registered DistType of its buffer
+  Field<int32_t, kEmRec> em_head, em_op0, em_last, em_ooff;
+  Field<int64_t, kEmRec> em_lb, delta, em_gb, em_blb;
+  Field<uint32_t, kEmRec> em_spec;
+  // flat
+  int32_t *opnd, *pos, *fs, *stk, *em_opnd, *lg;
+  uint32_t* carry;  // bit per argument: carries tiling (sliced or atomic)
   uint8_t* seen;
-  int32_t *em_head, *em_ooff;
-  int64_t* em_lb;
-  int32_t *em_last, *em_opnd;
-  int64_t *b_gb, *b_lb;
-  uint32_t* b_spec;
-  int64_t* delta;
 };
 
 PE_HD uint64_t align8(uint64_t x) { return (x + 7) & ~uint64_t(7); }
+PE_HD uint64_t align128(uint64_t x) { return (x + 127) & ~uint64_t(127); }
 
 inline Layout relayout(const GraphView& g, const Caps& caps);
 
@@ -130,92 +152,79 @@ inline Layout relayout(const GraphView& g, const Caps& caps) {
   uint64_t o = 0;
   auto take = [&](uint64_t bytes) {
     uint64_t at = o;
-    o = align8(o + bytes);
+    o = align128(o + bytes);
     return at;
   };
   int64_t V = L.caps.V, Lc = L.caps.L, EM = L.caps.EM;
-  L.vk = take(V);
-  L.vref = take(4 * V);
-  L.vaux = take(4 * V);
-  L.uses = take(4 * V);
-  L.slcnt = take(4 * V);
-  L.bnext = take(4 * V);
-  L.bprev = take(4 * V);
-  L.vpos = take(4 * V);
-  L.lo_buf = take(4 * V);
-  L.lo_spec = take(4 * V);
-  L.lo_acq = take(V);
-  L.lo_g = take(16 * V);
+  L.vrec = take(kRec * V);
+  L.lrec = take(kRec * V);
+  L.arec = take(2 * kRec * ((int64_t)A + 1));
+  L.looprec = take(kRec * Lc);
+  L.emrec = take(kEmRec * (EM + 1));
   L.opnd = take(4 * (int64_t)E + 4);
-  L.adirect = take(4 * (int64_t)A + 4);
-  L.aslice = take(4 * (int64_t)A + 4);
-  L.awrapped = take((int64_t)A + 4);
-  L.aspec0 = take(4 * (int64_t)A + 4);
-  L.alb0 = take(8 * (int64_t)A + 8);
-  L.lkind = take(Lc);
-  L.laxis = take(Lc);
-  L.ldim = take(Lc);
-  L.lhead = take(4 * Lc);
-  L.ltail = take(4 * Lc);
-  L.lyield = take(4 * Lc);
-  L.ltype = take(4 * Lc);
   L.pos = take(8 * (int64_t)N + 8);
   L.fs = take(4 * (int64_t)L.caps.FS);
   L.stk = take(8 * (int64_t)N + 8);
   L.seen = take((int64_t)N + 8);
-  L.em_head = take(4 * EM);
-  L.em_ooff = take(4 * EM + 4);
-  L.em_lb = take(8 * EM);
-  L.em_last = take(4 * EM);
   L.em_opnd = take(4 * (int64_t)L.caps.EO);
-  L.b_gb = take(8 * (EM + A));
-  L.b_lb = take(8 * (EM + A));
-  L.b_spec = take(4 * (EM + A));
-  L.delta = take(8 * EM + 8);
-  L.bytes = align8(o);
+  L.carry = take(4 * ((int64_t)A / 32 + 2));
+  L.lg = take(4 * ((int64_t)g.n_ord + 1));
+  L.bytes = align128(o);
   return L;
 }
 
 PE_HD Arena carve(const Layout& L, uint8_t* base) {
   Arena a;
-  a.vk = base + L.vk;
-  a.vref = (int32_t*)(base + L.vref);
-  a.vaux = (int32_t*)(base + L.vaux);
-  a.uses = (int32_t*)(base + L.uses);
-  a.slcnt = (int32_t*)(base + L.slcnt);
-  a.bnext = (int32_t*)(base + L.bnext);
-  a.bprev = (int32_t*)(base + L.bprev);
-  a.vpos = (int32_t*)(base + L.vpos);
-  a.lo_buf = (int32_t*)(base + L.lo_buf);
-  a.lo_spec = (uint32_t*)(base + L.lo_spec);
-  a.lo_acq = base + L.lo_acq;
-  a.lo_g = (int32_t*)(base + L.lo_g);
+  uint8_t* v = base + L.vrec;
+  a.vk = {v + 0};
+  a.vref = {v + 4};
+  a.vaux = {v + 8};
+  a.uses = {v + 12};
+  a.slcnt = {v + 16};
+  a.bnext = {v + 20};
+  a.bprev = {v + 24};
+  a.vpos = {v + 28};
+  uint8_t* lo = base + L.lrec;
+  a.lo_base = lo;
+  a.lo_buf = {lo + 0};
+  a.lo_spec = {lo + 4};
+  a.lo_acq = {lo + 8};
+  // ArgRec is 64 B: state (0..23) + the buffer's final registered type (24..47)
+  uint8_t* ar = base + L.arec;
+  a.adirect = {ar + 0};
+  a.aslice = {ar + 4};
+  a.awrapped = {ar + 8};
+  a.aspec0 = {ar + 12};
+  a.alb0 = {ar + 16};
+  a.arg_gb = {ar + 24};
+  a.arg_lb = {ar + 32};
+  a.arg_spec = {ar + 40};
+  uint8_t* lr = base + L.looprec;
+  a.lkind = {lr + 0};
+  a.laxis = {lr + 1};
+  a.ldim = {lr + 2};
+  a.lhead = {lr + 4};
+  a.ltail = {lr + 8};
+  a.lyield = {lr + 12};
+  a.ltype = {lr + 16};
+  uint8_t* em = base + L.emrec;
+  a.em_head = {em + 0};
+  a.em_op0 = {em + 4};
+  a.em_last = {em + 8};
+  a.em_ooff = {em + 12};
+  a.em_lb = {em + 16};
+  a.delta = {em + 24};
+  a.em_gb = {em + 32};
+  a.em_blb = {em + 40};
+  a.em_spec = {em + 48};
   a.opnd = (int32_t*)(base + L.opnd);
-  a.adirect = (int32_t*)(base + L.adirect);
-  a.aslice = (int32_t*)(base + L.aslice);
-  a.awrapped = base + L.awrapped;
-  a.aspec0 = (uint32_t*)(base + L.aspec0);
-  a.alb0 = (int64_t*)(base + L.alb0);
-  a.lkind = base + L.lkind;
-  a.laxis = base + L.laxis;
-  a.ldim = (int8_t*)(base + L.ldim);
-  a.lhead = (int32_t*)(base + L.lhead);
-  a.ltail = (int32_t*)(base + L.ltail);
-  a.lyield = (int32_t*)(base + L.lyield);
-  a.ltype = (int32_t*)(base + L.ltype);
   a.pos = (int32_t*)(base + L.pos);
   a.fs = (int32_t*)(base + L.fs);
   a.stk = (int32_t*)(base + L.stk);
   a.seen = base + L.seen;
-  a.em_head = (int32_t*)(base + L.em_head);
-  a.em_ooff = (int32_t*)(base + L.em_ooff);
-  a.em_lb = (int64_t*)(base + L.em_lb);
-  a.em_last = (int32_t*)(base + L.em_last);
   a.em_opnd = (int32_t*)(base + L.em_opnd);
-  a.b_gb = (int64_t*)(base + L.b_gb);
-  a.b_lb = (int64_t*)(base + L.b_lb);
-  a.b_spec = (uint32_t*)(base + L.b_spec);
-  a.delta = (int64_t*)(base + L.delta);
+  a.carry = (uint32_t*)(base + L.carry);
+  a.lg = (int32_t*)(base + L.lg);
   return a;
 }
 
@@ -258,6 +267,7 @@ struct Cand {
   int32_t status;
   int64_t flops;
   int32_t result_buf;
+  bool tracing = false;  // keep the full SPMD operand log (parity trace only)
 #if defined(PE_PHASE_TIMERS) && defined(__CUDA_ARCH__)
   // profiling build only: clock64 cycles per phase
   // 0 init 1 apply 2 forward 3 backward 4 wrap 5 legal 6 analyze 7 lower 8 score
@@ -288,8 +298,21 @@ struct Cand {
   PE_HD bool bad() const { return status == PE_CAND_INTERNAL || status == PE_CAND_CAPACITY; }
   PE_HD int32_t NV() const { return g.A + g.N; }
   PE_HD int64_t asz(int32_t ax) const { return g.axis_size[ax]; }
-  PE_HD bool is_tile_loop(int32_t v) const {
-    return a.vk[v] == VK_LOOP && a.lkind[a.vref[v]] == LK_TILE;
+  // VRec header word: vk | tile-loop flag << 8 | loop axis << 16 | loop dim << 24
+  // (loop axis/dim denormalised into the value record so the sweeps test
+  // "operand is a tile loop on (axis, dim)" with one load)
+  PE_HD uint32_t vhdr(int32_t v) const {
+    return *reinterpret_cast<const uint32_t*>(a.vk.p + (int64_t)v * kRec);
+  }
+  PE_HD static bool hdr_tile(uint32_t h) { return (h & 0x1FFu) == (VK_LOOP | 0x100u); }
+  PE_HD static int32_t hdr_axis(uint32_t h) { return (int32_t)((h >> 16) & 0xFFu); }
+  PE_HD static int32_t hdr_dim(uint32_t h) { return (int32_t)(int8_t)(h >> 24); }
+  PE_HD bool is_tile_loop(int32_t v) const { return hdr_tile(vhdr(v)); }
+  // refresh the denormalised loop info of loop value v (loop record l)
+  PE_HD void mark_loop_value(int32_t v, int32_t l) {
+    uint32_t h = (uint32_t)VK_LOOP | ((a.lkind[l] == LK_TILE ? 1u : 0u) << 8) |
+                 ((uint32_t)a.laxis[l] << 16) | ((uint32_t)(uint8_t)a.ldim[l] << 24);
+    *reinterpret_cast<uint32_t*>(a.vk.p + (int64_t)v * kRec) = h;
   }
   // original value whose global shape a top-level value carries
   PE_HD int32_t shape_src(int32_t v) const {
@@ -366,6 +389,7 @@ struct Cand {
   PE_HD void slice_created(int32_t u, int32_t d, int32_t axis) {
     a.slcnt[u]++;
     if (u < g.A) {
+      a.carry[u >> 5] |= 1u << (u & 31);
       int32_t pair = d | (axis << 3);
       if (a.aslice[u] == -1) a.aslice[u] = pair;
       else if (a.aslice[u] != pair) a.aslice[u] = -2;
@@ -400,6 +424,7 @@ struct Cand {
       a.pos[2 * o + 1] = -1;
     }
     for (int32_t s = 0; s < g.E; ++s) a.opnd[s] = g.oopnd[s];
+    for (int32_t w = 0; w <= (A >> 5); ++w) a.carry[w] = 0;
     nslots = A + N;
     nloops = 0;
     nfs = 0;
@@ -439,8 +464,8 @@ struct Cand {
     a.ldim[l] = (int8_t)dim;
     a.ltype[l] = v;
     a.lyield[l] = s;
-    a.vk[ls] = VK_LOOP;
     a.vref[ls] = l;
+    mark_loop_value(ls, l);
     a.uses[ls] = a.uses[v];
     a.vk[s] = VK_SLICE;
     a.vref[s] = v;
@@ -482,9 +507,9 @@ struct Cand {
     int32_t cbase = g.ocls_off[o];
     for (int32_t k = 0; k < n; ++k) {
       int32_t u = a.opnd[base + k];
-      if (!is_tile_loop(u)) continue;
-      int32_t L = a.vref[u];
-      int32_t c = g.slot_cls[(base + k) * 4 + a.ldim[L]];
+      uint32_t h = vhdr(u);
+      if (!hdr_tile(h)) continue;
+      int32_t c = g.slot_cls[(base + k) * 4 + hdr_dim(h)];
       if (c < 0 || g.cls_role[cbase + c] == kBlocked) {
         p.reason = R_BLOCKED;
         return p;
@@ -492,15 +517,14 @@ struct Cand {
       if (p.drive < 0) {
         p.drive = u;
         p.cls = c;
-        p.axis = a.laxis[L];
+        p.axis = hdr_axis(h);
       }
     }
     if (p.drive < 0) return p;
     for (int32_t k = 0; k < n; ++k) {
-      int32_t u = a.opnd[base + k];
-      if (!is_tile_loop(u)) continue;
-      int32_t L = a.vref[u];
-      if (a.laxis[L] == p.axis && g.slot_cls[(base + k) * 4 + a.ldim[L]] != p.cls) {
+      uint32_t h = vhdr(a.opnd[base + k]);
+      if (!hdr_tile(h)) continue;
+      if (hdr_axis(h) == p.axis && g.slot_cls[(base + k) * 4 + hdr_dim(h)] != p.cls) {
         p.reason = R_CONFLICT;
         return p;
       }
@@ -514,9 +538,9 @@ struct Cand {
         p.reason = R_INSUFFICIENT;
         return p;
       }
-      if (is_tile_loop(u)) {
-        int32_t L = a.vref[u];
-        bool sa = a.laxis[L] == p.axis, sd = a.ldim[L] == d;
+      uint32_t h = vhdr(u);
+      if (hdr_tile(h)) {
+        bool sa = hdr_axis(h) == p.axis, sd = hdr_dim(h) == d;
         if (sa != sd) {
           p.reason = R_CONFLICT;
           return p;
@@ -616,8 +640,8 @@ struct Cand {
       a.vk[lv0] = VK_DEAD;
     }
     int32_t xv = g.A + o;
-    a.vk[xv] = VK_LOOP;
     a.vref[xv] = l;
+    mark_loop_value(xv, l);
   }
 
   PE_HD void forward() {
@@ -670,9 +694,9 @@ struct Cand {
                 int32_t k = g.mem[m] >> 2, dd = g.mem[m] & 3;
                 int32_t w = a.opnd[pb + k];
                 if (g.shape(shape_src(w))[dd] % sz != 0) go = false;
-                if (is_tile_loop(w)) {
-                  int32_t L2 = a.vref[w];
-                  bool sa = a.laxis[L2] == sz_axis, sd = a.ldim[L2] == dd;
+                uint32_t h = vhdr(w);
+                if (hdr_tile(h)) {
+                  bool sa = hdr_axis(h) == sz_axis, sd = hdr_dim(h) == dd;
                   if (sa != sd) go = false;
                 }
               }
@@ -775,6 +799,7 @@ struct Cand {
       replace_uses(x, t);
       a.uses[x] = 1;
       a.awrapped[x] = 1;
+      a.carry[x >> 5] |= 1u << (x & 31);
       push_front(t);
       if (bad()) return;
     }
@@ -865,23 +890,32 @@ struct Cand {
     return e;
   }
   PE_HD Low load(int32_t v) const {
+    const int32_t* r = reinterpret_cast<const int32_t*>(a.lo_base + (int64_t)v * kRec);
     Low w;
-    w.buf = a.lo_buf[v];
-    w.spec = a.lo_spec[v];
-    w.acq = a.lo_acq[v];
-    for (int d = 0; d < kMaxRank; ++d) w.g[d] = a.lo_g[4 * v + d];
+    w.buf = r[0];
+    w.spec = (uint32_t)r[1];
+    w.acq = (uint32_t)r[2] & 0xFFu;
+    for (int d = 0; d < kMaxRank; ++d) w.g[d] = r[3 + d];
     return w;
   }
   PE_HD void store(int32_t v, const Low& w) {
-    a.lo_buf[v] = w.buf;
-    a.lo_spec[v] = w.spec;
-    a.lo_acq[v] = (uint8_t)w.acq;
-    for (int d = 0; d < kMaxRank; ++d) a.lo_g[4 * v + d] = w.g[d];
+    int32_t* r = reinterpret_cast<int32_t*>(a.lo_base + (int64_t)v * kRec);
+    r[0] = w.buf;
+    r[1] = (int32_t)w.spec;
+    r[2] = (int32_t)w.acq;
+    for (int d = 0; d < kMaxRank; ++d) r[3 + d] = w.g[d];
   }
   PE_HD void register_type(int32_t buf, const Low& w) {
-    a.b_gb[buf] = global_bytes(w);
-    a.b_lb[buf] = 4 * local_elems(w);
-    a.b_spec[buf] = w.spec;
+    int64_t gb = global_bytes(w), lb = 4 * local_elems(w);
+    if (buf < g.A) {
+      a.arg_gb[buf] = gb;
+      a.arg_lb[buf] = lb;
+      a.arg_spec[buf] = w.spec;
+    } else {
+      a.em_gb[buf - g.A] = gb;
+      a.em_blb[buf - g.A] = lb;
+      a.em_spec[buf - g.A] = w.spec;
+    }
   }
   // opens an SPMD op; operands appended with add_operand
   PE_HD int32_t new_op(int32_t kind, int32_t axis, int32_t dim, int32_t nopnd) {
@@ -893,14 +927,15 @@ struct Cand {
     a.em_head[j] = kind | ((axis + 1) << 8) | ((dim + 1) << 12) | (nopnd << 16);
     a.em_ooff[j] = neo;
     a.em_last[j] = j;
+    a.em_op0[j] = -1;
     return j;
   }
   PE_HD void add_operand(int32_t j, int32_t buf) {
-    a.em_opnd[neo++] = buf;
-    if (buf >= g.A) {
-      int32_t jj = buf - g.A;
-      if (a.em_last[jj] < j) a.em_last[jj] = j;
-    }
+    if (tracing) a.em_opnd[neo] = buf;
+    if (a.em_op0[j] < 0) a.em_op0[j] = buf;
+    ++neo;
+    // ops are emitted in order, so the current op is always the latest use
+    if (buf >= g.A) a.em_last[buf - g.A] = j;
   }
   PE_HD int32_t pending_front(uint32_t spec) const {
     uint32_t pm = spec_pending(spec);
@@ -933,33 +968,43 @@ struct Cand {
     register_type(w.buf, w);
   }
   // materialize_for_direct_use (REF spmd.cc:119-129); loop_axis = -1 at top
-  PE_HD void materialize(int32_t v, int32_t loop_axis) {
+  PE_HD Low materialize(int32_t v, int32_t loop_axis) {
     Low w = load(v);
+    int32_t b0 = w.buf;
     int r = rank_of_spec(w.spec);
     for (int d = 0; d < r; ++d) {
       uint32_t ax1 = spec_axis(w.spec, d);
       if (!ax1) continue;
       bool live = loop_axis >= 0 && (int32_t)ax1 - 1 == loop_axis && ((w.acq >> d) & 1);
       if (!live) emit_gather(w, d);
-      if (bad()) return;
+      if (bad()) return w;
     }
     while (spec_pending(w.spec)) {
       emit_all_reduce(w, pending_front(w.spec));
-      if (bad()) return;
+      if (bad()) return w;
     }
-    store(v, w);
+    // every gather / all_reduce moves the record to a new buffer
+    if (w.buf != b0) store(v, w);
+    return w;
   }
 
   // lower_base (REF spmd.cc:256-323 with patch B) for a top-level op
-  // (l = -1) or a per-iteration copy in loop l.
+  // (l = -1) or a per-iteration copy in loop l.  The first two operand
+  // records are kept in registers after materialisation (every kind but
+  // concatenate has <= 2 operands).
   PE_HD void lower_base(int32_t v, int32_t o, int32_t l) {
     int32_t base = g.oopnd_off[o], n = g.oopnd_off[o + 1] - base;
     int32_t lax = l >= 0 ? (int32_t)a.laxis[l] : -1;
     uint8_t kind = g.okind[o];
+    Low in0, in1;
     for (int32_t k = 0; k < n; ++k) {
-      materialize(a.opnd[base + k], lax);
+      Low w = materialize(a.opnd[base + k], lax);
       if (bad()) return;
+      if (k == 0) in0 = w;
+      else if (k == 1) in1 = w;
     }
+    // a repeated operand (mul(x, x)) sees the record its first use stored
+    if (n > 1 && a.opnd[base] == a.opnd[base + 1]) in0 = in1;
     Low r;
     int32_t xv = g.A + o;
     int rank = g.vrank[xv];
@@ -971,57 +1016,54 @@ struct Cand {
     r.spec = (uint32_t)rank << 24;
     r.acq = 0;
     r.buf = -1;
-    for (int32_t k = 0; k < n; ++k) r.spec |= spec_pending(a.lo_spec[a.opnd[base + k]]) << 16;
-    if (kind != kConstant) {
-      for (int32_t k = 0; k < n; ++k) {
-        Low w = load(a.opnd[base + k]);
-        int wr = rank_of_spec(w.spec);
-        bool any = false;
-        for (int d = 0; d < wr; ++d) any |= spec_axis(w.spec, d) != 0;
-        if (!any) continue;
-        ReshapeRule rr;
-        if (kind == kReshape) {
-          int64_t in[kMaxRank];
-          for (int d = 0; d < wr; ++d) in[d] = local_dim(w, d);
-          rr = reshape_rule(in, wr, r.g, rank);
-          if (rr.error) {
-            fail(PE_CAND_INTERNAL);
-            return;
-          }
+    for (int32_t k = 0; k < n; ++k) {
+      Low w = k == 0 ? in0 : k == 1 ? in1 : load(a.opnd[base + k]);
+      r.spec |= spec_pending(w.spec) << 16;
+      if (kind == kConstant) continue;
+      int wr = rank_of_spec(w.spec);
+      if ((w.spec & 0xFFFFu) == 0) continue;  // no sharded dim
+      ReshapeRule rr;
+      if (kind == kReshape) {
+        int64_t in[kMaxRank];
+        for (int d = 0; d < wr; ++d) in[d] = local_dim(w, d);
+        rr = reshape_rule(in, wr, r.g, rank);
+        if (rr.error) {
+          fail(PE_CAND_INTERNAL);
+          return;
         }
-        for (int d = 0; d < wr; ++d) {
-          uint32_t ax1 = spec_axis(w.spec, d);
-          if (!ax1) continue;
-          int role, rdim;
-          if (kind == kReshape) {
-            int c = rr.cls_of_dim[d];
-            if (c < 0) {
-              fail(PE_CAND_INTERNAL);
-              return;
-            }
-            role = rr.role[c];
-            rdim = rr.rdim[c];
-          } else {
-            int c = g.slot_cls[(base + k) * 4 + d];
-            if (c < 0) {
-              fail(PE_CAND_INTERNAL);
-              return;
-            }
-            role = g.cls_role[g.ocls_off[o] + c];
-            rdim = g.cls_rdim[g.ocls_off[o] + c];
-          }
-          if (role == kPass) {
-            uint32_t cur = spec_axis(r.spec, rdim);
-            if (cur && cur != ax1) {
-              fail(PE_CAND_INTERNAL);
-              return;
-            }
-            r.spec = spec_set_axis(r.spec, rdim, ax1);
-            r.acq = (r.acq & ~(1u << rdim)) | (((w.acq >> d) & 1) << rdim);
-          } else if (role == kBlocked) {
+      }
+      for (int d = 0; d < wr; ++d) {
+        uint32_t ax1 = spec_axis(w.spec, d);
+        if (!ax1) continue;
+        int role, rdim;
+        if (kind == kReshape) {
+          int c = rr.cls_of_dim[d];
+          if (c < 0) {
             fail(PE_CAND_INTERNAL);
             return;
           }
+          role = rr.role[c];
+          rdim = rr.rdim[c];
+        } else {
+          int c = g.slot_cls[(base + k) * 4 + d];
+          if (c < 0) {
+            fail(PE_CAND_INTERNAL);
+            return;
+          }
+          role = g.cls_role[g.ocls_off[o] + c];
+          rdim = g.cls_rdim[g.ocls_off[o] + c];
+        }
+        if (role == kPass) {
+          uint32_t cur = spec_axis(r.spec, rdim);
+          if (cur && cur != ax1) {
+            fail(PE_CAND_INTERNAL);
+            return;
+          }
+          r.spec = spec_set_axis(r.spec, rdim, ax1);
+          r.acq = (r.acq & ~(1u << rdim)) | (((w.acq >> d) & 1) << rdim);
+        } else if (role == kBlocked) {
+          fail(PE_CAND_INTERNAL);
+          return;
         }
       }
     }
@@ -1031,18 +1073,17 @@ struct Cand {
     }
     int32_t j = new_op(kind, -1, -1, n);
     if (j < 0) return;
-    for (int32_t k = 0; k < n; ++k) add_operand(j, a.lo_buf[a.opnd[base + k]]);
+    for (int32_t k = 0; k < n; ++k)
+      add_operand(j, k == 0 ? in0.buf : k == 1 ? in1.buf : a.lo_buf[a.opnd[base + k]]);
     int64_t out_elems = local_elems(r);
     a.em_lb[j] = 4 * out_elems;
     // flops on LOCAL operand shapes
     switch (kind) {
       case kDot: {
-        Low lw = load(a.opnd[base]);
-        Low rw = load(a.opnd[base + 1]);
-        int64_t f = 2 * local_elems(lw);
-        int rr2 = rank_of_spec(rw.spec);
+        int64_t f = 2 * local_elems(in0);
+        int rr2 = rank_of_spec(in1.spec);
         for (int d = 0; d < rr2; ++d)
-          if ((g.omask[o] >> d) & 1) f *= local_dim(rw, d);
+          if ((g.omask[o] >> d) & 1) f *= local_dim(in1, d);
         flops += f;
         break;
       }
@@ -1051,7 +1092,7 @@ struct Cand {
         flops += out_elems;
         break;
       case kReduceSum: case kReduceMax:
-        flops += local_elems(load(a.opnd[base]));
+        flops += local_elems(in0);
         break;
       default:
         break;
@@ -1228,13 +1269,13 @@ struct Cand {
       int32_t h = a.em_head[j];
       int32_t kind = h & 0xFF, ax = ((h >> 8) & 0xF) - 1;
       if (kind == kAllReduce) {
-        int32_t b = a.em_opnd[a.em_ooff[j]];
+        int32_t b = a.em_op0[j];
         r.ar_cnt[ax]++;
-        r.ar_bytes[ax] += a.b_gb[b];
+        r.ar_bytes[ax] += b < g.A ? a.arg_gb[b] : a.em_gb[b - g.A];
       } else if (kind == kAllGather) {
-        int32_t b = a.em_opnd[a.em_ooff[j]];
+        int32_t b = a.em_op0[j];
         r.ag_cnt[ax]++;
-        r.ag_bytes[ax] += a.b_lb[b] * (asz(ax) - 1);
+        r.ag_bytes[ax] += (b < g.A ? a.arg_lb[b] : a.em_blb[b - g.A]) * (asz(ax) - 1);
       } else if (kind == kSliceByCoord) {
         r.sbc_cnt[ax]++;
       }
@@ -1293,7 +1334,7 @@ struct Cand {
     };
     put(g.A);
     for (int32_t x = 0; x < g.A; ++x) put(a.aspec0[x]);
-    put(a.b_spec[result_buf]);
+    put(result_buf < g.A ? a.arg_spec[result_buf] : a.em_spec[result_buf - g.A]);
     put(nstk);
     for (int32_t i = 0; i < nstk; ++i) {
       put(a.stk[2 * i]);
@@ -1305,7 +1346,7 @@ struct Cand {
       put(h);
       put(a.em_lb[j] & 0xffffffff);
       put(a.em_lb[j] >> 32);
-      put(a.b_spec[g.A + j]);
+      put(a.em_spec[j]);
       int32_t no = (h >> 16) & 0xFFFF;
       for (int32_t q = 0; q < no; ++q) put(a.em_opnd[a.em_ooff[j] + q]);
     }
@@ -1349,6 +1390,7 @@ struct Cand {
 
   PE_HD void eval(const pe_action* acts, int32_t n, const pe_cost_params& cp,
                   int64_t baseline, pe_result& r, int32_t* trace, uint32_t trace_words) {
+    tracing = trace != nullptr && trace_words > 0;
     tick_start();
     init();
     tick(0);
@@ -1374,23 +1416,21 @@ struct Cand {
   }
 
   // ------------------------------------------------------------ rollouts
-  PE_HD bool member_legal(int32_t m, int32_t d, int32_t ax) const {
-    if (d >= g.vrank[m]) return false;
-    if (g.shape(m)[d] % asz(ax) != 0) return false;
-    return !(a.slcnt[m] > 0 || a.awrapped[m]);
-  }
-  PE_HD bool ordinal_legal(int32_t e, int32_t d, int32_t ax) const {
-    for (int32_t i = g.ent_off[e]; i < g.ent_off[e + 1]; ++i)
-      if (member_legal(g.ent_mem[i], d, ax)) return true;
-    return false;
-  }
-  PE_HD int32_t count_legal() const {
-    int32_t c = 0;
-    for (int32_t e = 0; e < g.n_entries; ++e)
-      for (int32_t d = 0; d < kMaxRank; ++d)
-        for (int32_t ai = 0; ai < g.n_auto; ++ai)
-          if (ordinal_legal(e, d, g.auto_axes[ai])) ++c;
-    return c;
+  // legal_actions (SPEC search module): a TileValue ordinal is legal when at
+  // least one statically legal member does not carry tiling yet
+  // (REF rewrite.cc:75-76).  Fills a.lg with the legal ordinals in order.
+  PE_HD int32_t build_legal() {
+    int32_t n = 0;
+    for (int32_t o = 0; o < g.n_ord; ++o) {
+      for (int32_t i = g.ord_off[o]; i < g.ord_off[o + 1]; ++i) {
+        int32_t m = g.ord_mem[i];
+        if (!((a.carry[m >> 5] >> (m & 31)) & 1u)) {
+          a.lg[n++] = o;
+          break;
+        }
+      }
+    }
+    return n;
   }
   PE_HD pe_action ordinal_action(int32_t ord) const {
     pe_action x;
@@ -1408,18 +1448,6 @@ struct Cand {
     }
     return x;
   }
-  // the pick-th legal ordinal
-  PE_HD int32_t nth_legal(int32_t pick) const {
-    int32_t c = 0;
-    for (int32_t e = 0; e < g.n_entries; ++e)
-      for (int32_t d = 0; d < kMaxRank; ++d)
-        for (int32_t ai = 0; ai < g.n_auto; ++ai)
-          if (ordinal_legal(e, d, g.auto_axes[ai])) {
-            if (c == pick) return (e * kMaxRank + d) * g.n_auto + ai;
-            ++c;
-          }
-    return -1;
-  }
   PE_HD static uint64_t splitmix(uint64_t& st) {
     st += 0x9E3779B97F4A7C15ull;
     uint64_t z = st;
@@ -1431,6 +1459,7 @@ struct Cand {
   PE_HD void rollout(const pe_action* prefix, int32_t np, uint64_t seed, int32_t maxd,
                      const pe_cost_params& cp, int64_t baseline, pe_action* acts_out,
                      uint32_t* n_out, pe_result& r, uint64_t* legal_out, int32_t legal_words) {
+    tracing = false;
     tick_start();
     init();
     tick(0);
@@ -1462,24 +1491,19 @@ struct Cand {
     }
     if (!bad() && status == PE_CAND_OK) {
       if (legal_out) {
-        for (int32_t e = 0; e < g.n_entries; ++e)
-          for (int32_t d = 0; d < kMaxRank; ++d)
-            for (int32_t ai = 0; ai < g.n_auto; ++ai)
-              if (ordinal_legal(e, d, g.auto_axes[ai])) {
-                int32_t o = (e * kMaxRank + d) * g.n_auto + ai;
-                legal_out[o >> 6] |= 1ull << (o & 63);
-              }
+        int32_t nl = build_legal();
+        for (int32_t i = 0; i < nl; ++i) legal_out[a.lg[i] >> 6] |= 1ull << (a.lg[i] & 63);
       }
       uint64_t st = seed;
       while (!terminal) {
         if (steps >= maxd) break;
         tick(4);
-        int32_t nl = count_legal();
+        int32_t nl = build_legal();
         if (nl == 0) break;
         uint64_t ws = steps >= 1 ? 2 : 1;
         uint64_t pick = splitmix(st) % ((uint64_t)nl + ws);
         if (pick >= (uint64_t)nl) break;
-        pe_action x = ordinal_action(nth_legal((int32_t)pick));
+        pe_action x = ordinal_action(a.lg[pick]);
         tick(5);
         bool ok = apply_action(x);
         if (bad()) break;

@@ -44,8 +44,7 @@ struct pe_engine {
   uint32_t big_slots = 0;
   int64_t baseline = 1;
   uint32_t n_ordinals = 0;
-  std::vector<int32_t> auto_axes;
-  std::vector<int32_t> ent_off, ent_mem;
+  pe::Worklist wl;
   uint64_t launches = 0;
   int64_t graph_bytes = 0;
   int sm_count = 148;
@@ -70,8 +69,14 @@ bool cuda_ok(cudaError_t e, pe_error* err, const char* what) {
   return false;
 }
 
+#ifndef PE_MIN_BLOCKS
+#define PE_MIN_BLOCKS 4
+#endif
 constexpr int kBlock = 128;
-constexpr int kMinBlocks = 4;  // 16 warps / SM: caps registers at 128 per thread
+// resident blocks per SM the register allocation must allow: 4 -> 16 warps
+// per SM (<= 128 registers / thread); the per-thread work is a dependent
+// chain of global-memory accesses, so resident warps = latency hiding
+constexpr int kMinBlocks = PE_MIN_BLOCKS;
 
 #ifdef PE_PHASE_TIMERS
 // profiling build only (tools/phase_profile.py): summed clock64 per phase
@@ -118,7 +123,7 @@ pe_rollout_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
               legal_out ? legal_out + (uint64_t)i * legal_words : nullptr, legal_words);
     out[i] = r;
   }
-#ifdef PE_PHASE_TIMERS
+#if defined(PE_PHASE_TIMERS) && defined(__CUDA_ARCH__)
   for (int k = 0; k < 9; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)c.ph[k]);
 #endif
 }
@@ -260,29 +265,10 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   if (e->cfg.max_decisions == 0) e->cfg.max_decisions = 32;
   cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, device);
   const pe::HostGraph& g = graph->g;
-  int32_t A = (int32_t)g.args.size();
-  for (int32_t a = 0; a < (int32_t)g.axis_names.size(); ++a)
-    if (e->cfg.auto_axes_mask & (1u << a)) e->auto_axes.push_back(a);
   // worklist entries (SPEC build_worklist: arguments, optionally grouped)
-  e->ent_off.push_back(0);
-  if (e->cfg.group_scopes) {
-    for (const auto& grp : g.groups) {
-      for (int32_t m : grp) e->ent_mem.push_back(m);
-      e->ent_off.push_back((int32_t)e->ent_mem.size());
-    }
-  } else {
-    for (int32_t a = 0; a < A; ++a) {
-      e->ent_mem.push_back(a);
-      e->ent_off.push_back((int32_t)e->ent_mem.size());
-    }
-  }
-  std::vector<int32_t> grp_off{0}, grp_mem;
-  for (const auto& grp : g.groups) {
-    for (int32_t m : grp) grp_mem.push_back(m);
-    grp_off.push_back((int32_t)grp_mem.size());
-  }
-  int32_t n_entries = (int32_t)e->ent_off.size() - 1;
-  e->n_ordinals = (uint32_t)(n_entries * pe::kMaxRank * (int32_t)e->auto_axes.size());
+  e->wl = pe::build_worklist(g, e->cfg.auto_axes_mask, e->cfg.group_scopes != 0);
+  const pe::Worklist& w = e->wl;
+  e->n_ordinals = (uint32_t)w.n_ordinals();
 
   // device image of the graph tables
   std::vector<uint8_t> img;
@@ -295,8 +281,9 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   size_t o_mem = stage(img, g.mem), o_scls = stage(img, g.slot_cls);
   size_t o_rcls = stage(img, g.op_rcls), o_uoff = stage(img, g.user_off);
   size_t o_users = stage(img, g.users), o_iu = stage(img, g.init_uses);
-  size_t o_eoff = stage(img, e->ent_off), o_emem = stage(img, e->ent_mem);
-  size_t o_goff = stage(img, grp_off), o_gmem = stage(img, grp_mem);
+  size_t o_eoff = stage(img, w.ent_off), o_emem = stage(img, w.ent_mem);
+  size_t o_goff = stage(img, w.grp_off), o_gmem = stage(img, w.grp_mem);
+  size_t o_ooff2 = stage(img, w.ord_off), o_omem2 = stage(img, w.ord_mem);
   if (!cuda_ok(cudaMalloc(&e->d_graph, img.size()), err, "cudaMalloc(graph)") ||
       !cuda_ok(cudaMemcpy(e->d_graph, img.data(), img.size(), cudaMemcpyHostToDevice), err,
                "cudaMemcpy(graph)")) {
@@ -324,16 +311,13 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   v.user_off = (const int32_t*)(b + o_uoff);
   v.users = (const int32_t*)(b + o_users);
   v.init_uses = (const int32_t*)(b + o_iu);
-  v.n_entries = n_entries;
-  v.n_auto = (int32_t)e->auto_axes.size();
-  for (int i = 0; i < pe::kMaxAxes; ++i)
-    v.auto_axes[i] = i < v.n_auto ? e->auto_axes[i] : 0;
-  v.entries_are_groups = e->cfg.group_scopes ? 1 : 0;
+  pe::attach_worklist(v, w);  // scalars; pointers re-targeted to the device image
   v.ent_off = (const int32_t*)(b + o_eoff);
   v.ent_mem = (const int32_t*)(b + o_emem);
-  v.n_groups = (int32_t)g.groups.size();
   v.grp_off = (const int32_t*)(b + o_goff);
   v.grp_mem = (const int32_t*)(b + o_gmem);
+  v.ord_off = (const int32_t*)(b + o_ooff2);
+  v.ord_mem = (const int32_t*)(b + o_omem2);
   e->dview = v;
 
   // per-candidate arenas: one per thread slot, bounded by an HBM budget
@@ -405,17 +389,18 @@ int64_t pe_engine_graph_bytes(const pe_engine* e) { return e->graph_bytes; }
 
 pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* out) {
   if (!out || ord >= e->n_ordinals) return PE_ERR_INVALID_ARGUMENT;
-  uint32_t na = (uint32_t)e->auto_axes.size();
+  const pe::Worklist& w = e->wl;
+  uint32_t na = (uint32_t)w.auto_axes.size();
   uint32_t ai = ord % na, d = (ord / na) % pe::kMaxRank, ent = ord / na / pe::kMaxRank;
-  out->axis = (uint8_t)e->auto_axes[ai];
+  out->axis = (uint8_t)w.auto_axes[ai];
   out->dim = (uint8_t)d;
   out->pad = 0;
-  if (e->cfg.group_scopes) {
+  if (w.groups) {
     out->kind = PE_ACT_TILE_GROUP;
     out->value = ent;
   } else {
     out->kind = PE_ACT_TILE;
-    out->value = (uint32_t)e->ent_mem[e->ent_off[ent]];
+    out->value = (uint32_t)w.ent_mem[w.ent_off[ent]];
   }
   return PE_OK;
 }
@@ -486,7 +471,7 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
     return PE_ERR_INVALID_ARGUMENT;
   }
   if (n == 0) return PE_OK;
-  if (e->auto_axes.empty()) {
+  if (e->wl.auto_axes.empty()) {
     set_err(err, PE_ERR_INVALID_ARGUMENT, "no auto axes selected");
     return PE_ERR_INVALID_ARGUMENT;
   }

@@ -788,6 +788,55 @@ GraphView HostGraph::host_view() const {
   return v;
 }
 
+Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes) {
+  Worklist w;
+  w.groups = group_scopes;
+  for (int32_t a = 0; a < (int32_t)g.axis_names.size(); ++a)
+    if (auto_axes_mask & (1u << a)) w.auto_axes.push_back(a);
+  w.grp_off.push_back(0);
+  for (const auto& grp : g.groups) {
+    for (int32_t m : grp) w.grp_mem.push_back(m);
+    w.grp_off.push_back((int32_t)w.grp_mem.size());
+  }
+  if (group_scopes) {
+    w.ent_off = w.grp_off;
+    w.ent_mem = w.grp_mem;
+  } else {
+    w.ent_off.push_back(0);
+    for (int32_t a = 0; a < (int32_t)g.args.size(); ++a) {
+      w.ent_mem.push_back(a);
+      w.ent_off.push_back((int32_t)w.ent_mem.size());
+    }
+  }
+  w.ord_off.push_back(0);
+  for (int32_t e = 0; e < w.n_entries(); ++e)
+    for (int32_t d = 0; d < kMaxRank; ++d)
+      for (int32_t ax : w.auto_axes) {
+        for (int32_t i = w.ent_off[e]; i < w.ent_off[e + 1]; ++i) {
+          int32_t m = w.ent_mem[i];
+          const auto& s = g.args[m].shape;
+          if (d < (int32_t)s.size() && s[d] % g.axis_sizes[ax] == 0) w.ord_mem.push_back(m);
+        }
+        w.ord_off.push_back((int32_t)w.ord_mem.size());
+      }
+  return w;
+}
+
+void attach_worklist(GraphView& v, const Worklist& w) {
+  v.n_entries = w.n_entries();
+  v.n_auto = (int32_t)w.auto_axes.size();
+  for (int i = 0; i < kMaxAxes; ++i) v.auto_axes[i] = i < v.n_auto ? w.auto_axes[i] : 0;
+  v.entries_are_groups = w.groups ? 1 : 0;
+  v.ent_off = w.ent_off.data();
+  v.ent_mem = w.ent_mem.data();
+  v.n_groups = (int32_t)w.grp_off.size() - 1;
+  v.grp_off = w.grp_off.data();
+  v.grp_mem = w.grp_mem.data();
+  v.n_ord = w.n_ordinals();
+  v.ord_off = w.ord_off.data();
+  v.ord_mem = w.ord_mem.data();
+}
+
 bool load_graph(const char* text, size_t len, HostGraph& g, LoadError& err) {
   try {
     Parser p(text, len, g);

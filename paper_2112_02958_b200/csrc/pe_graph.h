@@ -71,6 +71,24 @@ struct HostGraph {
   GraphView host_view() const;
 };
 
+// SPEC build_worklist (search module): worklist entries are scope groups or
+// single arguments; TileValue ordinals enumerate entry x dim x auto axis
+// (ordinal = (entry*4 + dim)*n_auto + auto-axis rank).  ord_mem lists, per
+// ordinal, the members for which the action is statically legal (rank and
+// divisibility, REF rewrite.cc:63-74); the dynamic part (carries_tiling) is
+// checked per candidate.
+struct Worklist {
+  std::vector<int32_t> auto_axes, ent_off, ent_mem, grp_off, grp_mem, ord_off, ord_mem;
+  bool groups = true;
+  int32_t n_entries() const { return (int32_t)ent_off.size() - 1; }
+  int32_t n_ordinals() const {
+    return n_entries() * kMaxRank * (int32_t)auto_axes.size();
+  }
+};
+Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes);
+// points the worklist fields of `v` at the (host) vectors of `w`
+void attach_worklist(GraphView& v, const Worklist& w);
+
 struct LoadError {
   int code = 0;  // pe_status
   int line = 0, column = 0;

@@ -82,6 +82,10 @@ struct GraphView {
   int32_t n_groups;
   const int32_t* grp_off;    // [n_groups+1]
   const int32_t* grp_mem;
+  // TileValue ordinals: statically legal members per ordinal
+  int32_t n_ord;
+  const int32_t* ord_off;    // [n_ord+1]
+  const int32_t* ord_mem;
 
   PE_HD const int32_t* shape(int32_t v) const { return vshape + 4 * v; }
 };

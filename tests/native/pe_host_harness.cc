@@ -21,8 +21,7 @@ struct Harness {
   pe::HostGraph g;
   pe::GraphView v;
   pe::Layout L;
-  std::vector<int32_t> ent_off, ent_mem, grp_off, grp_mem;
-  std::vector<int32_t> auto_axes;
+  pe::Worklist w;
   std::vector<uint8_t> arena;
   pe_search_config cfg;
   pe_cost_params cp;
@@ -55,33 +54,8 @@ int setup(Harness& h, const char* pir, size_t len, const pe_search_config* cfg,
   if (cfg) h.cfg = *cfg;
   if (cp) h.cp = *cp;
   h.v = h.g.host_view();
-  for (int a = 0; a < (int)h.g.axis_names.size(); ++a)
-    if (h.cfg.auto_axes_mask & (1u << a)) h.auto_axes.push_back(a);
-  h.ent_off.push_back(0);
-  h.grp_off.push_back(0);
-  for (const auto& grp : h.g.groups) {
-    for (int m : grp) h.grp_mem.push_back(m);
-    h.grp_off.push_back((int32_t)h.grp_mem.size());
-  }
-  if (h.cfg.group_scopes) {
-    h.ent_off = h.grp_off;
-    h.ent_mem = h.grp_mem;
-  } else {
-    for (int a = 0; a < (int)h.g.args.size(); ++a) {
-      h.ent_mem.push_back(a);
-      h.ent_off.push_back((int32_t)h.ent_mem.size());
-    }
-  }
-  h.v.n_entries = (int32_t)h.ent_off.size() - 1;
-  h.v.n_auto = (int32_t)h.auto_axes.size();
-  for (int i = 0; i < pe::kMaxAxes; ++i)
-    h.v.auto_axes[i] = i < h.v.n_auto ? h.auto_axes[i] : 0;
-  h.v.entries_are_groups = h.cfg.group_scopes ? 1 : 0;
-  h.v.ent_off = h.ent_off.data();
-  h.v.ent_mem = h.ent_mem.data();
-  h.v.n_groups = (int32_t)h.g.groups.size();
-  h.v.grp_off = h.grp_off.data();
-  h.v.grp_mem = h.grp_mem.data();
+  h.w = pe::build_worklist(h.g, h.cfg.auto_axes_mask, h.cfg.group_scopes != 0);
+  pe::attach_worklist(h.v, h.w);
   h.L = pe::make_layout(h.v);
   h.arena.assign(h.L.bytes, 0);
   pe::Cand c(h.v, h.L, h.arena.data());
