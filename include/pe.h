@@ -116,7 +116,9 @@ typedef struct pe_search_config {
   uint64_t seed;
   double uct_c;            /* default 1.414                                */
   uint32_t leaf_batch;     /* leaves evaluated per GPU launch              */
-  uint32_t reserved;
+  uint32_t scoped_only;    /* 1 = worklist holds only arguments with a scope
+                              (parameters); unscoped inputs are left to manual
+                              decisions, as automap's batch axis (PAPER §2.2) */
 } pe_search_config;
 
 void pe_default_cost_params(pe_cost_params* out);
@@ -161,6 +163,8 @@ int32_t pe_graph_value_name(const pe_graph* g, int32_t value, char* buf,
                             int32_t cap);
 /* value rank and dims */
 int32_t pe_graph_value_shape(const pe_graph* g, int32_t value, int64_t* dims);
+/* argument scope tag (SPEC tensor_ir `scope`); returns length or -1 */
+int32_t pe_graph_arg_scope(const pe_graph* g, int32_t arg, char* buf, int32_t cap);
 /* scope groups (normalisation SPEC:568) */
 int32_t pe_graph_num_groups(const pe_graph* g);
 int32_t pe_graph_group_size(const pe_graph* g, int32_t group);
@@ -223,6 +227,54 @@ uint32_t pe_engine_slots(const pe_engine* e);
 int64_t pe_engine_graph_bytes(const pe_engine* e);
 /* kernel launches issued by this engine since creation */
 uint64_t pe_engine_launch_count(const pe_engine* e);
+
+/* ---- search (SPEC search module: mcts_search / emit_plan) ---- */
+#define PE_PLAN_MAX_ACTIONS 64
+
+typedef struct pe_plan {
+  pe_action actions[PE_PLAN_MAX_ACTIONS]; /* best terminal action sequence */
+  uint32_t n_actions;
+  uint32_t episodes;         /* episodes run on this rank                    */
+  uint32_t found_at_episode; /* episode (on the winning rank) that found it  */
+  uint32_t winner_rank;
+  uint64_t seed;
+  pe_result result;          /* evaluation of the best plan                  */
+} pe_plan;
+
+/* Root-parallel merge hook: replace `values[0..n)` with their element-wise
+ * SUM (op 0) or MAX (op 1) over all ranks (an NCCL / gloo all_reduce).
+ * Returns 0 on success.  NULL = single rank. */
+typedef int (*pe_merge_fn)(void* user, int64_t* values, uint32_t n, int32_t op);
+
+/* Evaluator hook with pe_rollout_batch semantics on host buffers. */
+typedef int (*pe_rollout_fn)(void* user, const pe_action* prefix,
+                             const uint32_t* prefix_off, const uint64_t* seeds,
+                             uint32_t n, pe_action* acts_out, uint32_t* n_acts_out,
+                             pe_result* out, uint64_t* legal_out);
+
+typedef struct pe_mcts_params {
+  uint32_t n_ordinals;    /* TileValue ordinals; Stop is ordinal n_ordinals  */
+  uint32_t max_decisions; /* SPEC default 32                                 */
+  uint32_t episodes;      /* budget on this rank                             */
+  uint32_t leaf_batch;    /* leaves selected (virtual loss) per evaluation   */
+  uint32_t merge_every;   /* episodes between root-statistic merges (0: never) */
+  uint32_t rank;
+  uint64_t seed;
+  double uct_c;           /* SPEC default 1.414                              */
+} pe_mcts_params;
+
+/* mcts_search (SPEC search module): UCT selection (ties -> lowest ordinal),
+ * lowest-ordinal expansion, uniform rollouts, backpropagation of the reward
+ * as 2^-32 fixed point, best terminal plan.  Deterministic for a given
+ * (params, evaluator).  `ordinal_actions[k]` decodes ordinal k. */
+pe_status pe_mcts_run(const pe_mcts_params* p, pe_rollout_fn eval, void* eval_user,
+                      pe_merge_fn merge, void* merge_user,
+                      const pe_action* ordinal_actions, pe_plan* out, pe_error* err);
+
+/* mcts_search on this engine: cfg->leaf_batch rollouts per GPU launch. */
+pe_status pe_search(pe_engine* e, const pe_search_config* cfg, uint32_t merge_every,
+                    uint32_t rank, pe_merge_fn merge, void* merge_user, pe_plan* out,
+                    pe_error* err);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -73,6 +73,7 @@ struct Setup {
   std::map<std::string, int> op_index;     // original op id -> op index
   std::vector<std::vector<int>> groups;    // group -> member arg indices
   std::vector<std::vector<int>> entries;   // worklist entries (groups or singletons)
+  std::vector<int> entry_val;              // action value per entry
   std::vector<int> auto_axes;
   pe_search_config cfg;
   pe_cost_params cp;
@@ -96,10 +97,20 @@ void build_groups(Setup& s) {
       s.groups[it->second].push_back((int)a);
     }
   }
+  // worklist entries and the action value each one decodes to (the group
+  // index for TILE_GROUP, the argument for TILE)
   if (s.cfg.group_scopes) {
-    s.entries = s.groups;
+    for (size_t gi = 0; gi < s.groups.size(); ++gi) {
+      if (s.cfg.scoped_only && s.root.args[s.groups[gi][0]].scope.empty()) continue;
+      s.entries.push_back(s.groups[gi]);
+      s.entry_val.push_back((int)gi);
+    }
   } else {
-    for (size_t a = 0; a < s.root.args.size(); ++a) s.entries.push_back({(int)a});
+    for (size_t a = 0; a < s.root.args.size(); ++a) {
+      if (s.cfg.scoped_only && s.root.args[a].scope.empty()) continue;
+      s.entries.push_back({(int)a});
+      s.entry_val.push_back((int)a);
+    }
   }
 }
 
@@ -407,13 +418,8 @@ pe_action ordinal_action(const Setup& s, uint32_t ord) {
   uint32_t e = ord / na / PE_MAX_RANK;
   a.axis = (uint8_t)s.auto_axes[ai];
   a.dim = (uint8_t)d;
-  if (s.cfg.group_scopes) {
-    a.kind = PE_ACT_TILE_GROUP;
-    a.value = e;
-  } else {
-    a.kind = PE_ACT_TILE;
-    a.value = (uint32_t)s.entries[e][0];
-  }
+  a.kind = s.cfg.group_scopes ? PE_ACT_TILE_GROUP : PE_ACT_TILE;
+  a.value = (uint32_t)s.entry_val[e];
   return a;
 }
 

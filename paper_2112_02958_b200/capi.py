@@ -75,8 +75,28 @@ class PeSearchConfig(C.Structure):
     _fields_ = [("auto_axes_mask", C.c_uint32), ("max_decisions", C.c_uint32),
                 ("group_scopes", C.c_uint32), ("episodes", C.c_uint32),
                 ("seed", C.c_uint64), ("uct_c", C.c_double),
-                ("leaf_batch", C.c_uint32), ("reserved", C.c_uint32)]
+                ("leaf_batch", C.c_uint32), ("scoped_only", C.c_uint32)]
 
+
+PE_PLAN_MAX_ACTIONS = 64
+
+
+class PePlan(C.Structure):
+    _fields_ = [("actions", PeAction * PE_PLAN_MAX_ACTIONS), ("n_actions", C.c_uint32),
+                ("episodes", C.c_uint32), ("found_at_episode", C.c_uint32),
+                ("winner_rank", C.c_uint32), ("seed", C.c_uint64), ("result", PeResult)]
+
+
+class PeMctsParams(C.Structure):
+    _fields_ = [("n_ordinals", C.c_uint32), ("max_decisions", C.c_uint32),
+                ("episodes", C.c_uint32), ("leaf_batch", C.c_uint32),
+                ("merge_every", C.c_uint32), ("rank", C.c_uint32), ("seed", C.c_uint64),
+                ("uct_c", C.c_double)]
+
+
+MERGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int64), C.c_uint32, C.c_int32)
+ROLLOUT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
+                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
 
 assert C.sizeof(PeAction) == 8
 assert C.sizeof(PeResult) == 192, C.sizeof(PeResult)
@@ -109,6 +129,7 @@ SIGNATURES = {
     "pe_graph_axis_index": (C.c_int32, [_P, C.c_char_p]),
     "pe_graph_value_name": (C.c_int32, [_P, C.c_int32, C.c_char_p, C.c_int32]),
     "pe_graph_value_shape": (C.c_int32, [_P, C.c_int32, C.POINTER(C.c_int64)]),
+    "pe_graph_arg_scope": (C.c_int32, [_P, C.c_int32, C.c_char_p, C.c_int32]),
     "pe_graph_num_groups": (C.c_int32, [_P]),
     "pe_graph_group_size": (C.c_int32, [_P, C.c_int32]),
     "pe_graph_group_member": (C.c_int32, [_P, C.c_int32, C.c_int32]),
@@ -127,6 +148,10 @@ SIGNATURES = {
     "pe_engine_slots": (C.c_uint32, [_P]),
     "pe_engine_launch_count": (C.c_uint64, [_P]),
     "pe_engine_graph_bytes": (C.c_int64, [_P]),
+    "pe_mcts_run": (C.c_int, [C.POINTER(PeMctsParams), ROLLOUT_FN, _P, MERGE_FN, _P, _P,
+                              C.POINTER(PePlan), C.POINTER(PeError)]),
+    "pe_search": (C.c_int, [_P, C.POINTER(PeSearchConfig), C.c_uint32, C.c_uint32, MERGE_FN,
+                            _P, C.POINTER(PePlan), C.POINTER(PeError)]),
 }
 
 HERE = os.path.dirname(os.path.abspath(__file__))

@@ -1439,13 +1439,8 @@ struct Cand {
     x.axis = (uint8_t)g.auto_axes[ai];
     x.dim = (uint8_t)d;
     x.pad = 0;
-    if (g.entries_are_groups) {
-      x.kind = PE_ACT_TILE_GROUP;
-      x.value = (uint32_t)e;
-    } else {
-      x.kind = PE_ACT_TILE;
-      x.value = (uint32_t)g.ent_mem[g.ent_off[e]];
-    }
+    x.kind = g.entries_are_groups ? PE_ACT_TILE_GROUP : PE_ACT_TILE;
+    x.value = (uint32_t)g.ent_val[e];
     return x;
   }
   PE_HD static uint64_t splitmix(uint64_t& st) {

@@ -225,6 +225,12 @@ int32_t pe_graph_value_shape(const pe_graph* g, int32_t v, int64_t* dims) {
   for (size_t d = 0; d < s.size() && dims; ++d) dims[d] = s[d];
   return (int32_t)s.size();
 }
+int32_t pe_graph_arg_scope(const pe_graph* g, int32_t arg, char* buf, int32_t cap) {
+  if (arg < 0 || arg >= (int32_t)g->g.args.size()) return -1;
+  const std::string& s = g->g.args[arg].scope;
+  if (buf && cap > 0) std::snprintf(buf, cap, "%s", s.c_str());
+  return (int32_t)s.size();
+}
 int32_t pe_graph_num_groups(const pe_graph* g) { return (int32_t)g->g.groups.size(); }
 int32_t pe_graph_group_size(const pe_graph* g, int32_t grp) {
   if (grp < 0 || grp >= (int32_t)g->g.groups.size()) return -1;
@@ -266,7 +272,8 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, device);
   const pe::HostGraph& g = graph->g;
   // worklist entries (SPEC build_worklist: arguments, optionally grouped)
-  e->wl = pe::build_worklist(g, e->cfg.auto_axes_mask, e->cfg.group_scopes != 0);
+  e->wl = pe::build_worklist(g, e->cfg.auto_axes_mask, e->cfg.group_scopes != 0,
+                             e->cfg.scoped_only != 0);
   const pe::Worklist& w = e->wl;
   e->n_ordinals = (uint32_t)w.n_ordinals();
 
@@ -284,6 +291,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   size_t o_eoff = stage(img, w.ent_off), o_emem = stage(img, w.ent_mem);
   size_t o_goff = stage(img, w.grp_off), o_gmem = stage(img, w.grp_mem);
   size_t o_ooff2 = stage(img, w.ord_off), o_omem2 = stage(img, w.ord_mem);
+  size_t o_eval = stage(img, w.ent_val);
   if (!cuda_ok(cudaMalloc(&e->d_graph, img.size()), err, "cudaMalloc(graph)") ||
       !cuda_ok(cudaMemcpy(e->d_graph, img.data(), img.size(), cudaMemcpyHostToDevice), err,
                "cudaMemcpy(graph)")) {
@@ -318,6 +326,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   v.grp_mem = (const int32_t*)(b + o_gmem);
   v.ord_off = (const int32_t*)(b + o_ooff2);
   v.ord_mem = (const int32_t*)(b + o_omem2);
+  v.ent_val = (const int32_t*)(b + o_eval);
   e->dview = v;
 
   // per-candidate arenas: one per thread slot, bounded by an HBM budget
@@ -395,13 +404,8 @@ pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* 
   out->axis = (uint8_t)w.auto_axes[ai];
   out->dim = (uint8_t)d;
   out->pad = 0;
-  if (w.groups) {
-    out->kind = PE_ACT_TILE_GROUP;
-    out->value = ent;
-  } else {
-    out->kind = PE_ACT_TILE;
-    out->value = (uint32_t)w.ent_mem[w.ent_off[ent]];
-  }
+  out->kind = w.groups ? PE_ACT_TILE_GROUP : PE_ACT_TILE;
+  out->value = (uint32_t)w.ent_val[ent];
   return PE_OK;
 }
 
@@ -559,3 +563,37 @@ extern "C" int pe_debug_phase_cycles(unsigned long long* out9, int reset) {
   return 0;
 }
 #endif
+
+// ------------------------------------------------------------------ search
+namespace {
+int engine_rollout_eval(void* user, const pe_action* prefix, const uint32_t* poff,
+                        const uint64_t* seeds, uint32_t n, pe_action* acts_out,
+                        uint32_t* n_acts_out, pe_result* out, uint64_t* legal_out) {
+  pe_error err;
+  return (int)pe_rollout_batch((pe_engine*)user, prefix, poff, seeds, n, acts_out, n_acts_out,
+                               out, legal_out, 0, nullptr, &err);
+}
+}  // namespace
+
+extern "C" pe_status pe_search(pe_engine* e, const pe_search_config* cfg, uint32_t merge_every,
+                               uint32_t rank, pe_merge_fn merge, void* merge_user,
+                               pe_plan* out, pe_error* err) {
+  if (!e || !out) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  const pe_search_config& c = cfg ? *cfg : e->cfg;
+  std::vector<pe_action> ords(e->n_ordinals + 1);
+  for (uint32_t o = 0; o < e->n_ordinals; ++o) pe_engine_ordinal_action(e, o, &ords[o]);
+  ords[e->n_ordinals] = pe_action{0, 0, 0, PE_ACT_STOP, 0};
+  pe_mcts_params p;
+  p.n_ordinals = e->n_ordinals;
+  p.max_decisions = e->cfg.max_decisions;  // the rollout kernel's cap
+  p.episodes = c.episodes;
+  p.leaf_batch = c.leaf_batch ? c.leaf_batch : 256;
+  p.merge_every = merge_every;
+  p.rank = rank;
+  p.seed = c.seed;
+  p.uct_c = c.uct_c;
+  return pe_mcts_run(&p, engine_rollout_eval, e, merge, merge_user, ords.data(), out, err);
+}

@@ -788,7 +788,8 @@ GraphView HostGraph::host_view() const {
   return v;
 }
 
-Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes) {
+Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes,
+                        bool scoped_only) {
   Worklist w;
   w.groups = group_scopes;
   for (int32_t a = 0; a < (int32_t)g.axis_names.size(); ++a)
@@ -798,14 +799,21 @@ Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_
     for (int32_t m : grp) w.grp_mem.push_back(m);
     w.grp_off.push_back((int32_t)w.grp_mem.size());
   }
+  w.ent_off.push_back(0);
   if (group_scopes) {
-    w.ent_off = w.grp_off;
-    w.ent_mem = w.grp_mem;
+    for (int32_t gi = 0; gi < (int32_t)g.groups.size(); ++gi) {
+      const auto& grp = g.groups[gi];
+      if (scoped_only && g.args[grp[0]].scope.empty()) continue;
+      for (int32_t m : grp) w.ent_mem.push_back(m);
+      w.ent_off.push_back((int32_t)w.ent_mem.size());
+      w.ent_val.push_back(gi);
+    }
   } else {
-    w.ent_off.push_back(0);
     for (int32_t a = 0; a < (int32_t)g.args.size(); ++a) {
+      if (scoped_only && g.args[a].scope.empty()) continue;
       w.ent_mem.push_back(a);
       w.ent_off.push_back((int32_t)w.ent_mem.size());
+      w.ent_val.push_back(a);
     }
   }
   w.ord_off.push_back(0);
@@ -829,6 +837,7 @@ void attach_worklist(GraphView& v, const Worklist& w) {
   v.entries_are_groups = w.groups ? 1 : 0;
   v.ent_off = w.ent_off.data();
   v.ent_mem = w.ent_mem.data();
+  v.ent_val = w.ent_val.data();
   v.n_groups = (int32_t)w.grp_off.size() - 1;
   v.grp_off = w.grp_off.data();
   v.grp_mem = w.grp_mem.data();

@@ -79,13 +79,15 @@ struct HostGraph {
 // checked per candidate.
 struct Worklist {
   std::vector<int32_t> auto_axes, ent_off, ent_mem, grp_off, grp_mem, ord_off, ord_mem;
+  std::vector<int32_t> ent_val;  // action value per entry: group index or argument
   bool groups = true;
   int32_t n_entries() const { return (int32_t)ent_off.size() - 1; }
   int32_t n_ordinals() const {
     return n_entries() * kMaxRank * (int32_t)auto_axes.size();
   }
 };
-Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes);
+Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes,
+                        bool scoped_only = false);
 // points the worklist fields of `v` at the (host) vectors of `w`
 void attach_worklist(GraphView& v, const Worklist& w);
 

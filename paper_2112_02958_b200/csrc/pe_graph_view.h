@@ -78,6 +78,7 @@ struct GraphView {
   int32_t entries_are_groups;
   const int32_t* ent_off;    // [n_entries+1]
   const int32_t* ent_mem;    // arg indices
+  const int32_t* ent_val;    // [n_entries] action value: group index / argument
   // scope groups (for PE_ACT_TILE_GROUP)
   int32_t n_groups;
   const int32_t* grp_off;    // [n_groups+1]

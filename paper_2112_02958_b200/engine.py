@@ -94,6 +94,13 @@ class Graph:
             r = L.pe_graph_value_shape(h, v, dims)
             self.shapes.append([dims[i] for i in range(r)])
         self.axis_sizes = [L.pe_graph_axis_size(h, a) for a in range(self.n_axes)]
+        self.scopes = []
+        for a in range(self.n_args):
+            L.pe_graph_arg_scope(h, a, buf, 1024)
+            self.scopes.append(buf.value.decode())
+        import re
+        m = re.search(r"mesh\s*\{([^}]*)\}", text)
+        self.axis_names = re.findall(r'"([^"]+)"\s*=', m.group(1)) if m else []
         self.groups = [[L.pe_graph_group_member(h, g, i) for i in range(L.pe_graph_group_size(h, g))]
                        for g in range(L.pe_graph_num_groups(h))]
         self._index = {n: i for i, n in enumerate(self.names)}

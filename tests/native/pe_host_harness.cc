@@ -54,7 +54,8 @@ int setup(Harness& h, const char* pir, size_t len, const pe_search_config* cfg,
   if (cfg) h.cfg = *cfg;
   if (cp) h.cp = *cp;
   h.v = h.g.host_view();
-  h.w = pe::build_worklist(h.g, h.cfg.auto_axes_mask, h.cfg.group_scopes != 0);
+  h.w = pe::build_worklist(h.g, h.cfg.auto_axes_mask, h.cfg.group_scopes != 0,
+                           h.cfg.scoped_only != 0);
   pe::attach_worklist(h.v, h.w);
   h.L = pe::make_layout(h.v);
   h.arena.assign(h.L.bytes, 0);
