@@ -54,61 +54,117 @@ struct Caps {
   int32_t EO;  // emitted operand references
 };
 
-// Per-candidate arena, packed as 32-byte records so that the fields a sweep
-// touches together share one sector:
-//   VRec[V]     value slot:  vk, vref, vaux, uses, slcnt, body links, position
-//   LowRec[V]   lowered view (REF spmd.cc:42 `Lowered`): buffer, spec, acq, shape
-//   ArgRec[A]   per argument: direct-in-loop count, slice demand, atomic flag
-//   LoopRec[L]  tile / sum loop: kind, axis, dim, body list, yield, result type
-//   EmRec[EM+1] emitted SPMD op: head, operand offset, last use, local bytes
-//   BRec[A+EM]  final registered DistType of every SPMD buffer (bytes, spec)
-// plus flat int arrays (operands, top-level positions, stuck list).
+// Per-candidate arenas, interleaved candidate-minor.
+// The PE_LANES candidates of one warp share a group arena in which every
+// field is stored as [index][lane]: lanes walking the graph in near-lockstep
+// (same op index in init, the forward sweep and the lowering walk) touch the
+// same cache lines, so their accesses coalesce.  The host test harness uses
+// PE_LANES = 1 (plain structure of arrays).
+//   value slots   vhdr (kind | tile flag | loop axis | loop dim), vref, vaux,
+//                 uses, slcnt, body links, top-level position
+//   lowering      lo_buf, lo_spec, lo_acq, lo_g (REF spmd.cc:42 `Lowered`)
+//   arguments     direct-in-loop count, slice demand, atomic flag, SPMD arg
+//                 type, final registered type of the argument buffer
+//   loops         kind, axis, dim, body list, yield, result type
+//   SPMD ops      head, first operand, last use, operand offset, local bytes,
+//                 liveness delta, final registered type of the op's buffer
+//   flat          operands, top-level positions, front stack, stuck list,
+//                 carries bitmask, legal-ordinal list, operand log (trace)
+#ifndef PE_LANES
+#ifdef __CUDACC__
+#define PE_LANES 32
+#else
+#define PE_LANES 1
+#endif
+#endif
+constexpr int kLanes = PE_LANES;
+
 template <typename T, int STRIDE>
 struct Field {
   uint8_t* p;
   PE_HD T& operator[](int64_t i) const { return *reinterpret_cast<T*>(p + i * STRIDE); }
 };
+template <typename T>
+using LF = Field<T, kLanes * (int)sizeof(T)>;
 
-constexpr int kRec = 32;
-constexpr int kEmRec = 64;
+struct alignas(16) G4 {
+  int32_t v[kMaxRank];
+};
 
 struct Layout {
   Caps caps;
-  // byte offsets inside one candidate arena
+  // byte offsets inside one group arena (kLanes candidates); record arrays
+  // are interleaved [index][lane] at record granularity
   uint64_t vrec, lrec, arec, looprec, emrec;
   uint64_t opnd, pos, fs, stk, seen, em_opnd, carry, lg;
-  uint64_t bytes;
+  uint64_t bytes;  // one group arena
 };
 
+constexpr int kRec = 32;    // VRec, LowRec, LoopRec
+constexpr int kRec64 = 64;  // ArgRec, EmRec
+
+// A lane's view of its group arena: lane-adjusted base pointers (one per
+// record / element size) and the layout's offsets, which live in the kernel
+// parameter (constant) bank, so field views cost no registers.
+//   VRec   [V]   0 vhdr (vk | tile flag | loop axis | loop dim) 4 vref 8 vaux
+//                12 uses 16 slcnt 20 bnext 24 bprev 28 vpos
+//   LowRec [V]   0 buf 4 spec 8 acq 16 g[4]            (REF spmd.cc:42 Lowered)
+//   ArgRec [A]   0 direct-in-loop 4 slice demand 8 atomic 12 SPMD arg spec
+//                16 arg local bytes 24/32/40 final registered gb/lb/spec
+//   LoopRec[L]   0 kind 1 axis 2 dim 4 head 8 tail 12 yield 16 result type
+//   EmRec  [EM]  0 head 4 first operand 8 last use 12 operand offset
+//                16 local bytes 24 liveness delta 32/40/48 final gb/lb/spec
 struct Arena {
-  // VRec
-  Field<uint8_t, kRec> vk;
-  Field<int32_t, kRec> vref, vaux, uses, slcnt, bnext, bprev, vpos;
-  // LowRec
-  uint8_t* lo_base;
-  Field<int32_t, kRec> lo_buf;
-  Field<uint32_t, kRec> lo_spec;
-  Field<uint8_t, kRec> lo_acq;
-  // ArgRec (64 B)
-  Field<int32_t, 2 * kRec> adirect, aslice;
-  Field<uint8_t, 2 * kRec> awrapped;
-  Field<uint32_t, 2 * kRec> aspec0;
-  Field<int64_t, 2 * kRec> alb0;
-  // LoopRec
-  Field<uint8_t, kRec> lkind, laxis;
-  Field<int8_t, kRec> ldim;
-  Field<int32_t, kRec> lhead, ltail, lyield, ltype;
-  // EmRec
-  Field<int64_t, 2 * kRec> arg_gb, arg_lb;
-  Field<uint32_t, 2 * kRec> arg_spec;
-  // EmRec (64 B): emitted op + final registered DistType of its buffer
-  Field<int32_t, kEmRec> em_head, em_op0, em_last, em_ooff;
-  Field<int64_t, kEmRec> em_lb, delta, em_gb, em_blb;
-  Field<uint32_t, kEmRec> em_spec;
-  // flat
-  int32_t *opnd, *pos, *fs, *stk, *em_opnd, *lg;
-  uint32_t* carry;  // bit per argument: carries tiling (sliced or atomic)
-  uint8_t* seen;
+  const struct Layout* L;
+  uint8_t *b1, *b4, *r32, *r64;
+#define PE_REC(name, T, base, arr, off, STRIDE) \
+  PE_HD Field<T, STRIDE> name() const { return {base + L->arr + (off)}; }
+  PE_REC(vk, uint8_t, r32, vrec, 0, kLanes * kRec)
+  PE_REC(vh, uint32_t, r32, vrec, 0, kLanes * kRec)
+  PE_REC(vref, int32_t, r32, vrec, 4, kLanes * kRec)
+  PE_REC(vaux, int32_t, r32, vrec, 8, kLanes * kRec)
+  PE_REC(uses, int32_t, r32, vrec, 12, kLanes * kRec)
+  PE_REC(slcnt, int32_t, r32, vrec, 16, kLanes * kRec)
+  PE_REC(bnext, int32_t, r32, vrec, 20, kLanes * kRec)
+  PE_REC(bprev, int32_t, r32, vrec, 24, kLanes * kRec)
+  PE_REC(vpos, int32_t, r32, vrec, 28, kLanes * kRec)
+  PE_REC(lo_buf, int32_t, r32, lrec, 0, kLanes * kRec)
+  PE_REC(lo_spec, uint32_t, r32, lrec, 4, kLanes * kRec)
+  PE_REC(lo_acq, uint32_t, r32, lrec, 8, kLanes * kRec)
+  PE_REC(lo_g, G4, r32, lrec, 16, kLanes * kRec)
+  PE_REC(adirect, int32_t, r64, arec, 0, kLanes * kRec64)
+  PE_REC(aslice, int32_t, r64, arec, 4, kLanes * kRec64)
+  PE_REC(awrapped, uint8_t, r64, arec, 8, kLanes * kRec64)
+  PE_REC(aspec0, uint32_t, r64, arec, 12, kLanes * kRec64)
+  PE_REC(alb0, int64_t, r64, arec, 16, kLanes * kRec64)
+  PE_REC(arg_gb, int64_t, r64, arec, 24, kLanes * kRec64)
+  PE_REC(arg_lb, int64_t, r64, arec, 32, kLanes * kRec64)
+  PE_REC(arg_spec, uint32_t, r64, arec, 40, kLanes * kRec64)
+  PE_REC(lkind, uint8_t, r32, looprec, 0, kLanes * kRec)
+  PE_REC(laxis, uint8_t, r32, looprec, 1, kLanes * kRec)
+  PE_REC(ldim, int8_t, r32, looprec, 2, kLanes * kRec)
+  PE_REC(lhead, int32_t, r32, looprec, 4, kLanes * kRec)
+  PE_REC(ltail, int32_t, r32, looprec, 8, kLanes * kRec)
+  PE_REC(lyield, int32_t, r32, looprec, 12, kLanes * kRec)
+  PE_REC(ltype, int32_t, r32, looprec, 16, kLanes * kRec)
+  PE_REC(em_head, int32_t, r64, emrec, 0, kLanes * kRec64)
+  PE_REC(em_op0, int32_t, r64, emrec, 4, kLanes * kRec64)
+  PE_REC(em_last, int32_t, r64, emrec, 8, kLanes * kRec64)
+  PE_REC(em_ooff, int32_t, r64, emrec, 12, kLanes * kRec64)
+  PE_REC(em_lb, int64_t, r64, emrec, 16, kLanes * kRec64)
+  PE_REC(delta, int64_t, r64, emrec, 24, kLanes * kRec64)
+  PE_REC(em_gb, int64_t, r64, emrec, 32, kLanes * kRec64)
+  PE_REC(em_blb, int64_t, r64, emrec, 40, kLanes * kRec64)
+  PE_REC(em_spec, uint32_t, r64, emrec, 48, kLanes * kRec64)
+  PE_REC(opnd, int32_t, b4, opnd, 0, kLanes * 4)
+  PE_REC(pos, int32_t, b4, pos, 0, kLanes * 4)
+  PE_REC(fs, int32_t, b4, fs, 0, kLanes * 4)
+  PE_REC(stk, int32_t, b4, stk, 0, kLanes * 4)
+  PE_REC(em_opnd, int32_t, b4, em_opnd, 0, kLanes * 4)
+  PE_REC(lg, int32_t, b4, lg, 0, kLanes * 4)
+  PE_REC(carry, uint32_t, b4, carry, 0, kLanes * 4)
+  PE_REC(seen, uint8_t, b1, seen, 0, kLanes * 1)
+#undef PE_REC
 };
 
 PE_HD uint64_t align8(uint64_t x) { return (x + 7) & ~uint64_t(7); }
@@ -116,7 +172,7 @@ PE_HD uint64_t align128(uint64_t x) { return (x + 127) & ~uint64_t(127); }
 
 inline Layout relayout(const GraphView& g, const Caps& caps);
 
-// Host-side sizing (DESIGN.md §3.4).  The FULL layout's bounds are
+// Host-side sizing (DESIGN.md §3.1).  The FULL layout's bounds are
 // structural: every original op is pulled or migrated at most once, every
 // value is tiled at most once.  The TIGHT layout is sized from measured
 // high-water marks (slots ~ N+E, SPMD ops ~ 1.45 N on the 24-layer graph)
@@ -144,87 +200,42 @@ inline Layout make_layout(const GraphView& g, bool tight = false) {
   return relayout(g, L.caps);
 }
 
-// Byte offsets of every per-candidate array for the given capacities.
+// Byte offsets of every array of a group arena for the given capacities.
 inline Layout relayout(const GraphView& g, const Caps& caps) {
   Layout L{};
   L.caps = caps;
-  int32_t A = g.A, N = g.N, E = g.E;
+  int64_t A = g.A, N = g.N, E = g.E;
   uint64_t o = 0;
-  auto take = [&](uint64_t bytes) {
+  auto take = [&](int64_t elems, int64_t elem_bytes) {
     uint64_t at = o;
-    o = align128(o + bytes);
+    o = align128(o + (uint64_t)(elems + 1) * elem_bytes * kLanes);
     return at;
   };
-  int64_t V = L.caps.V, Lc = L.caps.L, EM = L.caps.EM;
-  L.vrec = take(kRec * V);
-  L.lrec = take(kRec * V);
-  L.arec = take(2 * kRec * ((int64_t)A + 1));
-  L.looprec = take(kRec * Lc);
-  L.emrec = take(kEmRec * (EM + 1));
-  L.opnd = take(4 * (int64_t)E + 4);
-  L.pos = take(8 * (int64_t)N + 8);
-  L.fs = take(4 * (int64_t)L.caps.FS);
-  L.stk = take(8 * (int64_t)N + 8);
-  L.seen = take((int64_t)N + 8);
-  L.em_opnd = take(4 * (int64_t)L.caps.EO);
-  L.carry = take(4 * ((int64_t)A / 32 + 2));
-  L.lg = take(4 * ((int64_t)g.n_ord + 1));
+  L.vrec = take(caps.V, kRec);
+  L.lrec = take(caps.V, kRec);
+  L.arec = take(A, kRec64);
+  L.looprec = take(caps.L, kRec);
+  L.emrec = take((int64_t)caps.EM + 1, kRec64);
+  L.opnd = take(E, 4);
+  L.pos = take(2 * N, 4);
+  L.fs = take(caps.FS, 4);
+  L.stk = take(2 * N, 4);
+  L.seen = take(N, 1);
+  L.em_opnd = take(caps.EO, 4);
+  L.carry = take(A / 32 + 1, 4);
+  L.lg = take(g.n_ord, 4);
   L.bytes = align128(o);
   return L;
 }
 
-PE_HD Arena carve(const Layout& L, uint8_t* base) {
+// View of lane `lane` inside the group arena at `base`.
+PE_HD Arena carve(const Layout& L, uint8_t* base, int lane = 0) {
   Arena a;
-  uint8_t* v = base + L.vrec;
-  a.vk = {v + 0};
-  a.vref = {v + 4};
-  a.vaux = {v + 8};
-  a.uses = {v + 12};
-  a.slcnt = {v + 16};
-  a.bnext = {v + 20};
-  a.bprev = {v + 24};
-  a.vpos = {v + 28};
-  uint8_t* lo = base + L.lrec;
-  a.lo_base = lo;
-  a.lo_buf = {lo + 0};
-  a.lo_spec = {lo + 4};
-  a.lo_acq = {lo + 8};
-  // ArgRec is 64 B: state (0..23) + the buffer's final registered type (24..47)
-  uint8_t* ar = base + L.arec;
-  a.adirect = {ar + 0};
-  a.aslice = {ar + 4};
-  a.awrapped = {ar + 8};
-  a.aspec0 = {ar + 12};
-  a.alb0 = {ar + 16};
-  a.arg_gb = {ar + 24};
-  a.arg_lb = {ar + 32};
-  a.arg_spec = {ar + 40};
-  uint8_t* lr = base + L.looprec;
-  a.lkind = {lr + 0};
-  a.laxis = {lr + 1};
-  a.ldim = {lr + 2};
-  a.lhead = {lr + 4};
-  a.ltail = {lr + 8};
-  a.lyield = {lr + 12};
-  a.ltype = {lr + 16};
-  uint8_t* em = base + L.emrec;
-  a.em_head = {em + 0};
-  a.em_op0 = {em + 4};
-  a.em_last = {em + 8};
-  a.em_ooff = {em + 12};
-  a.em_lb = {em + 16};
-  a.delta = {em + 24};
-  a.em_gb = {em + 32};
-  a.em_blb = {em + 40};
-  a.em_spec = {em + 48};
-  a.opnd = (int32_t*)(base + L.opnd);
-  a.pos = (int32_t*)(base + L.pos);
-  a.fs = (int32_t*)(base + L.fs);
-  a.stk = (int32_t*)(base + L.stk);
-  a.seen = base + L.seen;
-  a.em_opnd = (int32_t*)(base + L.em_opnd);
-  a.carry = (uint32_t*)(base + L.carry);
-  a.lg = (int32_t*)(base + L.lg);
+  a.L = &L;
+  a.b1 = base + (uint64_t)lane;
+  a.b4 = base + (uint64_t)lane * 4;
+  a.r32 = base + (uint64_t)lane * kRec;
+  a.r64 = base + (uint64_t)lane * kRec64;
   return a;
 }
 
@@ -284,8 +295,8 @@ struct Cand {
   PE_HD void tick(int) {}
 #endif
 
-  PE_HD Cand(const GraphView& gv, const Layout& L, uint8_t* base)
-      : g(gv), caps(L.caps), a(carve(L, base)) {
+  PE_HD Cand(const GraphView& gv, const Layout& L, uint8_t* base, int lane = 0)
+      : g(gv), caps(L.caps), a(carve(L, base, lane)) {
 #if defined(PE_PHASE_TIMERS) && defined(__CUDA_ARCH__)
     for (int k = 0; k < 9; ++k) ph[k] = 0;
 #endif
@@ -301,24 +312,22 @@ struct Cand {
   // VRec header word: vk | tile-loop flag << 8 | loop axis << 16 | loop dim << 24
   // (loop axis/dim denormalised into the value record so the sweeps test
   // "operand is a tile loop on (axis, dim)" with one load)
-  PE_HD uint32_t vhdr(int32_t v) const {
-    return *reinterpret_cast<const uint32_t*>(a.vk.p + (int64_t)v * kRec);
-  }
+  PE_HD uint32_t vhdr(int32_t v) const { return a.vh()[v]; }
   PE_HD static bool hdr_tile(uint32_t h) { return (h & 0x1FFu) == (VK_LOOP | 0x100u); }
   PE_HD static int32_t hdr_axis(uint32_t h) { return (int32_t)((h >> 16) & 0xFFu); }
   PE_HD static int32_t hdr_dim(uint32_t h) { return (int32_t)(int8_t)(h >> 24); }
   PE_HD bool is_tile_loop(int32_t v) const { return hdr_tile(vhdr(v)); }
   // refresh the denormalised loop info of loop value v (loop record l)
   PE_HD void mark_loop_value(int32_t v, int32_t l) {
-    uint32_t h = (uint32_t)VK_LOOP | ((a.lkind[l] == LK_TILE ? 1u : 0u) << 8) |
-                 ((uint32_t)a.laxis[l] << 16) | ((uint32_t)(uint8_t)a.ldim[l] << 24);
-    *reinterpret_cast<uint32_t*>(a.vk.p + (int64_t)v * kRec) = h;
+    uint32_t h = (uint32_t)VK_LOOP | ((a.lkind()[l] == LK_TILE ? 1u : 0u) << 8) |
+                 ((uint32_t)a.laxis()[l] << 16) | ((uint32_t)(uint8_t)a.ldim()[l] << 24);
+    a.vh()[v] = h;
   }
   // original value whose global shape a top-level value carries
   PE_HD int32_t shape_src(int32_t v) const {
-    uint8_t k = a.vk[v];
-    if (k == VK_LOOP) return a.ltype[a.vref[v]];
-    if (k == VK_ATOMIC) return a.vref[v];
+    uint8_t k = a.vk()[v];
+    if (k == VK_LOOP) return a.ltype()[a.vref()[v]];
+    if (k == VK_ATOMIC) return a.vref()[v];
     return v;  // ARG / TOP
   }
   PE_HD int32_t alloc_slot() {
@@ -327,11 +336,11 @@ struct Cand {
       return -1;
     }
     int32_t s = nslots++;
-    a.slcnt[s] = 0;
-    a.uses[s] = 0;
-    a.bnext[s] = -1;
-    a.bprev[s] = -1;
-    a.vpos[s] = 0;
+    a.slcnt()[s] = 0;
+    a.uses()[s] = 0;
+    a.bnext()[s] = -1;
+    a.bprev()[s] = -1;
+    a.vpos()[s] = 0;
     return s;
   }
   PE_HD int32_t alloc_loop() {
@@ -340,29 +349,29 @@ struct Cand {
       return -1;
     }
     int32_t l = nloops++;
-    a.lhead[l] = -1;
-    a.ltail[l] = -1;
+    a.lhead()[l] = -1;
+    a.ltail()[l] = -1;
     return l;
   }
   PE_HD void body_append(int32_t l, int32_t s) {
-    a.bnext[s] = -1;
-    a.bprev[s] = a.ltail[l];
-    if (a.ltail[l] >= 0) a.bnext[a.ltail[l]] = s;
-    else a.lhead[l] = s;
-    a.ltail[l] = s;
+    a.bnext()[s] = -1;
+    a.bprev()[s] = a.ltail()[l];
+    if (a.ltail()[l] >= 0) a.bnext()[a.ltail()[l]] = s;
+    else a.lhead()[l] = s;
+    a.ltail()[l] = s;
   }
   PE_HD void body_insert_before(int32_t l, int32_t at, int32_t s) {
-    int32_t p = a.bprev[at];
-    a.bprev[s] = p;
-    a.bnext[s] = at;
-    a.bprev[at] = s;
-    if (p >= 0) a.bnext[p] = s;
-    else a.lhead[l] = s;
+    int32_t p = a.bprev()[at];
+    a.bprev()[s] = p;
+    a.bnext()[s] = at;
+    a.bprev()[at] = s;
+    if (p >= 0) a.bnext()[p] = s;
+    else a.lhead()[l] = s;
   }
   PE_HD void set_pos(int32_t v, int32_t code) {
-    a.vpos[v] = code;
-    if (code >= 0) a.pos[code] = v;
-    else a.fs[-code - 1] = v;
+    a.vpos()[v] = code;
+    if (code >= 0) a.pos()[code] = v;
+    else a.fs()[-code - 1] = v;
   }
   PE_HD void push_front(int32_t v) {
     if (nfs >= caps.FS) {
@@ -373,26 +382,26 @@ struct Cand {
     nfs++;
   }
   PE_HD void clear_pos(int32_t v) {
-    int32_t code = a.vpos[v];
-    if (code >= 0) a.pos[code] = -1;
-    else a.fs[-code - 1] = -1;
+    int32_t code = a.vpos()[v];
+    if (code >= 0) a.pos()[code] = -1;
+    else a.fs()[-code - 1] = -1;
   }
   // REF rewrite.cc:27-38 replace_uses: every operand occurrence of an
   // original value lives in one of its original operand slots.
   PE_HD void replace_uses(int32_t v, int32_t t) {
     for (int32_t i = g.user_off[v]; i < g.user_off[v + 1]; ++i) {
       int32_t s = g.users[i];
-      if (a.opnd[s] == v) a.opnd[s] = t;
+      if (a.opnd()[s] == v) a.opnd()[s] = t;
     }
     if (result_ref == v) result_ref = t;
   }
   PE_HD void slice_created(int32_t u, int32_t d, int32_t axis) {
-    a.slcnt[u]++;
+    a.slcnt()[u]++;
     if (u < g.A) {
-      a.carry[u >> 5] |= 1u << (u & 31);
+      a.carry()[u >> 5] |= 1u << (u & 31);
       int32_t pair = d | (axis << 3);
-      if (a.aslice[u] == -1) a.aslice[u] = pair;
-      else if (a.aslice[u] != pair) a.aslice[u] = -2;
+      if (a.aslice()[u] == -1) a.aslice()[u] = pair;
+      else if (a.aslice()[u] != pair) a.aslice()[u] = -2;
     }
   }
   PE_HD bool is_member(int32_t gc, int32_t k) const {
@@ -405,26 +414,26 @@ struct Cand {
   PE_HD void init() {
     int32_t A = g.A, N = g.N;
     for (int32_t v = 0; v < A; ++v) {
-      a.vk[v] = VK_ARG;
-      a.vref[v] = v;
-      a.uses[v] = g.init_uses[v];
-      a.slcnt[v] = 0;
-      a.adirect[v] = 0;
-      a.aslice[v] = -1;
-      a.awrapped[v] = 0;
+      a.vk()[v] = VK_ARG;
+      a.vref()[v] = v;
+      a.uses()[v] = g.init_uses[v];
+      a.slcnt()[v] = 0;
+      a.adirect()[v] = 0;
+      a.aslice()[v] = -1;
+      a.awrapped()[v] = 0;
     }
     for (int32_t o = 0; o < N; ++o) {
       int32_t v = A + o;
-      a.vk[v] = VK_TOP;
-      a.vref[v] = o;
-      a.uses[v] = g.init_uses[v];
-      a.slcnt[v] = 0;
-      a.vpos[v] = 2 * o;
-      a.pos[2 * o] = v;
-      a.pos[2 * o + 1] = -1;
+      a.vk()[v] = VK_TOP;
+      a.vref()[v] = o;
+      a.uses()[v] = g.init_uses[v];
+      a.slcnt()[v] = 0;
+      a.vpos()[v] = 2 * o;
+      a.pos()[2 * o] = v;
+      a.pos()[2 * o + 1] = -1;
     }
-    for (int32_t s = 0; s < g.E; ++s) a.opnd[s] = g.oopnd[s];
-    for (int32_t w = 0; w <= (A >> 5); ++w) a.carry[w] = 0;
+    for (int32_t s = 0; s < g.E; ++s) a.opnd()[s] = g.oopnd[s];
+    for (int32_t w = 0; w <= (A >> 5); ++w) a.carry()[w] = 0;
     nslots = A + N;
     nloops = 0;
     nfs = 0;
@@ -440,16 +449,16 @@ struct Cand {
   // ------------------------------------------------------------ actions
   // carries_tiling (REF rewrite.cc:42-51) for an original value at top level
   PE_HD bool carries(int32_t v) const {
-    if (a.vk[v] == VK_LOOP) return true;
-    if (a.slcnt[v] > 0) return true;
-    return v < g.A && a.awrapped[v];
+    if (a.vk()[v] == VK_LOOP) return true;
+    if (a.slcnt()[v] > 0) return true;
+    return v < g.A && a.awrapped()[v];
   }
 
   // apply_tile_action (REF rewrite.cc:61-113).  Returns false when illegal
   // (IllegalActionError); the state is untouched in that case.
   PE_HD bool apply_tile(int32_t v, int32_t dim, int32_t axis) {
     if (v < 0 || v >= NV()) return false;
-    uint8_t k = a.vk[v];
+    uint8_t k = a.vk()[v];
     if (k != VK_ARG && k != VK_TOP && k != VK_LOOP) return false;  // erased: does not exist
     if (axis < 0 || axis >= g.n_axes) return false;
     if (dim < 0 || dim >= g.vrank[v]) return false;
@@ -459,20 +468,20 @@ struct Cand {
     int32_t ls = alloc_slot();
     int32_t s = alloc_slot();
     if (bad()) return false;
-    a.lkind[l] = LK_TILE;
-    a.laxis[l] = (uint8_t)axis;
-    a.ldim[l] = (int8_t)dim;
-    a.ltype[l] = v;
-    a.lyield[l] = s;
-    a.vref[ls] = l;
+    a.lkind()[l] = LK_TILE;
+    a.laxis()[l] = (uint8_t)axis;
+    a.ldim()[l] = (int8_t)dim;
+    a.ltype()[l] = v;
+    a.lyield()[l] = s;
+    a.vref()[ls] = l;
     mark_loop_value(ls, l);
-    a.uses[ls] = a.uses[v];
-    a.vk[s] = VK_SLICE;
-    a.vref[s] = v;
-    a.vaux[s] = dim | (l << 3);
-    a.uses[s] = 1;  // the loop yield
+    a.uses()[ls] = a.uses()[v];
+    a.vk()[s] = VK_SLICE;
+    a.vref()[s] = v;
+    a.vaux()[s] = dim | (l << 3);
+    a.uses()[s] = 1;  // the loop yield
     body_append(l, s);
-    a.uses[v] = 1;  // the slice
+    a.uses()[v] = 1;  // the slice
     slice_created(v, dim, axis);
     replace_uses(v, ls);
     if (v < g.A) push_front(ls);
@@ -506,7 +515,7 @@ struct Cand {
     int32_t base = g.oopnd_off[o], n = g.oopnd_off[o + 1] - base;
     int32_t cbase = g.ocls_off[o];
     for (int32_t k = 0; k < n; ++k) {
-      int32_t u = a.opnd[base + k];
+      int32_t u = a.opnd()[base + k];
       uint32_t h = vhdr(u);
       if (!hdr_tile(h)) continue;
       int32_t c = g.slot_cls[(base + k) * 4 + hdr_dim(h)];
@@ -522,7 +531,7 @@ struct Cand {
     }
     if (p.drive < 0) return p;
     for (int32_t k = 0; k < n; ++k) {
-      uint32_t h = vhdr(a.opnd[base + k]);
+      uint32_t h = vhdr(a.opnd()[base + k]);
       if (!hdr_tile(h)) continue;
       if (hdr_axis(h) == p.axis && g.slot_cls[(base + k) * 4 + hdr_dim(h)] != p.cls) {
         p.reason = R_CONFLICT;
@@ -533,7 +542,7 @@ struct Cand {
     int32_t gc = cbase + p.cls;
     for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
       int32_t k = g.mem[m] >> 2, d = g.mem[m] & 3;
-      int32_t u = a.opnd[base + k];
+      int32_t u = a.opnd()[base + k];
       if (g.shape(shape_src(u))[d] % sz != 0) {
         p.reason = R_INSUFFICIENT;
         return p;
@@ -553,7 +562,7 @@ struct Cand {
 
   PE_HD bool has_tiled_operand(int32_t o) const {
     for (int32_t s = g.oopnd_off[o]; s < g.oopnd_off[o + 1]; ++s)
-      if (is_tile_loop(a.opnd[s])) return true;
+      if (is_tile_loop(a.opnd()[s])) return true;
     return false;
   }
 
@@ -566,31 +575,31 @@ struct Cand {
     bool contracting = g.cls_role[gc] == kContract;
     int32_t rd = g.cls_rdim[gc];
     int32_t lv0 = p.drive;
-    bool extend = !contracting && a.uses[lv0] == 1;
+    bool extend = !contracting && a.uses()[lv0] == 1;
     int32_t f = alloc_slot();
-    int32_t l = extend ? a.vref[lv0] : alloc_loop();
+    int32_t l = extend ? a.vref()[lv0] : alloc_loop();
     if (bad()) return;
     if (!extend) {
-      a.lkind[l] = contracting ? LK_SUM : LK_TILE;
-      a.laxis[l] = (uint8_t)p.axis;
-      a.ldim[l] = (int8_t)(contracting ? -1 : rd);
+      a.lkind()[l] = contracting ? LK_SUM : LK_TILE;
+      a.laxis()[l] = (uint8_t)p.axis;
+      a.ldim()[l] = (int8_t)(contracting ? -1 : rd);
     }
-    a.vk[f] = VK_LOCAL;
-    a.vref[f] = o;
-    a.vaux[f] = (contracting ? 0 : rd + 1) | (l << 3);
-    a.uses[f] = 1;  // yielded
+    a.vk()[f] = VK_LOCAL;
+    a.vref()[f] = o;
+    a.vaux()[f] = (contracting ? 0 : rd + 1) | (l << 3);
+    a.uses()[f] = 1;  // yielded
     // slice cache: members of one class reference at most its member count
     int32_t cache_u[8], cache_d[8], cache_s[8];
     int32_t nc = 0;
     for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
       int32_t k = g.mem[m] >> 2, d = g.mem[m] & 3;
       int32_t ps = base + k;
-      int32_t u = a.opnd[ps];
+      int32_t u = a.opnd()[ps];
       if (extend && u == lv0) {
-        int32_t y = a.lyield[l];
-        a.opnd[ps] = y;
-        a.uses[lv0]--;
-        a.uses[y]++;
+        int32_t y = a.lyield()[l];
+        a.opnd()[ps] = y;
+        a.uses()[lv0]--;
+        a.uses()[y]++;
         continue;
       }
       int32_t sl = -1;
@@ -600,20 +609,20 @@ struct Cand {
         // linear search fallback for very wide concatenates
         for (int32_t q = g.cls_moff[gc]; q < m && sl < 0 && nc >= 8; ++q) {
           int32_t k2 = g.mem[q] >> 2, d2 = g.mem[q] & 3;
-          int32_t s2 = a.opnd[base + k2];
-          if (d2 == d && a.vk[s2] == VK_SLICE && a.vref[s2] == u &&
-              (a.vaux[s2] >> 3) == l && (a.vaux[s2] & 7) == d)
+          int32_t s2 = a.opnd()[base + k2];
+          if (d2 == d && a.vk()[s2] == VK_SLICE && a.vref()[s2] == u &&
+              (a.vaux()[s2] >> 3) == l && (a.vaux()[s2] & 7) == d)
             sl = s2;
         }
       }
       if (sl < 0) {
         sl = alloc_slot();
         if (bad()) return;
-        a.vk[sl] = VK_SLICE;
-        a.vref[sl] = u;
-        a.vaux[sl] = d | (l << 3);
+        a.vk()[sl] = VK_SLICE;
+        a.vref()[sl] = u;
+        a.vaux()[sl] = d | (l << 3);
         body_append(l, sl);
-        a.uses[u]++;
+        a.uses()[u]++;
         slice_created(u, d, p.axis);
         if (nc < 8) {
           cache_u[nc] = u;
@@ -622,31 +631,31 @@ struct Cand {
           nc++;
         }
       }
-      a.opnd[ps] = sl;
-      a.uses[u]--;
-      a.uses[sl]++;
+      a.opnd()[ps] = sl;
+      a.uses()[u]--;
+      a.uses()[sl]++;
     }
     for (int32_t k = 0; k < n; ++k) {
-      int32_t u = a.opnd[base + k];
-      if (a.vk[u] == VK_ARG && !is_member(gc, k)) a.adirect[u]++;
+      int32_t u = a.opnd()[base + k];
+      if (a.vk()[u] == VK_ARG && !is_member(gc, k)) a.adirect()[u]++;
     }
-    if (extend) a.uses[a.lyield[l]]--;  // old yield is no longer yielded
-    a.lyield[l] = f;
+    if (extend) a.uses()[a.lyield()[l]]--;  // old yield is no longer yielded
+    a.lyield()[l] = f;
     body_append(l, f);
-    a.ltype[l] = g.A + o;
+    a.ltype()[l] = g.A + o;
     if (extend) {
-      a.ldim[l] = (int8_t)rd;
+      a.ldim()[l] = (int8_t)rd;
       clear_pos(lv0);
-      a.vk[lv0] = VK_DEAD;
+      a.vk()[lv0] = VK_DEAD;
     }
     int32_t xv = g.A + o;
-    a.vref[xv] = l;
+    a.vref()[xv] = l;
     mark_loop_value(xv, l);
   }
 
   PE_HD void forward() {
     for (int32_t o = 0; o < g.N; ++o) {
-      if (a.vk[g.A + o] != VK_TOP) continue;
+      if (a.vk()[g.A + o] != VK_TOP) continue;
       if (!has_tiled_operand(o)) continue;
       if (g.orule_err[o]) {
         fail(PE_CAND_INTERNAL);
@@ -663,16 +672,16 @@ struct Cand {
   // REF propagate.cc:284-375: migrate single-use producers of sliced values
   // into the consuming loop, visiting loops and their body slices in order.
   PE_HD void backward_loop(int32_t l) {
-    int32_t sz_axis = a.laxis[l];
+    int32_t sz_axis = a.laxis()[l];
     int64_t sz = asz(sz_axis);
-    int32_t s = a.lhead[l];
+    int32_t s = a.lhead()[l];
     while (s >= 0) {
-      int32_t next = a.bnext[s];
-      if (a.vk[s] == VK_SLICE) {
-        int32_t u = a.vref[s];
-        int32_t d = a.vaux[s] & 7;
-        if (a.vk[u] == VK_TOP && a.uses[u] == 1) {
-          int32_t P = a.vref[u];
+      int32_t next = a.bnext()[s];
+      if (a.vk()[s] == VK_SLICE) {
+        int32_t u = a.vref()[s];
+        int32_t d = a.vaux()[s] & 7;
+        if (a.vk()[u] == VK_TOP && a.uses()[u] == 1) {
+          int32_t P = a.vref()[u];
           uint8_t kind = g.okind[P];
           int32_t pb = g.oopnd_off[P], pn = g.oopnd_off[P + 1] - pb;
           bool simple = kind == kConstant ||
@@ -692,7 +701,7 @@ struct Cand {
               gc = g.ocls_off[P] + rc;
               for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
                 int32_t k = g.mem[m] >> 2, dd = g.mem[m] & 3;
-                int32_t w = a.opnd[pb + k];
+                int32_t w = a.opnd()[pb + k];
                 if (g.shape(shape_src(w))[dd] % sz != 0) go = false;
                 uint32_t h = vhdr(w);
                 if (hdr_tile(h)) {
@@ -708,27 +717,27 @@ struct Cand {
               int32_t nc = 0;
               for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
                 int32_t k = g.mem[m] >> 2, dd = g.mem[m] & 3;
-                int32_t w = a.opnd[pb + k];
+                int32_t w = a.opnd()[pb + k];
                 int32_t sl = -1;
                 for (int32_t c = 0; c < nc; ++c)
                   if (cache_u[c] == w && cache_d[c] == dd) sl = cache_s[c];
                 if (sl < 0 && nc >= 8) {
                   for (int32_t q = g.cls_moff[gc]; q < m && sl < 0; ++q) {
                     int32_t k2 = g.mem[q] >> 2, d2 = g.mem[q] & 3;
-                    int32_t s2 = a.opnd[pb + k2];
-                    if (d2 == dd && a.vk[s2] == VK_SLICE && a.vref[s2] == w &&
-                        (a.vaux[s2] >> 3) == l)
+                    int32_t s2 = a.opnd()[pb + k2];
+                    if (d2 == dd && a.vk()[s2] == VK_SLICE && a.vref()[s2] == w &&
+                        (a.vaux()[s2] >> 3) == l)
                       sl = s2;
                   }
                 }
                 if (sl < 0) {
                   sl = alloc_slot();
                   if (bad()) return;
-                  a.vk[sl] = VK_SLICE;
-                  a.vref[sl] = w;
-                  a.vaux[sl] = dd | (l << 3);
+                  a.vk()[sl] = VK_SLICE;
+                  a.vref()[sl] = w;
+                  a.vaux()[sl] = dd | (l << 3);
                   body_insert_before(l, s, sl);
-                  a.uses[w]++;
+                  a.uses()[w]++;
                   slice_created(w, dd, sz_axis);
                   if (first_new < 0) first_new = sl;
                   if (nc < 8) {
@@ -738,23 +747,23 @@ struct Cand {
                     nc++;
                   }
                 }
-                a.opnd[pb + k] = sl;
-                a.uses[w]--;
-                a.uses[sl]++;
+                a.opnd()[pb + k] = sl;
+                a.uses()[w]--;
+                a.uses()[sl]++;
               }
             }
             for (int32_t k = 0; k < pn; ++k) {
-              int32_t w = a.opnd[pb + k];
-              if (a.vk[w] == VK_ARG && (simple || !is_member(gc, k))) a.adirect[w]++;
+              int32_t w = a.opnd()[pb + k];
+              if (a.vk()[w] == VK_ARG && (simple || !is_member(gc, k))) a.adirect()[w]++;
             }
             // the slice becomes P's per-iteration copy (it keeps S's name)
-            a.vk[s] = VK_LOCAL;
-            a.vref[s] = P;
-            a.vaux[s] = (d + 1) | (l << 3);
-            a.slcnt[u]--;
+            a.vk()[s] = VK_LOCAL;
+            a.vref()[s] = P;
+            a.vaux()[s] = (d + 1) | (l << 3);
+            a.slcnt()[u]--;
             clear_pos(u);
-            a.vk[u] = VK_DEAD;
-            next = first_new >= 0 ? first_new : a.bnext[s];
+            a.vk()[u] = VK_DEAD;
+            next = first_new >= 0 ? first_new : a.bnext()[s];
           }
         }
       }
@@ -765,14 +774,14 @@ struct Cand {
   template <typename F>
   PE_HD void for_top(F&& f) {
     for (int32_t i = nfs - 1; i >= 0; --i) {
-      int32_t v = a.fs[i];
+      int32_t v = a.fs()[i];
       if (v >= 0) {
         f(v);
         if (bad()) return;
       }
     }
     for (int32_t p = 0; p < 2 * g.N; ++p) {
-      int32_t v = a.pos[p];
+      int32_t v = a.pos()[p];
       if (v >= 0) {
         f(v);
         if (bad()) return;
@@ -782,7 +791,7 @@ struct Cand {
 
   PE_HD void backward() {
     for_top([&](int32_t v) {
-      if (a.vk[v] == VK_LOOP) backward_loop(a.vref[v]);
+      if (a.vk()[v] == VK_LOOP) backward_loop(a.vref()[v]);
     });
   }
 
@@ -790,16 +799,16 @@ struct Cand {
   // inside a loop and never sliced are wrapped atomic, each at index 0.
   PE_HD void wrap() {
     for (int32_t x = 0; x < g.A; ++x) {
-      if (a.adirect[x] == 0 || a.slcnt[x] != 0 || a.awrapped[x]) continue;
+      if (a.adirect()[x] == 0 || a.slcnt()[x] != 0 || a.awrapped()[x]) continue;
       int32_t t = alloc_slot();
       if (bad()) return;
-      a.vk[t] = VK_ATOMIC;
-      a.vref[t] = x;
-      a.uses[t] = a.uses[x];
+      a.vk()[t] = VK_ATOMIC;
+      a.vref()[t] = x;
+      a.uses()[t] = a.uses()[x];
       replace_uses(x, t);
-      a.uses[x] = 1;
-      a.awrapped[x] = 1;
-      a.carry[x >> 5] |= 1u << (x & 31);
+      a.uses()[x] = 1;
+      a.awrapped()[x] = 1;
+      a.carry()[x >> 5] |= 1u << (x & 31);
       push_front(t);
       if (bad()) return;
     }
@@ -820,27 +829,27 @@ struct Cand {
   // stuck analysis (REF propagate.cc:412-454), dedup by op id in discovery
   // order (:477-479).
   PE_HD void add_stuck(int32_t o, int32_t r) {
-    if (a.seen[o]) return;
-    a.seen[o] = 1;
-    a.stk[2 * nstk] = o;
-    a.stk[2 * nstk + 1] = r;
+    if (a.seen()[o]) return;
+    a.seen()[o] = 1;
+    a.stk()[2 * nstk] = o;
+    a.stk()[2 * nstk + 1] = r;
     nstk++;
   }
   PE_HD void analyze() {
-    for (int32_t o = 0; o < g.N; ++o) a.seen[o] = 0;
+    for (int32_t o = 0; o < g.N; ++o) a.seen()[o] = 0;
     nstk = 0;
     for_top([&](int32_t v) {
-      uint8_t k = a.vk[v];
+      uint8_t k = a.vk()[v];
       if (k == VK_LOOP) {
-        int32_t l = a.vref[v];
-        for (int32_t s = a.lhead[l]; s >= 0; s = a.bnext[s]) {
-          if (a.vk[s] != VK_SLICE) continue;
-          int32_t u = a.vref[s], d = a.vaux[s] & 7;
-          if (a.vk[u] != VK_TOP) continue;
-          int32_t P = a.vref[u];
+        int32_t l = a.vref()[v];
+        for (int32_t s = a.lhead()[l]; s >= 0; s = a.bnext()[s]) {
+          if (a.vk()[s] != VK_SLICE) continue;
+          int32_t u = a.vref()[s], d = a.vaux()[s] & 7;
+          if (a.vk()[u] != VK_TOP) continue;
+          int32_t P = a.vref()[u];
           uint8_t kind = g.okind[P];
           if (kind == kConstant) continue;
-          if (a.uses[u] != 1) continue;
+          if (a.uses()[u] != 1) continue;
           if (kind == kBroadcastInDim && !((g.omask[P] >> d) & 1)) continue;
           if (g.orule_err[P]) {
             fail(PE_CAND_INTERNAL);
@@ -849,7 +858,7 @@ struct Cand {
           if (g.op_rcls[P * 4 + d] < 0) add_stuck(P, R_BLOCKED);
         }
       } else if (k == VK_TOP) {
-        int32_t o = a.vref[v];
+        int32_t o = a.vref()[v];
         if (!has_tiled_operand(o)) return;
         if (g.orule_err[o]) {
           fail(PE_CAND_INTERNAL);
@@ -890,31 +899,32 @@ struct Cand {
     return e;
   }
   PE_HD Low load(int32_t v) const {
-    const int32_t* r = reinterpret_cast<const int32_t*>(a.lo_base + (int64_t)v * kRec);
     Low w;
-    w.buf = r[0];
-    w.spec = (uint32_t)r[1];
-    w.acq = (uint32_t)r[2] & 0xFFu;
-    for (int d = 0; d < kMaxRank; ++d) w.g[d] = r[3 + d];
+    w.buf = a.lo_buf()[v];
+    w.spec = a.lo_spec()[v];
+    w.acq = a.lo_acq()[v];
+    G4 gg = a.lo_g()[v];
+    for (int d = 0; d < kMaxRank; ++d) w.g[d] = gg.v[d];
     return w;
   }
   PE_HD void store(int32_t v, const Low& w) {
-    int32_t* r = reinterpret_cast<int32_t*>(a.lo_base + (int64_t)v * kRec);
-    r[0] = w.buf;
-    r[1] = (int32_t)w.spec;
-    r[2] = (int32_t)w.acq;
-    for (int d = 0; d < kMaxRank; ++d) r[3 + d] = w.g[d];
+    a.lo_buf()[v] = w.buf;
+    a.lo_spec()[v] = w.spec;
+    a.lo_acq()[v] = w.acq;
+    G4 gg;
+    for (int d = 0; d < kMaxRank; ++d) gg.v[d] = w.g[d];
+    a.lo_g()[v] = gg;
   }
   PE_HD void register_type(int32_t buf, const Low& w) {
     int64_t gb = global_bytes(w), lb = 4 * local_elems(w);
     if (buf < g.A) {
-      a.arg_gb[buf] = gb;
-      a.arg_lb[buf] = lb;
-      a.arg_spec[buf] = w.spec;
+      a.arg_gb()[buf] = gb;
+      a.arg_lb()[buf] = lb;
+      a.arg_spec()[buf] = w.spec;
     } else {
-      a.em_gb[buf - g.A] = gb;
-      a.em_blb[buf - g.A] = lb;
-      a.em_spec[buf - g.A] = w.spec;
+      a.em_gb()[buf - g.A] = gb;
+      a.em_blb()[buf - g.A] = lb;
+      a.em_spec()[buf - g.A] = w.spec;
     }
   }
   // opens an SPMD op; operands appended with add_operand
@@ -924,18 +934,18 @@ struct Cand {
       return -1;
     }
     int32_t j = nem++;
-    a.em_head[j] = kind | ((axis + 1) << 8) | ((dim + 1) << 12) | (nopnd << 16);
-    a.em_ooff[j] = neo;
-    a.em_last[j] = j;
-    a.em_op0[j] = -1;
+    a.em_head()[j] = kind | ((axis + 1) << 8) | ((dim + 1) << 12) | (nopnd << 16);
+    a.em_ooff()[j] = neo;
+    a.em_last()[j] = j;
+    a.em_op0()[j] = -1;
     return j;
   }
   PE_HD void add_operand(int32_t j, int32_t buf) {
-    if (tracing) a.em_opnd[neo] = buf;
-    if (a.em_op0[j] < 0) a.em_op0[j] = buf;
+    if (tracing) a.em_opnd()[neo] = buf;
+    if (a.em_op0()[j] < 0) a.em_op0()[j] = buf;
     ++neo;
     // ops are emitted in order, so the current op is always the latest use
-    if (buf >= g.A) a.em_last[buf - g.A] = j;
+    if (buf >= g.A) a.em_last()[buf - g.A] = j;
   }
   PE_HD int32_t pending_front(uint32_t spec) const {
     uint32_t pm = spec_pending(spec);
@@ -953,7 +963,7 @@ struct Cand {
     add_operand(j, w.buf);
     w.spec = spec_set_axis(w.spec, d, 0);
     w.acq &= ~(1u << d);
-    a.em_lb[j] = 4 * local_elems(w);
+    a.em_lb()[j] = 4 * local_elems(w);
     w.buf = g.A + j;
     register_type(w.buf, w);
   }
@@ -963,7 +973,7 @@ struct Cand {
     if (j < 0) return;
     add_operand(j, w.buf);
     w.spec &= ~(1u << (16 + ax));
-    a.em_lb[j] = 4 * local_elems(w);
+    a.em_lb()[j] = 4 * local_elems(w);
     w.buf = g.A + j;
     register_type(w.buf, w);
   }
@@ -994,30 +1004,30 @@ struct Cand {
   // concatenate has <= 2 operands).
   PE_HD void lower_base(int32_t v, int32_t o, int32_t l) {
     int32_t base = g.oopnd_off[o], n = g.oopnd_off[o + 1] - base;
-    int32_t lax = l >= 0 ? (int32_t)a.laxis[l] : -1;
+    int32_t lax = l >= 0 ? (int32_t)a.laxis()[l] : -1;
     uint8_t kind = g.okind[o];
     Low in0, in1;
     for (int32_t k = 0; k < n; ++k) {
-      Low w = materialize(a.opnd[base + k], lax);
+      Low w = materialize(a.opnd()[base + k], lax);
       if (bad()) return;
       if (k == 0) in0 = w;
       else if (k == 1) in1 = w;
     }
     // a repeated operand (mul(x, x)) sees the record its first use stored
-    if (n > 1 && a.opnd[base] == a.opnd[base + 1]) in0 = in1;
+    if (n > 1 && a.opnd()[base] == a.opnd()[base + 1]) in0 = in1;
     Low r;
     int32_t xv = g.A + o;
     int rank = g.vrank[xv];
     for (int d = 0; d < kMaxRank; ++d) r.g[d] = g.shape(xv)[d];
     if (l >= 0) {
-      int32_t dd = (a.vaux[v] & 7) - 1;
+      int32_t dd = (a.vaux()[v] & 7) - 1;
       if (dd >= 0) r.g[dd] = (int32_t)(r.g[dd] / asz(lax));
     }
     r.spec = (uint32_t)rank << 24;
     r.acq = 0;
     r.buf = -1;
     for (int32_t k = 0; k < n; ++k) {
-      Low w = k == 0 ? in0 : k == 1 ? in1 : load(a.opnd[base + k]);
+      Low w = k == 0 ? in0 : k == 1 ? in1 : load(a.opnd()[base + k]);
       r.spec |= spec_pending(w.spec) << 16;
       if (kind == kConstant) continue;
       int wr = rank_of_spec(w.spec);
@@ -1074,9 +1084,9 @@ struct Cand {
     int32_t j = new_op(kind, -1, -1, n);
     if (j < 0) return;
     for (int32_t k = 0; k < n; ++k)
-      add_operand(j, k == 0 ? in0.buf : k == 1 ? in1.buf : a.lo_buf[a.opnd[base + k]]);
+      add_operand(j, k == 0 ? in0.buf : k == 1 ? in1.buf : a.lo_buf()[a.opnd()[base + k]]);
     int64_t out_elems = local_elems(r);
-    a.em_lb[j] = 4 * out_elems;
+    a.em_lb()[j] = 4 * out_elems;
     // flops on LOCAL operand shapes
     switch (kind) {
       case kDot: {
@@ -1104,9 +1114,9 @@ struct Cand {
 
   // lower_slice_axis (REF spmd.cc:206-254)
   PE_HD void lower_slice(int32_t s, int32_t l) {
-    int32_t lax = a.laxis[l];
-    int32_t u = a.vref[s];
-    int d = a.vaux[s] & 7;
+    int32_t lax = a.laxis()[l];
+    int32_t u = a.vref()[s];
+    int d = a.vaux()[s] & 7;
     Low src = load(u);
     if ((int32_t)spec_axis(src.spec, d) == lax + 1) {
       Low r = src;
@@ -1135,7 +1145,7 @@ struct Cand {
     Low r = src;
     r.spec = spec_set_axis(r.spec, d, (uint32_t)(lax + 1));
     r.acq |= 1u << d;
-    a.em_lb[j] = 4 * local_elems(r);
+    a.em_lb()[j] = 4 * local_elems(r);
     r.buf = g.A + j;
     register_type(r.buf, r);
     store(s, r);
@@ -1151,22 +1161,22 @@ struct Cand {
 
   // lower_loop (REF spmd.cc:157-204)
   PE_HD void lower_loop(int32_t v) {
-    int32_t l = a.vref[v];
-    int32_t lax = a.laxis[l];
-    for (int32_t s = a.lhead[l]; s >= 0; s = a.bnext[s]) {
-      if (a.vk[s] == VK_SLICE) lower_slice(s, l);
-      else lower_base(s, a.vref[s], l);
+    int32_t l = a.vref()[v];
+    int32_t lax = a.laxis()[l];
+    for (int32_t s = a.lhead()[l]; s >= 0; s = a.bnext()[s]) {
+      if (a.vk()[s] == VK_SLICE) lower_slice(s, l);
+      else lower_base(s, a.vref()[s], l);
       if (bad()) return;
     }
-    Low yv = load(a.lyield[l]);
-    int32_t lt = a.ltype[l];
-    if (a.lkind[l] == LK_TILE) {
+    Low yv = load(a.lyield()[l]);
+    int32_t lt = a.ltype()[l];
+    if (a.lkind()[l] == LK_TILE) {
       if (spec_pending(yv.spec)) {
         fail(PE_CAND_INTERNAL);
         return;
       }
       Low r = yv;
-      int dim = a.ldim[l];
+      int dim = a.ldim()[l];
       uint32_t have = spec_axis(r.spec, dim);
       if ((int32_t)have == lax + 1) {
         r.acq &= ~(1u << dim);
@@ -1216,22 +1226,22 @@ struct Cand {
       w.spec = (uint32_t)rank << 24;
       w.acq = 0;
       w.buf = x;
-      int32_t direct = a.uses[x] - a.slcnt[x] - (result_ref == x ? 1 : 0);
-      if (direct == 0 && a.aslice[x] >= 0) {
-        int d = a.aslice[x] & 7, ax = a.aslice[x] >> 3;
+      int32_t direct = a.uses()[x] - a.slcnt()[x] - (result_ref == x ? 1 : 0);
+      if (direct == 0 && a.aslice()[x] >= 0) {
+        int d = a.aslice()[x] & 7, ax = a.aslice()[x] >> 3;
         if (w.g[d] % asz(ax) == 0) w.spec = spec_set_axis(w.spec, d, (uint32_t)(ax + 1));
       }
       store(x, w);
       register_type(x, w);
-      a.aspec0[x] = w.spec;
-      a.alb0[x] = 4 * local_elems(w);
+      a.aspec0()[x] = w.spec;
+      a.alb0()[x] = 4 * local_elems(w);
     }
     for_top([&](int32_t v) {
-      uint8_t k = a.vk[v];
+      uint8_t k = a.vk()[v];
       if (k == VK_TOP) {
-        lower_base(v, a.vref[v], -1);
+        lower_base(v, a.vref()[v], -1);
       } else if (k == VK_ATOMIC) {
-        Low w = load(a.vref[v]);
+        Low w = load(a.vref()[v]);
         int r = rank_of_spec(w.spec);
         bool rep = spec_pending(w.spec) == 0;
         for (int d = 0; d < r; ++d) rep = rep && spec_axis(w.spec, d) == 0;
@@ -1266,32 +1276,32 @@ struct Cand {
     }
     // collective_stats (REF spmd.cc:405-434) over final registered types
     for (int32_t j = 0; j < nem; ++j) {
-      int32_t h = a.em_head[j];
+      int32_t h = a.em_head()[j];
       int32_t kind = h & 0xFF, ax = ((h >> 8) & 0xF) - 1;
       if (kind == kAllReduce) {
-        int32_t b = a.em_op0[j];
+        int32_t b = a.em_op0()[j];
         r.ar_cnt[ax]++;
-        r.ar_bytes[ax] += b < g.A ? a.arg_gb[b] : a.em_gb[b - g.A];
+        r.ar_bytes[ax] += b < g.A ? a.arg_gb()[b] : a.em_gb()[b - g.A];
       } else if (kind == kAllGather) {
-        int32_t b = a.em_op0[j];
+        int32_t b = a.em_op0()[j];
         r.ag_cnt[ax]++;
-        r.ag_bytes[ax] += (b < g.A ? a.arg_lb[b] : a.em_blb[b - g.A]) * (asz(ax) - 1);
+        r.ag_bytes[ax] += (b < g.A ? a.arg_lb()[b] : a.em_blb()[b - g.A]) * (asz(ax) - 1);
       } else if (kind == kSliceByCoord) {
         r.sbc_cnt[ax]++;
       }
     }
     // peak liveness
     int64_t base = 0;
-    for (int32_t x = 0; x < g.A; ++x) base += a.alb0[x];
-    if (result_buf >= g.A) a.em_last[result_buf - g.A] = nem - 1;
-    for (int32_t j = 0; j <= nem; ++j) a.delta[j] = 0;
+    for (int32_t x = 0; x < g.A; ++x) base += a.alb0()[x];
+    if (result_buf >= g.A) a.em_last()[result_buf - g.A] = nem - 1;
+    for (int32_t j = 0; j <= nem; ++j) a.delta()[j] = 0;
     for (int32_t j = 0; j < nem; ++j) {
-      a.delta[j] += a.em_lb[j];
-      a.delta[a.em_last[j] + 1] -= a.em_lb[j];
+      a.delta()[j] += a.em_lb()[j];
+      a.delta()[a.em_last()[j] + 1] -= a.em_lb()[j];
     }
     int64_t run = 0, best = 0;
     for (int32_t j = 0; j < nem; ++j) {
-      run += a.delta[j];
+      run += a.delta()[j];
       if (run > best) best = run;
     }
     r.peak_bytes = base + best;
@@ -1333,22 +1343,22 @@ struct Cand {
       ++n;
     };
     put(g.A);
-    for (int32_t x = 0; x < g.A; ++x) put(a.aspec0[x]);
-    put(result_buf < g.A ? a.arg_spec[result_buf] : a.em_spec[result_buf - g.A]);
+    for (int32_t x = 0; x < g.A; ++x) put(a.aspec0()[x]);
+    put(result_buf < g.A ? a.arg_spec()[result_buf] : a.em_spec()[result_buf - g.A]);
     put(nstk);
     for (int32_t i = 0; i < nstk; ++i) {
-      put(a.stk[2 * i]);
-      put(a.stk[2 * i + 1]);
+      put(a.stk()[2 * i]);
+      put(a.stk()[2 * i + 1]);
     }
     put(nem);
     for (int32_t j = 0; j < nem; ++j) {
-      int32_t h = a.em_head[j];
+      int32_t h = a.em_head()[j];
       put(h);
-      put(a.em_lb[j] & 0xffffffff);
-      put(a.em_lb[j] >> 32);
-      put(a.em_spec[j]);
+      put(a.em_lb()[j] & 0xffffffff);
+      put(a.em_lb()[j] >> 32);
+      put(a.em_spec()[j]);
       int32_t no = (h >> 16) & 0xFFFF;
-      for (int32_t q = 0; q < no; ++q) put(a.em_opnd[a.em_ooff[j] + q]);
+      for (int32_t q = 0; q < no; ++q) put(a.em_opnd()[a.em_ooff()[j] + q]);
     }
     if (cap > 0) t[0] = over ? -(int32_t)n : (int32_t)n;
   }
@@ -1424,8 +1434,8 @@ struct Cand {
     for (int32_t o = 0; o < g.n_ord; ++o) {
       for (int32_t i = g.ord_off[o]; i < g.ord_off[o + 1]; ++i) {
         int32_t m = g.ord_mem[i];
-        if (!((a.carry[m >> 5] >> (m & 31)) & 1u)) {
-          a.lg[n++] = o;
+        if (!((a.carry()[m >> 5] >> (m & 31)) & 1u)) {
+          a.lg()[n++] = o;
           break;
         }
       }
@@ -1487,7 +1497,7 @@ struct Cand {
     if (!bad() && status == PE_CAND_OK) {
       if (legal_out) {
         int32_t nl = build_legal();
-        for (int32_t i = 0; i < nl; ++i) legal_out[a.lg[i] >> 6] |= 1ull << (a.lg[i] & 63);
+        for (int32_t i = 0; i < nl; ++i) legal_out[a.lg()[i] >> 6] |= 1ull << (a.lg()[i] & 63);
       }
       uint64_t st = seed;
       while (!terminal) {
@@ -1498,7 +1508,7 @@ struct Cand {
         uint64_t ws = steps >= 1 ? 2 : 1;
         uint64_t pick = splitmix(st) % ((uint64_t)nl + ws);
         if (pick >= (uint64_t)nl) break;
-        pe_action x = ordinal_action(a.lg[pick]);
+        pe_action x = ordinal_action(a.lg()[pick]);
         tick(5);
         bool ok = apply_action(x);
         if (bad()) break;

@@ -90,12 +90,13 @@ __device__ unsigned long long g_phase_cycles[9];
 // whose tight arena overflowed (status PE_CAND_CAPACITY).
 template <bool RETRY>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
-pe_eval_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
+pe_eval_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
+               uint8_t* arena, uint32_t slots,
                const pe_action* acts, const uint32_t* off, uint32_t n, pe_cost_params cp,
                int64_t baseline, pe_result* out, int32_t* trace, uint32_t trace_words) {
   uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
-  pe::Cand c(g, L, arena + (uint64_t)slot * L.bytes);
+  pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
   for (uint32_t i = slot; i < n; i += slots) {
     if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
@@ -107,14 +108,15 @@ pe_eval_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
 
 template <bool RETRY>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
-pe_rollout_kernel(pe::GraphView g, pe::Layout L, uint8_t* arena, uint32_t slots,
+pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
+                  uint8_t* arena, uint32_t slots,
                   const pe_action* prefix, const uint32_t* poff, const uint64_t* seeds,
                   uint32_t n, int32_t maxd, pe_cost_params cp, int64_t baseline,
                   pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
                   int32_t legal_words) {
   uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
-  pe::Cand c(g, L, arena + (uint64_t)slot * L.bytes);
+  pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
   for (uint32_t i = slot; i < n; i += slots) {
     if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
@@ -342,17 +344,21 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   size_t budget = std::min<size_t>(free_b / 2, (size_t)48 << 30);
-  // one resident thread per slot: kMinBlocks blocks of kBlock threads per SM
+  // one resident thread per slot: kMinBlocks blocks of kBlock threads per SM;
+  // arenas come in groups of kLanes interleaved candidates (one per warp)
+  const uint64_t lanes = pe::kLanes;
   uint64_t want = (uint64_t)e->sm_count * kBlock * kMinBlocks;
-  e->big_slots = (uint32_t)std::min<uint64_t>(
-      (uint64_t)e->sm_count * 8,
+  uint64_t big_groups = std::min<uint64_t>(
+      (uint64_t)e->sm_count * 8 / lanes,
       std::max<uint64_t>(1, (budget / 8) / std::max<uint64_t>(e->big_layout.bytes, 1)));
-  uint64_t fit = (budget - (uint64_t)e->big_slots * e->big_layout.bytes) /
-                 std::max<uint64_t>(e->layout.bytes, 1);
-  e->slots = (uint32_t)std::max<uint64_t>(1, std::min(want, fit));
-  if (!cuda_ok(cudaMalloc(&e->d_arena, (size_t)e->slots * e->layout.bytes), err,
+  e->big_slots = (uint32_t)(big_groups * lanes);
+  uint64_t fit_groups = (budget - big_groups * e->big_layout.bytes) /
+                        std::max<uint64_t>(e->layout.bytes, 1);
+  uint64_t groups = std::max<uint64_t>(1, std::min(want / lanes, fit_groups));
+  e->slots = (uint32_t)(groups * lanes);
+  if (!cuda_ok(cudaMalloc(&e->d_arena, (size_t)groups * e->layout.bytes), err,
                "cudaMalloc(arena)") ||
-      !cuda_ok(cudaMalloc(&e->d_big_arena, (size_t)e->big_slots * e->big_layout.bytes), err,
+      !cuda_ok(cudaMalloc(&e->d_big_arena, (size_t)big_groups * e->big_layout.bytes), err,
                "cudaMalloc(big arena)")) {
     pe_engine_destroy(e);
     return PE_ERR_CUDA;
@@ -391,7 +397,9 @@ void pe_engine_destroy(pe_engine* e) {
 uint32_t pe_engine_num_ordinals(const pe_engine* e) { return e->n_ordinals; }
 uint32_t pe_engine_legal_words(const pe_engine* e) { return (e->n_ordinals + 63) / 64; }
 int64_t pe_engine_baseline_bytes(const pe_engine* e) { return e->baseline; }
-int64_t pe_engine_arena_bytes(const pe_engine* e) { return (int64_t)e->layout.bytes; }
+int64_t pe_engine_arena_bytes(const pe_engine* e) {
+  return (int64_t)(e->layout.bytes / pe::kLanes);  // per candidate
+}
 uint32_t pe_engine_slots(const pe_engine* e) { return e->slots; }
 uint64_t pe_engine_launch_count(const pe_engine* e) { return e->launches; }
 int64_t pe_engine_graph_bytes(const pe_engine* e) { return e->graph_bytes; }
