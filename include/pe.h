@@ -60,8 +60,17 @@ typedef struct pe_action {
   uint8_t dim;
   uint8_t axis;   /* mesh axis index in declaration order */
   uint8_t kind;   /* PE_ACT_* */
-  uint8_t pad;
+  uint8_t pad;    /* PE_ACT_FLAG_* */
 } pe_action;
+
+/* A TILE action produced by expanding an INFER_REST decision: applied and
+ * propagated like any tile action, but not counted as a decision (the
+ * INFER_REST marker before it is). */
+#define PE_ACT_FLAG_INFERRED 1u
+/* An INFER_REST marker whose inferred tile actions follow it (output of
+ * pe_infer_rest).  Unexpanded INFER_REST actions are expanded by the host
+ * entry points; the kernels only accept expanded markers. */
+#define PE_ACT_FLAG_EXPANDED 2u
 
 /* ---- per-candidate result record ---- */
 enum {
@@ -195,6 +204,24 @@ pe_status pe_eval_batch(pe_engine* e, const pe_action* acts,
                         const uint32_t* seq_off, uint32_t n_cand,
                         pe_result* out, int32_t* trace, uint32_t trace_words,
                         uint32_t flags, void* stream, pe_error* err);
+
+/* pe_eval_batch plus per-candidate argument flags (n_cand x A bytes, may be
+ * NULL): bit 0 = the argument is sliced (tiled), bit 1 = atomic-wrapped.
+ * INFER_REST actions must already be expanded. */
+pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts,
+                           const uint32_t* seq_off, uint32_t n_cand,
+                           pe_result* out, int32_t* trace, uint32_t trace_words,
+                           uint8_t* argflags, uint32_t flags, void* stream,
+                           pe_error* err);
+
+/* infer_rest (REF propagate.cc:484-544, the InferRest action SPEC:522,531)
+ * applied to the state reached by `prefix` (host buffers): writes
+ * prefix + [INFER_REST marker] + the inferred TILE actions
+ * (PE_ACT_FLAG_INFERRED) to `out`.  Each inference round evaluates all
+ * (argument x dim x auto axis) trials as one GPU batch. */
+pe_status pe_infer_rest(pe_engine* e, const pe_action* prefix, uint32_t n_prefix,
+                        pe_action* out, uint32_t cap, uint32_t* n_out,
+                        pe_error* err);
 
 /* Leaf-parallel MCTS rollouts (SPEC mcts_search: "uniform-random rollout to
  * terminal"): candidate c first applies its prefix, records the legal

@@ -319,6 +319,17 @@ bool member_legal(const Setup& s, const Program& p, int arg, int dim, int axis) 
 // propagate (internal / validation failures).
 bool apply_action(const Setup& s, Program& p, std::vector<StuckNode>& stuck,
                   const pe_action& act) {
+  if (act.kind == PE_ACT_INFER_REST) {
+    // the reference's own infer_rest (REF propagate.cc:484-544) over the
+    // auto axes; the stuck list is that of the resulting fixpoint
+    std::vector<std::string> axes;
+    for (int ax : s.auto_axes) axes.push_back(s.root.mesh.axes[ax].name);
+    p = infer_rest(p, axes);
+    PropagateResult pr = propagate(p);
+    p = std::move(pr.program);
+    stuck = std::move(pr.stuck);
+    return true;
+  }
   const std::string& axis = s.root.mesh.axes.at(act.axis).name;
   if (act.kind == PE_ACT_TILE) {
     if (act.value >= s.names.size()) return false;
@@ -356,6 +367,9 @@ void eval_one(const Setup& s, const pe_action* acts, uint32_t n, pe_result& r,
   try {
     for (uint32_t k = 0; k < n; ++k) {
       if (acts[k].kind == PE_ACT_STOP) break;
+      // tiles the engine inferred while expanding an INFER_REST decision are
+      // re-derived here by the reference's infer_rest itself
+      if (acts[k].pad & PE_ACT_FLAG_INFERRED) continue;
       if (!apply_action(s, p, stuck, acts[k])) {
         r.status = PE_CAND_ILLEGAL;
         r.fail_step = (int32_t)k;

@@ -36,6 +36,9 @@ PE_CAND_CAPACITY = 3
 PE_MEM_DEVICE = 1
 PE_SYNC = 2
 
+PE_ACT_FLAG_INFERRED = 1
+PE_ACT_FLAG_EXPANDED = 2
+
 TRACE_KIND_ALL_REDUCE = 22
 TRACE_KIND_ALL_GATHER = 23
 TRACE_KIND_SLICE_BY_COORD = 24
@@ -140,6 +143,10 @@ SIGNATURES = {
                                 C.POINTER(PeError)]),
     "pe_rollout_batch": (C.c_int, [_P, _P, _P, _P, C.c_uint32, _P, _P, _P, _P, C.c_uint32, _P,
                                    C.POINTER(PeError)]),
+    "pe_eval_batch_ex": (C.c_int, [_P, _P, _P, C.c_uint32, _P, _P, C.c_uint32, _P, C.c_uint32,
+                                   _P, C.POINTER(PeError)]),
+    "pe_infer_rest": (C.c_int, [_P, _P, C.c_uint32, _P, C.c_uint32, C.POINTER(C.c_uint32),
+                                C.POINTER(PeError)]),
     "pe_engine_num_ordinals": (C.c_uint32, [_P]),
     "pe_engine_legal_words": (C.c_uint32, [_P]),
     "pe_engine_ordinal_action": (C.c_int, [_P, C.c_uint32, C.POINTER(PeAction)]),

@@ -1398,8 +1398,11 @@ struct Cand {
     tick(8);
   }
 
+  // argflags (optional, A bytes): bit 0 = argument sliced, bit 1 = atomic
+  // (infer_rest's arg_is_tiled / arg_is_atomic, REF propagate.cc:490-503)
   PE_HD void eval(const pe_action* acts, int32_t n, const pe_cost_params& cp,
-                  int64_t baseline, pe_result& r, int32_t* trace, uint32_t trace_words) {
+                  int64_t baseline, pe_result& r, int32_t* trace, uint32_t trace_words,
+                  uint8_t* argflags = nullptr) {
     tracing = trace != nullptr && trace_words > 0;
     tick_start();
     init();
@@ -1410,6 +1413,19 @@ struct Cand {
     bool propagated = false;
     for (int32_t k = 0; k < n; ++k) {
       if (acts[k].kind == PE_ACT_STOP) break;
+      if (acts[k].kind == PE_ACT_INFER_REST) {
+        // InferRest decision marker; the host expanded it into the inferred
+        // tile actions that follow (pe_engine.cu infer_rest_expand), which
+        // do not count as steps
+        if (!(acts[k].pad & PE_ACT_FLAG_EXPANDED)) {
+          status = PE_CAND_ILLEGAL;  // unexpanded: not executable on the device
+          r.fail_step = k;
+          break;
+        }
+        propagated = true;
+        ++steps;
+        continue;
+      }
       bool ok = apply_action(acts[k]);
       if (bad()) break;
       if (!ok) {
@@ -1420,9 +1436,12 @@ struct Cand {
       propagate();
       propagated = true;
       if (bad()) break;
-      ++steps;
+      if (!(acts[k].pad & PE_ACT_FLAG_INFERRED)) ++steps;
     }
     finish(cp, baseline, steps, propagated, r, trace, trace_words);
+    if (argflags)
+      for (int32_t x = 0; x < g.A; ++x)
+        argflags[x] = (uint8_t)((a.slcnt()[x] > 0 ? 1 : 0) | (a.awrapped()[x] ? 2 : 0));
   }
 
   // ------------------------------------------------------------ rollouts
@@ -1479,6 +1498,19 @@ struct Cand {
         terminal = true;
         break;
       }
+      if (prefix[k].kind == PE_ACT_INFER_REST) {  // expanded by the host
+        if (!(prefix[k].pad & PE_ACT_FLAG_EXPANDED)) {
+          status = PE_CAND_ILLEGAL;
+          r.fail_step = k;
+          terminal = true;
+          break;
+        }
+        propagated = true;
+        if (nacts < maxd) acts_out[nacts] = prefix[k];
+        ++nacts;
+        ++steps;
+        continue;
+      }
       bool ok = apply_action(prefix[k]);
       if (bad()) break;
       if (!ok) {
@@ -1492,7 +1524,7 @@ struct Cand {
       if (bad()) break;
       if (nacts < maxd) acts_out[nacts] = prefix[k];
       ++nacts;
-      ++steps;
+      if (!(prefix[k].pad & PE_ACT_FLAG_INFERRED)) ++steps;
     }
     if (!bad() && status == PE_CAND_OK) {
       if (legal_out) {

@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
 pe_eval_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
                uint8_t* arena, uint32_t slots,
                const pe_action* acts, const uint32_t* off, uint32_t n, pe_cost_params cp,
-               int64_t baseline, pe_result* out, int32_t* trace, uint32_t trace_words) {
+               int64_t baseline, pe_result* out, int32_t* trace, uint32_t trace_words,
+               uint8_t* argflags) {
   uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
@@ -101,7 +102,8 @@ pe_eval_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ 
     if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
     c.eval(acts + off[i], (int32_t)(off[i + 1] - off[i]), cp, baseline, r,
-           trace ? trace + (uint64_t)i * trace_words : nullptr, trace_words);
+           trace ? trace + (uint64_t)i * trace_words : nullptr, trace_words,
+           argflags ? argflags + (uint64_t)i * g.A : nullptr);
     out[i] = r;
   }
 }
@@ -417,6 +419,99 @@ pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* 
   return PE_OK;
 }
 
+// Host-orchestrated infer_rest (REF propagate.cc:484-544): every round
+// evaluates, in ONE batch on the GPU, the sequence so far extended by each
+// (untiled, non-atomic argument) x dim x auto axis trial, and accepts the
+// first argument (argument order) with exactly one trial that adds no
+// all_gather bytes; rounds repeat until no argument is uniquely determined.
+// The result is `prefix + [INFER_REST(expanded)] + inferred TILE actions`,
+// whose evaluation equals the reference's infer_rest on the same state.
+static pe_status infer_rest_expand(pe_engine* e, std::vector<pe_action>& cur, pe_error* err) {
+  const pe::HostGraph& g = e->graph->g;
+  const int32_t A = (int32_t)g.args.size();
+  pe_action marker{0, 0, 0, PE_ACT_INFER_REST, PE_ACT_FLAG_EXPANDED};
+  cur.push_back(marker);
+  std::vector<pe_result> res(1);
+  std::vector<uint8_t> flags(A);
+  auto eval = [&](const std::vector<pe_action>& acts, const std::vector<uint32_t>& off,
+                  uint32_t n, pe_result* out, uint8_t* fl) {
+    return pe_eval_batch_ex(e, acts.data(), off.data(), n, out, nullptr, 0, fl, 0, nullptr, err);
+  };
+  std::vector<uint32_t> off1{0, (uint32_t)cur.size()};
+  pe_status st = eval(cur, off1, 1, res.data(), flags.data());
+  if (st != PE_OK) return st;
+  if (res[0].status != PE_CAND_OK) return PE_OK;  // the candidate reports its own status
+  bool any_tiled = false;
+  for (int32_t a = 0; a < A; ++a) any_tiled |= (flags[a] & 1) != 0;
+  if (!any_tiled) return PE_OK;
+  for (;;) {
+    int64_t baseline = 0;
+    for (int x = 0; x < PE_MAX_AXES; ++x) baseline += res[0].ag_bytes[x];
+    std::vector<pe_action> trial_acts;
+    std::vector<uint32_t> toff{0};
+    std::vector<std::pair<int32_t, pe_action>> trials;  // (arg, action)
+    for (int32_t a = 0; a < A; ++a) {
+      if (flags[a] & 3) continue;  // arg_is_tiled / arg_is_atomic
+      const auto& s = g.args[a].shape;
+      for (int32_t d = 0; d < (int32_t)s.size(); ++d)
+        for (int32_t ax : e->wl.auto_axes) {
+          if (s[d] % g.axis_sizes[ax] != 0) continue;
+          pe_action t{(uint32_t)a, (uint8_t)d, (uint8_t)ax, PE_ACT_TILE, PE_ACT_FLAG_INFERRED};
+          trials.push_back({a, t});
+          trial_acts.insert(trial_acts.end(), cur.begin(), cur.end());
+          trial_acts.push_back(t);
+          toff.push_back((uint32_t)trial_acts.size());
+        }
+    }
+    if (trials.empty()) return PE_OK;
+    std::vector<pe_result> tr(trials.size());
+    st = eval(trial_acts, toff, (uint32_t)trials.size(), tr.data(), nullptr);
+    if (st != PE_OK) return st;
+    int32_t chosen = -1;
+    for (size_t i = 0; i < trials.size();) {
+      int32_t a = trials[i].first;
+      size_t j = i, hit = 0, n_consistent = 0;
+      for (; j < trials.size() && trials[j].first == a; ++j) {
+        int64_t ag = 0;
+        for (int x = 0; x < PE_MAX_AXES; ++x) ag += tr[j].ag_bytes[x];
+        if (tr[j].status == PE_CAND_OK && ag <= baseline) {
+          if (n_consistent == 0) hit = j;
+          ++n_consistent;
+        }
+      }
+      if (n_consistent == 1) {
+        chosen = (int32_t)hit;
+        break;
+      }
+      i = j;
+    }
+    if (chosen < 0) return PE_OK;
+    cur.push_back(trials[chosen].second);
+    off1[1] = (uint32_t)cur.size();
+    st = eval(cur, off1, 1, res.data(), flags.data());
+    if (st != PE_OK) return st;
+    if (res[0].status != PE_CAND_OK) return PE_OK;
+  }
+}
+
+pe_status pe_infer_rest(pe_engine* e, const pe_action* prefix, uint32_t n_prefix, pe_action* out,
+                        uint32_t cap, uint32_t* n_out, pe_error* err) {
+  if (!e || (!prefix && n_prefix) || !out || !n_out) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<pe_action> cur(prefix, prefix + n_prefix);
+  pe_status st = infer_rest_expand(e, cur, err);
+  if (st != PE_OK) return st;
+  *n_out = (uint32_t)cur.size();
+  if (cur.size() > cap) {
+    set_err(err, PE_ERR_CAPACITY, "output buffer too small");
+    return PE_ERR_CAPACITY;
+  }
+  std::copy(cur.begin(), cur.end(), out);
+  return PE_OK;
+}
+
 pe_status pe_eval_batch(pe_engine* e, const pe_action* acts, const uint32_t* seq_off,
                         uint32_t n, pe_result* out, int32_t* trace, uint32_t trace_words,
                         uint32_t flags, void* stream, pe_error* err) {
@@ -424,25 +519,65 @@ pe_status pe_eval_batch(pe_engine* e, const pe_action* acts, const uint32_t* seq
     set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
     return PE_ERR_INVALID_ARGUMENT;
   }
+  if (!(flags & PE_MEM_DEVICE) && n > 0) {
+    // expand unexpanded INFER_REST decisions on the host (nested GPU batches)
+    bool any = false;
+    for (uint32_t k = 0; k < seq_off[n] && !any; ++k)
+      any = acts[k].kind == PE_ACT_INFER_REST && !(acts[k].pad & PE_ACT_FLAG_EXPANDED);
+    if (any) {
+      std::vector<pe_action> flat;
+      std::vector<uint32_t> off{0};
+      for (uint32_t c = 0; c < n; ++c) {
+        std::vector<pe_action> cur;
+        for (uint32_t k = seq_off[c]; k < seq_off[c + 1]; ++k) {
+          if (acts[k].kind == PE_ACT_INFER_REST && !(acts[k].pad & PE_ACT_FLAG_EXPANDED)) {
+            pe_status st = infer_rest_expand(e, cur, err);
+            if (st != PE_OK) return st;
+          } else {
+            cur.push_back(acts[k]);
+          }
+        }
+        flat.insert(flat.end(), cur.begin(), cur.end());
+        off.push_back((uint32_t)flat.size());
+      }
+      return pe_eval_batch_ex(e, flat.data(), off.data(), n, out, trace, trace_words, nullptr,
+                              flags, stream, err);
+    }
+  }
+  return pe_eval_batch_ex(e, acts, seq_off, n, out, trace, trace_words, nullptr, flags, stream,
+                          err);
+}
+
+pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* seq_off,
+                           uint32_t n, pe_result* out, int32_t* trace, uint32_t trace_words,
+                           uint8_t* argflags, uint32_t flags, void* stream, pe_error* err) {
+  if (!e || !seq_off || !out) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
   if (n == 0) return PE_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+  const int32_t A = (int32_t)e->graph->g.args.size();
   const pe_action* d_acts = acts;
   const uint32_t* d_off = seq_off;
   pe_result* d_out = out;
   int32_t* d_trace = trace;
+  uint8_t* d_flags = argflags;
   if (!(flags & PE_MEM_DEVICE)) {
     uint32_t n_acts = seq_off[n];
     size_t b_acts = ((size_t)n_acts * sizeof(pe_action) + 255) & ~size_t(255);
     size_t b_off = ((size_t)(n + 1) * 4 + 255) & ~size_t(255);
     size_t b_out = ((size_t)n * sizeof(pe_result) + 255) & ~size_t(255);
-    size_t b_tr = trace ? (size_t)n * trace_words * 4 : 0;
-    if (!ensure_io(e, b_acts + b_off + b_out + b_tr + 256, err)) return PE_ERR_CUDA;
+    size_t b_tr = trace ? (((size_t)n * trace_words * 4 + 255) & ~size_t(255)) : 0;
+    size_t b_fl = argflags ? (size_t)n * A : 0;
+    if (!ensure_io(e, b_acts + b_off + b_out + b_tr + b_fl + 256, err)) return PE_ERR_CUDA;
     uint8_t* p = e->d_io;
     d_acts = (const pe_action*)p;
     d_off = (const uint32_t*)(p + b_acts);
     d_out = (pe_result*)(p + b_acts + b_off);
     d_trace = trace ? (int32_t*)(p + b_acts + b_off + b_out) : nullptr;
+    d_flags = argflags ? (p + b_acts + b_off + b_out + b_tr) : nullptr;
     if (n_acts && !cuda_ok(cudaMemcpyAsync((void*)d_acts, acts, (size_t)n_acts * sizeof(pe_action),
                                            cudaMemcpyHostToDevice, st), err, "H2D acts"))
       return PE_ERR_CUDA;
@@ -453,16 +588,19 @@ pe_status pe_eval_batch(pe_engine* e, const pe_action* acts, const uint32_t* seq
   uint32_t slots = launch_slots(e, n);
   pe_eval_kernel<false><<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->layout, e->d_arena, slots, d_acts, d_off, n, e->cp, e->baseline, d_out,
-      d_trace, trace_words);
+      d_trace, trace_words, d_flags);
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
   pe_eval_kernel<true><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->big_layout, e->d_big_arena, bs, d_acts, d_off, n, e->cp, e->baseline, d_out,
-      d_trace, trace_words);
+      d_trace, trace_words, d_flags);
   e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "pe_eval_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {
     if (!cuda_ok(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(pe_result),
                                  cudaMemcpyDeviceToHost, st), err, "D2H results"))
+      return PE_ERR_CUDA;
+    if (argflags && !cuda_ok(cudaMemcpyAsync(argflags, d_flags, (size_t)n * A,
+                                             cudaMemcpyDeviceToHost, st), err, "D2H flags"))
       return PE_ERR_CUDA;
     if (trace && !cuda_ok(cudaMemcpyAsync(trace, d_trace, (size_t)n * trace_words * 4,
                                           cudaMemcpyDeviceToHost, st), err, "D2H trace"))

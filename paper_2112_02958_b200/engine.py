@@ -219,6 +219,19 @@ class Engine:
             lgl = [list(lg[i * self.legal_words:(i + 1) * self.legal_words]) for i in range(n)]
         return list(out), seqs, lgl
 
+    def infer_rest(self, prefix):
+        """infer_rest (REF propagate.cc:484-544) after `prefix`: returns
+        prefix + [INFER_REST marker] + inferred TILE actions."""
+        acts, _ = capi.actions_array([prefix])
+        cap = len(prefix) + 1 + self.graph.n_args
+        out = (PeAction * cap)()
+        n = C.c_uint32(0)
+        err = PeError()
+        rc = self.lib.pe_infer_rest(self.h, acts, len(prefix), out, cap, C.byref(n), C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        return [out[i] for i in range(n.value)]
+
     # ---- device-buffer entry points (inputs already resident in HBM) ----
     def rollout_batch_device(self, prefix_ptr, poff_ptr, seeds_ptr, n, acts_out_ptr,
                              nacts_out_ptr, out_ptr, legal_ptr=None, stream=None, sync=False):

@@ -114,3 +114,43 @@ def test_capacity_retry_path(oracle_lib, monkeypatch):
     assert seqs == rseqs
     assert all(r.status == 0 for r in res)
     assert all(not H.compare_results(a, b) for a, b in zip(res, ref))
+
+
+INFER_PROGRAMS = {
+    "mlp2": lambda: modelgen.build_mlp(2, (16, 64, 16), 8, (("model", 2),)),
+    "mlp3": lambda: modelgen.build_mlp(3, (16, 64, 64, 16), 8, (("model", 2),)),
+    "t1": lambda: modelgen.config_program(2),
+    "t2": lambda: modelgen.build_transformer(2, mesh=(("model", 2),), **modelgen.TOY),
+}
+
+
+@pytest.mark.parametrize("cfgno", sorted(INFER_PROGRAMS))
+def test_infer_rest_device_vs_reference(oracle_lib, cfgno):
+    # a6: the engine's batched infer_rest expansion vs the reference's own
+    # infer_rest after every single first decision (t1 / t2 / mlp3 include
+    # prefixes where inference changes the state)
+    text = INFER_PROGRAMS[cfgno]()
+    eng = _engine(text)
+    names, shapes = modelgen.program_values(text)
+    seqs = []
+    for a in range(eng.graph.n_args):
+        for d in range(len(shapes[a])):
+            if shapes[a][d] % eng.graph.axis_sizes[0] == 0:
+                seqs.append([(a, d, 0, 0), (0, 0, 0, 2)])
+    seqs.append([(0, 0, 0, 2)])  # InferRest first: nothing tiled -> no-op
+    res, tr = eng.eval_batch(seqs, trace_words=TW)
+    ref, rtr = H.eval_batch("oracle", text, seqs, trace_words=TW)
+    for a, b, x, y in zip(res, ref, tr, rtr):
+        assert not H.compare_results(a, b)
+        assert x[:x[0]] == y[:y[0]]
+    # the explicit API returns prefix + expanded marker + inferred tiles whose
+    # evaluation equals evaluating the unexpanded InferRest decision
+    for s in seqs[:6]:
+        prefix = [capi.PeAction(*s[0], 0)]
+        exp = eng.infer_rest(prefix)
+        assert exp[0].value == prefix[0].value and exp[1].kind == capi.PE_ACT_INFER_REST
+        assert all(x.kind == capi.PE_ACT_TILE and x.pad == capi.PE_ACT_FLAG_INFERRED
+                   for x in exp[2:])
+        a = eng.eval_batch([exp])[0]
+        b = eng.eval_batch([s])[0]
+        assert not H.compare_results(a, b)

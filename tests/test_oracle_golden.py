@@ -101,3 +101,20 @@ def test_replicated_reward_and_infeasible(oracle_lib):
     assert r.feasible == 0 and r.reward == 0.0
     r = ev(modelgen.linear(), [[]])[0]
     assert 0.99 < r.reward <= 1.0
+
+
+def test_infer_rest_mlp_example(oracle_lib):
+    # SPEC infer_rest example: toy MLP with the first-layer weight tiled
+    # column-wise on "model" -> second-layer weight inferred row-wise
+    text = modelgen.build_mlp(2, (16, 64, 16), 8, (("model", 2),))
+    names = modelgen.program_values(text)[0]
+    w1, w2 = names.index("w1"), names.index("w2")
+    (t,) = H.eval_batch("oracle", text, [[(w1, 1, 0, 0), (0, 0, 0, 2)]], trace_words=1024)[1]
+    specs = t[2:2 + t[1]]
+    assert specs[w1] & 0xFF == 0x10          # w1 dim1 on model (the decision)
+    assert specs[w2] & 0xFF == 0x01          # w2 dim0 on model (inferred)
+    # fully tiled program -> unchanged (SPEC: "fully tiled program -> unchanged")
+    r1, r2 = H.eval_batch("oracle", text, [[(w1, 1, 0, 0), (0, 0, 0, 2)],
+                                           [(w1, 1, 0, 0), (0, 0, 0, 2), (0, 0, 0, 2)]])[0]
+    assert r1.ar_cnt[0] == r2.ar_cnt[0] and r1.peak_bytes == r2.peak_bytes
+    assert r2.n_steps == r1.n_steps + 1
