@@ -181,7 +181,208 @@ def config_program(cfg: int) -> str:
     if cfg == 3:
         return build_transformer(24, mesh=(("batch", 4), ("model", 2)), name="gpt2_medium",
                                  **GPT2_MEDIUM)
+    if cfg == 4:  # 48-layer training step: 13,757 ops, 1,153 arguments
+        return build_training_step(48, mesh=(("batch", 4), ("model", 2)), **GPT2_MEDIUM)
     raise ValueError(cfg)
+
+
+# ---------------------------------------------------------------- training step
+class Tape:
+    """Structured op recorder over ProgramBuilder with reverse-mode gradients
+    for the kinds the transformer uses (SPEC modelgen: "hand-derived gradient
+    ops"; here derived mechanically per op kind)."""
+
+    def __init__(self, b: ProgramBuilder):
+        self.b = b
+        self.rec = []  # (out, kind, ins, meta)
+
+    def shape(self, v):
+        return self.b.shapes[v]
+
+    def _op(self, kind, ins, shape, attrs, meta, name=None):
+        out = self.b.op(kind, ins, shape, attrs, name)
+        self.rec.append((out, kind, list(ins), meta))
+        return out
+
+    def const(self, value, shape):
+        return self.b.const(value, shape)
+
+    def ew(self, kind, *ins):
+        return self._op(kind, ins, self.shape(ins[0]), None, {})
+
+    def dot(self, a, b, lc, rc, lb=(), rb=()):
+        sa, sb = self.shape(a), self.shape(b)
+        used_a = set(lb) | set(lc)
+        used_b = set(rb) | set(rc)
+        shape = [sa[i] for i in lb] + [sa[i] for i in range(len(sa)) if i not in used_a] + \
+                [sb[j] for j in range(len(sb)) if j not in used_b]
+        attrs = {"contract": _pair(list(lc), list(rc)), "batch": _pair(list(lb), list(rb))}
+        return self._op("dot", [a, b], shape, attrs,
+                        {"lc": list(lc), "rc": list(rc), "lb": list(lb), "rb": list(rb)})
+
+    def reduce_sum(self, a, dims):
+        sa = self.shape(a)
+        shape = [sa[i] for i in range(len(sa)) if i not in dims]
+        return self._op("reduce_sum", [a], shape, {"dims": _list(sorted(dims))},
+                        {"dims": sorted(dims)})
+
+    def bcast(self, a, shape, mp):
+        return self._op("broadcast_in_dim", [a], list(shape), {"map": _list(mp)}, {"map": list(mp)})
+
+    def transpose(self, a, perm):
+        sa = self.shape(a)
+        return self._op("transpose", [a], [sa[p] for p in perm], {"perm": _list(perm)},
+                        {"perm": list(perm)})
+
+    def grads(self, loss, wrt):
+        needs = set(wrt)
+        for out, kind, ins, meta in self.rec:
+            if any(i in needs for i in ins):
+                needs.add(out)
+        g = {loss: self.const(1.0, self.shape(loss))}
+
+        def acc(x, gx):
+            if x not in needs:
+                return
+            g[x] = gx if x not in g else self.ew("add", g[x], gx)
+
+        for out, kind, ins, meta in reversed(self.rec):
+            if out not in g:
+                continue
+            go = g[out]
+            if kind == "add":
+                acc(ins[0], go)
+                acc(ins[1], go)
+            elif kind == "sub":
+                acc(ins[0], go)
+                if ins[1] in needs:
+                    acc(ins[1], self.ew("neg", go))
+            elif kind == "mul":
+                if ins[0] in needs:
+                    acc(ins[0], self.ew("mul", go, ins[1]))
+                if ins[1] in needs:
+                    acc(ins[1], self.ew("mul", go, ins[0]))
+            elif kind == "div":
+                if ins[0] in needs:
+                    acc(ins[0], self.ew("div", go, ins[1]))
+                if ins[1] in needs:
+                    acc(ins[1], self.ew("neg", self.ew("div", self.ew("mul", go, out), ins[1])))
+            elif kind == "exp":
+                acc(ins[0], self.ew("mul", go, out))
+            elif kind == "tanh":
+                one = self.const(1.0, self.shape(out))
+                acc(ins[0], self.ew("mul", go, self.ew("sub", one, self.ew("mul", out, out))))
+            elif kind == "rsqrt":
+                c = self.const(-0.5, self.shape(out))
+                cube = self.ew("mul", out, self.ew("mul", out, out))
+                acc(ins[0], self.ew("mul", go, self.ew("mul", c, cube)))
+            elif kind == "neg":
+                acc(ins[0], self.ew("neg", go))
+            elif kind == "reduce_sum":
+                sa = self.shape(ins[0])
+                keep = [i for i in range(len(sa)) if i not in meta["dims"]]
+                acc(ins[0], self.bcast(go, sa, keep))
+            elif kind == "broadcast_in_dim":
+                so = self.shape(out)
+                acc(ins[0], self.reduce_sum(go, [j for j in range(len(so)) if j not in meta["map"]]))
+            elif kind == "transpose":
+                perm = meta["perm"]
+                inv = [perm.index(i) for i in range(len(perm))]
+                acc(ins[0], self.transpose(go, inv))
+            elif kind == "dot":
+                self._dot_grads(out, ins, meta, go, acc, needs)
+            else:
+                raise NotImplementedError(kind)
+        return g
+
+    def _dot_grads(self, out, ins, meta, go, acc, needs):
+        a, b = ins
+        lb, rb, lc, rc = meta["lb"], meta["rb"], meta["lc"], meta["rc"]
+        ra, rbk = len(self.shape(a)), len(self.shape(b))
+        nb = len(lb)
+        a_free = [i for i in range(ra) if i not in lb and i not in lc]
+        b_free = [j for j in range(rbk) if j not in rb and j not in rc]
+        naf = len(a_free)
+        if a in needs:
+            r = self.dot(go, b, [nb + naf + j for j in range(len(b_free))], b_free,
+                         list(range(nb)), rb)
+            dims = lb + a_free + [lc[rc.index(c)] for c in sorted(rc)]
+            perm = [dims.index(i) for i in range(ra)]
+            acc(a, r if perm == list(range(ra)) else self.transpose(r, perm))
+        if b in needs:
+            r = self.dot(a, go, a_free, [nb + i for i in range(naf)], lb, list(range(nb)))
+            dims = rb + [rc[lc.index(c)] for c in sorted(lc)] + b_free
+            perm = [dims.index(j) for j in range(rbk)]
+            acc(b, r if perm == list(range(rbk)) else self.transpose(r, perm))
+
+
+def build_training_step(layers=48, batch=8, seq=1024, d_model=1024, heads=16, d_ff=4096,
+                        mesh=(("batch", 4), ("model", 2)), name="train_step") -> str:
+    """One training step of the head-split transformer (SURVEY.md §8(d)
+    config 4: "hand-derived backward plus optimiser state"): forward as
+    build_transformer with learned layer-norm gains, loss = sum of the
+    output, reverse-mode gradients of every parameter, and an Adam update
+    (first/second moments are arguments with the parameter's scope); the
+    function returns the sum of the updated parameters."""
+    B, S, D, H, F = batch, seq, d_model, heads, d_ff
+    Dh = D // H
+    bld = ProgramBuilder(name, list(mesh))
+    t = Tape(bld)
+    x = bld.arg("x", [B, S, D])
+    params = []
+    for i in range(layers):
+        for w, shp, sc in (("wq", [D, H, Dh], "attention/q_proj"), ("wk", [D, H, Dh], "attention/k_proj"),
+                           ("wv", [D, H, Dh], "attention/v_proj"), ("wo", [H, Dh, D], "attention/o_proj"),
+                           ("w1", [D, F], "mlp/w1"), ("w2", [F, D], "mlp/w2"),
+                           ("g1", [D], "ln1/gain"), ("g2", [D], "ln2/gain")):
+            params.append(bld.arg(f"l{i}_{w}", shp, f"layer_{i}/{sc}"))
+    opt = {}
+    for p in params:
+        sc = [a[2] for a in bld.args if a[0] == p][0]
+        opt[p] = (bld.arg(p + "_m", bld.shapes[p], sc + "/adam_m"),
+                  bld.arg(p + "_v", bld.shapes[p], sc + "/adam_v"))
+
+    def ln(v, gain):
+        s = t.reduce_sum(v, [2])
+        mean = t.ew("mul", s, t.const(1.0 / D, [B, S]))
+        xc = t.ew("sub", v, t.bcast(mean, [B, S, D], [0, 1]))
+        var = t.ew("mul", t.reduce_sum(t.ew("mul", xc, xc), [2]), t.const(1.0 / D, [B, S]))
+        rs = t.ew("rsqrt", t.ew("add", var, t.const(1e-5, [B, S])))
+        y = t.ew("mul", xc, t.bcast(rs, [B, S, D], [0, 1]))
+        return t.ew("mul", y, t.bcast(gain, [B, S, D], [2]))
+
+    h = x
+    for i in range(layers):
+        P = lambda w: f"l{i}_{w}"  # noqa: E731
+        a = ln(h, P("g1"))
+        q = t.dot(a, P("wq"), [2], [0])
+        k = t.dot(a, P("wk"), [2], [0])
+        v = t.dot(a, P("wv"), [2], [0])
+        sc = t.dot(q, k, [3], [3], [0, 2], [0, 2])
+        e = t.ew("exp", sc)
+        z = t.bcast(t.reduce_sum(e, [3]), [B, H, S, S], [0, 1, 2])
+        pr = t.ew("div", e, z)
+        ctx = t.dot(pr, v, [3], [1], [0, 1], [0, 2])
+        att = t.dot(ctx, P("wo"), [1, 3], [0, 1])
+        r1 = t.ew("add", h, att)
+        m = ln(r1, P("g2"))
+        hh = t.ew("tanh", t.dot(m, P("w1"), [2], [0]))
+        h = t.ew("add", r1, t.dot(hh, P("w2"), [2], [0]))
+    loss = t.reduce_sum(h, [0, 1, 2])
+    g = t.grads(loss, params)
+    total = None
+    for p in params:
+        s = bld.shapes[p]
+        m0, v0 = opt[p]
+        gp = g[p]
+        m1 = t.ew("add", t.ew("mul", m0, t.const(0.9, s)), t.ew("mul", gp, t.const(0.1, s)))
+        v1 = t.ew("add", t.ew("mul", v0, t.const(0.999, s)),
+                  t.ew("mul", t.ew("mul", gp, gp), t.const(0.001, s)))
+        upd = t.ew("mul", m1, t.ew("rsqrt", t.ew("add", v1, t.const(1e-8, s))))
+        p1 = t.ew("sub", p, t.ew("mul", upd, t.const(1e-3, s)))
+        red = t.reduce_sum(p1, list(range(len(s))))
+        total = red if total is None else t.ew("add", total, red)
+    return bld.text(total)
 
 
 # ---------------------------------------------------------------- fuzzing

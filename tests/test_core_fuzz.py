@@ -55,3 +55,21 @@ def test_megatron_two_layer_and_reshape_hazard(oracle_lib, harness_lib):
     rh, th = H.eval_batch("harness", text, [seq], trace_words=16384)
     assert not H.compare_results(ro[0], rh[0]) and to == th
     assert sum(rh[0].ar_cnt) == 4 and rh[0].reduction_bytes == 1024
+
+
+def test_training_step_graphs_match_oracle(oracle_lib, harness_lib):
+    # config-4 family (forward + reverse-mode gradients + Adam) at toy size:
+    # rollouts, legal sets and full SPMD traces identical
+    for layers, mesh in ((1, (("m", 2),)), (2, (("batch", 2), ("model", 2)))):
+        text = modelgen.build_training_step(layers, mesh=mesh, **modelgen.TOY)
+        cfg = capi.default_search_config(group_scopes=0)
+        lw = (H.oracle_info(text, cfg)["n_ordinals"] + 63) // 64
+        n = 60
+        ro, so, lo = H.rollout_batch("oracle", text, [[]] * n, list(range(n)), cfg, legal_words=lw,
+                                     threads=8)
+        rh, sh, lh = H.rollout_batch("harness", text, [[]] * n, list(range(n)), cfg, legal_words=lw)
+        assert so == sh and lo == lh
+        assert all(not H.compare_results(a, b) for a, b in zip(ro, rh))
+        e1, t1 = H.eval_batch("oracle", text, so, trace_words=1 << 16, threads=8)
+        e2, t2 = H.eval_batch("harness", text, so, trace_words=1 << 16)
+        assert all(x[:x[0]] == y[:y[0]] for x, y in zip(t1, t2))

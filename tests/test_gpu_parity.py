@@ -154,3 +154,30 @@ def test_infer_rest_device_vs_reference(oracle_lib, cfgno):
         a = eng.eval_batch([exp])[0]
         b = eng.eval_batch([s])[0]
         assert not H.compare_results(a, b)
+
+
+def test_training_step_device_vs_oracle(oracle_lib):
+    text = modelgen.build_training_step(2, mesh=(("batch", 2), ("model", 2)), **modelgen.TOY)
+    cfg = capi.default_search_config(group_scopes=0)
+    eng = _engine(text, cfg)
+    n = 256
+    res, seqs, legal = eng.rollout_batch([[]] * n, list(range(n)), legal=True)
+    ref, rseqs, rlegal = H.rollout_batch("oracle", text, [[]] * n, list(range(n)), cfg,
+                                         legal_words=eng.legal_words, threads=os.cpu_count() or 1)
+    assert seqs == rseqs and legal == rlegal
+    assert all(not H.compare_results(a, b) for a, b in zip(res, ref))
+    ev, tr = eng.eval_batch(seqs[:64], trace_words=1 << 16)
+    _, rtr = H.eval_batch("oracle", text, seqs[:64], trace_words=1 << 16,
+                          threads=os.cpu_count() or 1)
+    assert all(x[:x[0]] == y[:y[0]] for x, y in zip(tr, rtr))
+
+
+def test_config4_training_step_runs():
+    # config 4 at full size (48 layers, 13,757 ops, 1,153 arguments): every
+    # rollout evaluates (tight arena or retry), no failures
+    text = modelgen.config_program(4)
+    eng = _engine(text, capi.default_search_config(group_scopes=1))
+    assert eng.graph.n_ops == 13757 and eng.graph.n_args == 1153
+    res, seqs, _ = eng.rollout_batch([[]] * 256, list(range(256)))
+    assert all(r.status == 0 for r in res)
+    assert all(r.n_spmd_ops >= eng.graph.n_ops for r in res)
