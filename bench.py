@@ -281,7 +281,7 @@ def run_engine(args):
         import helpers as H
         if os.path.exists(H.ORACLE_SO):
             threads = os.cpu_count() or 1
-            n_cpu = 8 * threads
+            n_cpu = 24 * threads  # ~10 s of reference CPU work on this path
             v_cpu, dt = cpu_reference(text, n_cpu, 30_000_000, threads)
             cpu = {"value": v_cpu, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"{n_cpu} rollouts of the bench workload ({dt:.1f} s)"}
@@ -318,7 +318,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=65536)
+    # >= the engine's resident slots (148 SMs x 32 warps x 32 lanes = 151,552)
+    ap.add_argument("--batch", type=int, default=262144)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -69,13 +69,19 @@ bool cuda_ok(cudaError_t e, pe_error* err, const char* what) {
   return false;
 }
 
+#ifndef PE_SOLO
+#define PE_SOLO 0
+#endif
+constexpr uint32_t kThreadsPerSlot = PE_SOLO ? 32 : 1;
 #ifndef PE_MIN_BLOCKS
-#define PE_MIN_BLOCKS 4
+#define PE_MIN_BLOCKS 8
 #endif
 constexpr int kBlock = 128;
-// resident blocks per SM the register allocation must allow: 4 -> 16 warps
-// per SM (<= 128 registers / thread); the per-thread work is a dependent
-// chain of global-memory accesses, so resident warps = latency hiding
+// resident blocks per SM the register allocation must allow: 8 -> 32 warps
+// per SM (<= 64 registers / thread).  The per-thread work is a dependent
+// chain of global-memory accesses, so resident warps = latency hiding:
+// measured 342K vs 277K cand/s for 4 blocks (128 registers) at config 3
+// despite the spills (profiles/r1_summary.md).
 constexpr int kMinBlocks = PE_MIN_BLOCKS;
 
 #ifdef PE_PHASE_TIMERS
@@ -116,7 +122,13 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                   uint32_t n, int32_t maxd, pe_cost_params cp, int64_t baseline,
                   pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
                   int32_t legal_words) {
+#if PE_SOLO
+  // experiment: one active lane per warp (no SIMT divergence across candidates)
+  if (threadIdx.x % 32) return;
+  uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+#else
   uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+#endif
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
   for (uint32_t i = slot; i < n; i += slots) {
@@ -345,11 +357,15 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   }
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  size_t budget = std::min<size_t>(free_b / 2, (size_t)48 << 30);
+  // arena budget: up to 45 % of free HBM (two engines may coexist in one
+  // process), at most 96 GiB; PE_ARENA_BUDGET_GB overrides
+  size_t budget = std::min<size_t>((size_t)(free_b * 0.45), (size_t)96 << 30);
+  if (const char* gb = std::getenv("PE_ARENA_BUDGET_GB"))
+    budget = std::min<size_t>(free_b, (size_t)(std::atof(gb) * (double)(1ull << 30)));
   // one resident thread per slot: kMinBlocks blocks of kBlock threads per SM;
   // arenas come in groups of kLanes interleaved candidates (one per warp)
   const uint64_t lanes = pe::kLanes;
-  uint64_t want = (uint64_t)e->sm_count * kBlock * kMinBlocks;
+  uint64_t want = (uint64_t)e->sm_count * kBlock * kMinBlocks / kThreadsPerSlot;
   uint64_t big_groups = std::min<uint64_t>(
       (uint64_t)e->sm_count * 8 / lanes,
       std::max<uint64_t>(1, (budget / 8) / std::max<uint64_t>(e->big_layout.bytes, 1)));
@@ -669,11 +685,12 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
       return PE_ERR_CUDA;
   }
   uint32_t slots = launch_slots(e, n);
-  pe_rollout_kernel<false><<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+  pe_rollout_kernel<false>
+      <<<(slots * kThreadsPerSlot + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff, d_seeds, n, maxd, e->cp,
       e->baseline, d_acts, d_nacts, d_out, d_legal, lw);
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
-  pe_rollout_kernel<true><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+  pe_rollout_kernel<true><<<(bs * kThreadsPerSlot + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff, d_seeds, n, maxd, e->cp,
       e->baseline, d_acts, d_nacts, d_out, d_legal, lw);
   e->launches += 2;
