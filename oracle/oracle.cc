@@ -34,6 +34,7 @@
 #include "partir/propagate.h"
 #include "partir/rewrite.h"
 #include "partir/spmd.h"
+#include "partir/interp.h"
 #include "pe.h"
 
 using namespace partir;
@@ -644,6 +645,37 @@ int oracle_legal(const char* pir, size_t len, const pe_search_config* cfg, const
   std::vector<uint32_t> l = legal_ordinals(s, p);
   *n_out = (uint32_t)l.size();
   for (uint32_t i = 0; i < l.size() && i < cap; ++i) ords_out[i] = l[i];
+  return 0;
+}
+
+// Semantics check of a plan with the reference interpreter (REF
+// interp.cc:640-678 check_equivalence: eval_spmd of the lowered program vs
+// eval_base of the original on seeded random inputs).  Used to verify plans
+// found by the GPU search.
+int oracle_check_equivalence(const char* pir, size_t len, const pe_search_config* cfg,
+                             const pe_action* acts, uint32_t n, int trials, uint64_t seed,
+                             double* max_abs_diff, int* pass, int* order_preserving, char* err,
+                             size_t errcap) {
+  Setup s;
+  int rc = make_setup(s, pir, len, cfg, nullptr, err, errcap);
+  if (rc) return rc;
+  Program p = s.root;
+  std::vector<StuckNode> stuck;
+  try {
+    for (uint32_t k = 0; k < n; ++k) {
+      if (acts[k].kind == PE_ACT_STOP) break;
+      if (acts[k].pad & PE_ACT_FLAG_INFERRED) continue;
+      if (!apply_action(s, p, stuck, acts[k])) return 3;
+    }
+    SpmdProgram sp = lower_to_spmd(p);
+    EquivalenceReport rep = check_equivalence(s.root, sp, trials, seed);
+    *max_abs_diff = rep.max_abs_diff;
+    *pass = rep.pass ? 1 : 0;
+    *order_preserving = rep.order_preserving ? 1 : 0;
+  } catch (const Error& e) {
+    if (err) std::snprintf(err, errcap, "%s", e.what());
+    return 70;
+  }
   return 0;
 }
 

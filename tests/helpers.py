@@ -66,6 +66,10 @@ def oracle():
         lib.oracle_legal.restype = C.c_int
         lib.oracle_legal.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(PeSearchConfig), _P,
                                      C.c_uint32, _P, C.c_uint32, _P, C.c_char_p, C.c_size_t]
+        lib.oracle_check_equivalence.restype = C.c_int
+        lib.oracle_check_equivalence.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(PeSearchConfig),
+                                                 _P, C.c_uint32, C.c_int, C.c_uint64, _P, _P, _P,
+                                                 C.c_char_p, C.c_size_t]
         lib.oracle_debug_text.restype = C.c_int
         lib.oracle_debug_text.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(PeSearchConfig), _P,
                                           C.c_uint32, C.c_char_p, C.c_size_t]
@@ -169,6 +173,22 @@ def oracle_legal(text: str, seq, cfg=None):
     if rc:
         raise RuntimeError(f"rc={rc} {err.value.decode()}")
     return list(ords[:n.value])
+
+
+def oracle_check_equivalence(text: str, seq, trials=5, seed=0, cfg=None):
+    """Reference interpreter check of the plan `seq` (REF interp.cc:640-678).
+    Returns (pass, max_abs_diff, order_preserving)."""
+    b = text.encode()
+    acts, _ = capi.actions_array([seq])
+    mx = C.c_double(0)
+    ok = C.c_int(0)
+    op = C.c_int(0)
+    err = C.create_string_buffer(512)
+    rc = oracle().oracle_check_equivalence(b, len(b), C.byref(_cfg(cfg)), acts, len(seq), trials,
+                                           seed, C.byref(mx), C.byref(ok), C.byref(op), err, 512)
+    if rc:
+        raise RuntimeError(f"rc={rc} {err.value.decode()}")
+    return bool(ok.value), mx.value, bool(op.value)
 
 
 def oracle_debug(text: str, seq, cfg=None) -> str:

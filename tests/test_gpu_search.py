@@ -70,3 +70,12 @@ def test_gpu_gpt2_medium_24_layer_megatron():
     p = search.mcts_search(eng, episodes=1024, seed=0, leaf_batch=256)
     model = g0.axis_index("model")
     assert p.result.ar_cnt[model] == 48 and p.result.ag_cnt[model] == 0, search.plan_actions(p)
+
+
+def test_gpu_searched_plan_preserves_semantics(oracle_lib):
+    text = modelgen.build_transformer(**TWO_LAYER)
+    g, cfg, cp, ords, lw = setup(text)
+    eng = _engine(text, cfg, cp)
+    p = search.mcts_search(eng, episodes=500, seed=4, leaf_batch=64)
+    ok, diff, _ = H.oracle_check_equivalence(text, search.plan_actions(p), trials=3)
+    assert ok, diff
