@@ -96,7 +96,7 @@ struct Layout {
   // byte offsets inside one group arena (kLanes candidates); record arrays
   // are interleaved [index][lane] at record granularity
   uint64_t vrec, lrec, arec, looprec, emrec;
-  uint64_t opnd, pos, fs, stk, seen, em_opnd, carry, lg;
+  uint64_t opnd, pos, fs, stk, seen, em_opnd, carry, lg, dirty;
   uint64_t bytes;  // one group arena
 };
 
@@ -163,9 +163,16 @@ struct Arena {
   PE_REC(em_opnd, int32_t, b4, em_opnd, 0, kLanes * 4)
   PE_REC(lg, int32_t, b4, lg, 0, kLanes * 4)
   PE_REC(carry, uint32_t, b4, carry, 0, kLanes * 4)
+  PE_REC(dirty, uint32_t, b4, dirty, 0, kLanes * 4)
   PE_REC(seen, uint8_t, b1, seen, 0, kLanes * 1)
 #undef PE_REC
 };
+
+#ifdef __CUDA_ARCH__
+PE_HD int32_t pe_ctz(uint32_t x) { return __ffs((int)x) - 1; }
+#else
+PE_HD int32_t pe_ctz(uint32_t x) { return __builtin_ctz(x); }
+#endif
 
 PE_HD uint64_t align8(uint64_t x) { return (x + 7) & ~uint64_t(7); }
 PE_HD uint64_t align128(uint64_t x) { return (x + 127) & ~uint64_t(127); }
@@ -224,6 +231,7 @@ inline Layout relayout(const GraphView& g, const Caps& caps) {
   L.em_opnd = take(caps.EO, 4);
   L.carry = take(A / 32 + 1, 4);
   L.lg = take(g.n_ord, 4);
+  L.dirty = take(N / 32 + 1, 4);
   L.bytes = align128(o);
   return L;
 }
@@ -275,6 +283,7 @@ struct Cand {
   Arena a;
   int32_t nslots, nloops, nfs, nem, neo, nstk;
   int32_t result_ref;
+  int32_t pend;  // head of the pending-slice list (linked through vpos)
   int32_t status;
   int64_t flops;
   int32_t result_buf;
@@ -395,6 +404,22 @@ struct Cand {
     }
     if (result_ref == v) result_ref = t;
   }
+  // Incremental sweeps.  A top-level op's pull decision
+  // only changes when one of its operands becomes a tile loop, so forward()
+  // visits just the ops marked here; a slice's migration check, once failed,
+  // fails forever, so backward() checks each slice once, from the pending
+  // list (slices are never top-level, so their vpos field is free for the
+  // link).
+  PE_HD void mark_users(int32_t v) {
+    for (int32_t i = g.user_off[v]; i < g.user_off[v + 1]; ++i) {
+      int32_t o = g.slot_op[g.users[i]];
+      a.dirty()[o >> 5] |= 1u << (o & 31);
+    }
+  }
+  PE_HD void push_pending(int32_t s) {
+    a.vpos()[s] = pend;
+    pend = s;
+  }
   PE_HD void slice_created(int32_t u, int32_t d, int32_t axis) {
     a.slcnt()[u]++;
     if (u < g.A) {
@@ -434,6 +459,8 @@ struct Cand {
     }
     for (int32_t s = 0; s < g.E; ++s) a.opnd()[s] = g.oopnd[s];
     for (int32_t w = 0; w <= (A >> 5); ++w) a.carry()[w] = 0;
+    for (int32_t w = 0; w <= (N >> 5); ++w) a.dirty()[w] = 0;
+    pend = -1;
     nslots = A + N;
     nloops = 0;
     nfs = 0;
@@ -481,9 +508,11 @@ struct Cand {
     a.vaux()[s] = dim | (l << 3);
     a.uses()[s] = 1;  // the loop yield
     body_append(l, s);
+    push_pending(s);
     a.uses()[v] = 1;  // the slice
     slice_created(v, dim, axis);
     replace_uses(v, ls);
+    mark_users(v);
     if (v < g.A) push_front(ls);
     else set_pos(ls, 2 * (v - g.A) + 1);
     return !bad();
@@ -622,6 +651,7 @@ struct Cand {
         a.vref()[sl] = u;
         a.vaux()[sl] = d | (l << 3);
         body_append(l, sl);
+        push_pending(sl);
         a.uses()[u]++;
         slice_created(u, d, p.axis);
         if (nc < 8) {
@@ -651,33 +681,48 @@ struct Cand {
     int32_t xv = g.A + o;
     a.vref()[xv] = l;
     mark_loop_value(xv, l);
+    mark_users(xv);
   }
 
+  // REF propagate.cc:250-280: one in-order sweep over the top-level ops,
+  // restricted to the ops whose operands changed (users are always later
+  // in program order, so the sweep never has to look back).
   PE_HD void forward() {
-    for (int32_t o = 0; o < g.N; ++o) {
-      if (a.vk()[g.A + o] != VK_TOP) continue;
-      if (!has_tiled_operand(o)) continue;
-      if (g.orule_err[o]) {
-        fail(PE_CAND_INTERNAL);
-        return;
+    int32_t nw = (g.N >> 5) + 1;
+    for (int32_t w = 0; w < nw; ++w) {
+      uint32_t bits;
+      while ((bits = a.dirty()[w]) != 0) {
+        int32_t b = pe_ctz(bits);
+        a.dirty()[w] = bits & (bits - 1);
+        int32_t o = (w << 5) + b;
+        if (a.vk()[g.A + o] != VK_TOP) continue;
+        if (!has_tiled_operand(o)) continue;
+        if (g.orule_err[o]) {
+          fail(PE_CAND_INTERNAL);
+          return;
+        }
+        Pull p = plan_pull(o);
+        if (!p.ok) continue;
+        pull(o, p);
+        if (bad()) return;
       }
-      Pull p = plan_pull(o);
-      if (!p.ok) continue;
-      pull(o, p);
-      if (bad()) return;
     }
   }
 
   // ------------------------------------------------------------ backward
-  // REF propagate.cc:284-375: migrate single-use producers of sliced values
-  // into the consuming loop, visiting loops and their body slices in order.
-  PE_HD void backward_loop(int32_t l) {
-    int32_t sz_axis = a.laxis()[l];
-    int64_t sz = asz(sz_axis);
-    int32_t s = a.lhead()[l];
-    while (s >= 0) {
-      int32_t next = a.bnext()[s];
-      if (a.vk()[s] == VK_SLICE) {
+  // REF propagate.cc:284-375: migrate the single-use producer of a sliced
+  // value into the consuming loop.  The reference re-walks every loop body
+  // each sweep; here each slice is checked once, when it is new.  Every
+  // failure is permanent (the producer stays non-TOP, keeps >= 2 uses, or
+  // keeps a non-divisible / conflicting member), and migrations of
+  // different slices commute (each inserts at its own slice's position and
+  // touches only its producer's operands), so the pending order is free.
+  PE_HD void backward_slice(int32_t s) {
+    {
+      int32_t l = a.vaux()[s] >> 3;
+      int32_t sz_axis = a.laxis()[l];
+      int64_t sz = asz(sz_axis);
+      {
         int32_t u = a.vref()[s];
         int32_t d = a.vaux()[s] & 7;
         if (a.vk()[u] == VK_TOP && a.uses()[u] == 1) {
@@ -687,7 +732,6 @@ struct Cand {
           bool simple = kind == kConstant ||
                         (kind == kBroadcastInDim && !((g.omask[P] >> d) & 1));
           bool go = true;
-          int32_t first_new = -1;
           int32_t gc = -1;
           if (!simple) {
             if (g.orule_err[P]) {
@@ -737,9 +781,9 @@ struct Cand {
                   a.vref()[sl] = w;
                   a.vaux()[sl] = dd | (l << 3);
                   body_insert_before(l, s, sl);
+                  push_pending(sl);
                   a.uses()[w]++;
                   slice_created(w, dd, sz_axis);
-                  if (first_new < 0) first_new = sl;
                   if (nc < 8) {
                     cache_u[nc] = w;
                     cache_d[nc] = dd;
@@ -763,11 +807,9 @@ struct Cand {
             a.slcnt()[u]--;
             clear_pos(u);
             a.vk()[u] = VK_DEAD;
-            next = first_new >= 0 ? first_new : a.bnext()[s];
           }
         }
       }
-      s = next;
     }
   }
 
@@ -790,9 +832,13 @@ struct Cand {
   }
 
   PE_HD void backward() {
-    for_top([&](int32_t v) {
-      if (a.vk()[v] == VK_LOOP) backward_loop(a.vref()[v]);
-    });
+    while (pend >= 0) {
+      int32_t s = pend;
+      pend = a.vpos()[s];
+      if (a.vk()[s] != VK_SLICE) continue;
+      backward_slice(s);
+      if (bad()) return;
+    }
   }
 
   // wrap_replicated_args (REF propagate.cc:385-408): arguments used directly

@@ -51,6 +51,8 @@ struct pe_engine {
   // staging for host-pointer calls
   uint8_t* d_io = nullptr;
   size_t io_cap = 0;
+  // work counters of the main-pass kernels (zeroed before each launch)
+  uint32_t* d_ctr = nullptr;
 };
 
 namespace {
@@ -89,22 +91,34 @@ constexpr int kMinBlocks = PE_MIN_BLOCKS;
 __device__ unsigned long long g_phase_cycles[9];
 #endif
 
-// One thread per candidate.  Candidates are assigned statically (i = slot,
-// slot + slots, ...) so the 32 lanes of a warp start their candidates
-// together and stay in similar phases of the sweep (SIMT efficiency).
-// RETRY launches re-evaluate, in full-size arenas, exactly the candidates
-// whose tight arena overflowed (status PE_CAND_CAPACITY).
+#ifndef PE_STATIC_SCHED
+#define PE_STATIC_SCHED 0
+#endif
+// Next candidate of a thread.  Each thread starts on candidate `slot` (the
+// 32 lanes of a warp start together); after that, the main pass hands out
+// candidates from a work counter, so a batch that is not a multiple of the
+// slot count does not leave threads idle while others run a second wave.
+// RETRY launches (few candidates) keep the static stride.
+template <bool RETRY>
+__device__ __forceinline__ uint32_t next_cand(uint32_t i, uint32_t slots, uint32_t* ctr) {
+  if (RETRY || PE_STATIC_SCHED) return i + slots;
+  return slots + atomicAdd(ctr, 1u);
+}
+
+// One thread per candidate.  RETRY launches re-evaluate, in full-size
+// arenas, exactly the candidates whose tight arena overflowed (status
+// PE_CAND_CAPACITY).
 template <bool RETRY>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
 pe_eval_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
                uint8_t* arena, uint32_t slots,
                const pe_action* acts, const uint32_t* off, uint32_t n, pe_cost_params cp,
                int64_t baseline, pe_result* out, int32_t* trace, uint32_t trace_words,
-               uint8_t* argflags) {
+               uint8_t* argflags, uint32_t* ctr) {
   uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
-  for (uint32_t i = slot; i < n; i += slots) {
+  for (uint32_t i = slot; i < n; i = next_cand<RETRY>(i, slots, ctr)) {
     if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
     c.eval(acts + off[i], (int32_t)(off[i + 1] - off[i]), cp, baseline, r,
@@ -121,7 +135,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                   const pe_action* prefix, const uint32_t* poff, const uint64_t* seeds,
                   uint32_t n, int32_t maxd, pe_cost_params cp, int64_t baseline,
                   pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
-                  int32_t legal_words) {
+                  int32_t legal_words, uint32_t* ctr) {
 #if PE_SOLO
   // experiment: one active lane per warp (no SIMT divergence across candidates)
   if (threadIdx.x % 32) return;
@@ -131,7 +145,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
 #endif
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
-  for (uint32_t i = slot; i < n; i += slots) {
+  for (uint32_t i = slot; i < n; i = next_cand<RETRY>(i, slots, ctr)) {
     if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
     c.rollout(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, cp, baseline,
@@ -377,7 +391,8 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   if (!cuda_ok(cudaMalloc(&e->d_arena, (size_t)groups * e->layout.bytes), err,
                "cudaMalloc(arena)") ||
       !cuda_ok(cudaMalloc(&e->d_big_arena, (size_t)big_groups * e->big_layout.bytes), err,
-               "cudaMalloc(big arena)")) {
+               "cudaMalloc(big arena)") ||
+      !cuda_ok(cudaMalloc(&e->d_ctr, 4 * sizeof(uint32_t)), err, "cudaMalloc(counters)")) {
     pe_engine_destroy(e);
     return PE_ERR_CUDA;
   }
@@ -408,6 +423,7 @@ void pe_engine_destroy(pe_engine* e) {
   if (e->d_graph) cudaFree(e->d_graph);
   if (e->d_arena) cudaFree(e->d_arena);
   if (e->d_big_arena) cudaFree(e->d_big_arena);
+  if (e->d_ctr) cudaFree(e->d_ctr);
   if (e->d_io) cudaFree(e->d_io);
   delete e;
 }
@@ -602,13 +618,15 @@ pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* 
       return PE_ERR_CUDA;
   }
   uint32_t slots = launch_slots(e, n);
+  if (!cuda_ok(cudaMemsetAsync(e->d_ctr, 0, sizeof(uint32_t), st), err, "reset work counter"))
+    return PE_ERR_CUDA;
   pe_eval_kernel<false><<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->layout, e->d_arena, slots, d_acts, d_off, n, e->cp, e->baseline, d_out,
-      d_trace, trace_words, d_flags);
+      d_trace, trace_words, d_flags, e->d_ctr);
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
   pe_eval_kernel<true><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->big_layout, e->d_big_arena, bs, d_acts, d_off, n, e->cp, e->baseline, d_out,
-      d_trace, trace_words, d_flags);
+      d_trace, trace_words, d_flags, nullptr);
   e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "pe_eval_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {
@@ -685,14 +703,17 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
       return PE_ERR_CUDA;
   }
   uint32_t slots = launch_slots(e, n);
+  if (!cuda_ok(cudaMemsetAsync(e->d_ctr + 1, 0, sizeof(uint32_t), st), err,
+               "reset work counter"))
+    return PE_ERR_CUDA;
   pe_rollout_kernel<false>
       <<<(slots * kThreadsPerSlot + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff, d_seeds, n, maxd, e->cp,
-      e->baseline, d_acts, d_nacts, d_out, d_legal, lw);
+      e->baseline, d_acts, d_nacts, d_out, d_legal, lw, e->d_ctr + 1);
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
   pe_rollout_kernel<true><<<(bs * kThreadsPerSlot + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff, d_seeds, n, maxd, e->cp,
-      e->baseline, d_acts, d_nacts, d_out, d_legal, lw);
+      e->baseline, d_acts, d_nacts, d_out, d_legal, lw, nullptr);
   e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "pe_rollout_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {
