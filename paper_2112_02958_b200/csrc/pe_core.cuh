@@ -489,7 +489,7 @@ struct Cand {
     if (k != VK_ARG && k != VK_TOP && k != VK_LOOP) return false;  // erased: does not exist
     if (axis < 0 || axis >= g.n_axes) return false;
     if (dim < 0 || dim >= g.vrank[v]) return false;
-    if (g.shape(v)[dim] % asz(axis) != 0) return false;
+    if (g.amod((uint32_t)g.shape(v)[dim], axis) != 0) return false;
     if (carries(v)) return false;
     int32_t l = alloc_loop();
     int32_t ls = alloc_slot();
@@ -567,12 +567,11 @@ struct Cand {
         return p;
       }
     }
-    int64_t sz = asz(p.axis);
     int32_t gc = cbase + p.cls;
     for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
       int32_t k = g.mem[m] >> 2, d = g.mem[m] & 3;
       int32_t u = a.opnd()[base + k];
-      if (g.shape(shape_src(u))[d] % sz != 0) {
+      if (g.amod((uint32_t)g.shape(shape_src(u))[d], p.axis) != 0) {
         p.reason = R_INSUFFICIENT;
         return p;
       }
@@ -721,7 +720,6 @@ struct Cand {
     {
       int32_t l = a.vaux()[s] >> 3;
       int32_t sz_axis = a.laxis()[l];
-      int64_t sz = asz(sz_axis);
       {
         int32_t u = a.vref()[s];
         int32_t d = a.vaux()[s] & 7;
@@ -746,7 +744,7 @@ struct Cand {
               for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
                 int32_t k = g.mem[m] >> 2, dd = g.mem[m] & 3;
                 int32_t w = a.opnd()[pb + k];
-                if (g.shape(shape_src(w))[dd] % sz != 0) go = false;
+                if (g.amod((uint32_t)g.shape(shape_src(w))[dd], sz_axis) != 0) go = false;
                 uint32_t h = vhdr(w);
                 if (hdr_tile(h)) {
                   bool sa = hdr_axis(h) == sz_axis, sd = hdr_dim(h) == dd;
@@ -925,12 +923,12 @@ struct Cand {
   PE_HD int64_t local_dim(const Low& w, int d) {
     uint32_t ax1 = spec_axis(w.spec, d);
     if (!ax1) return w.g[d];
-    int64_t s = asz(ax1 - 1);
-    if (w.g[d] % s != 0) {
+    uint32_t x = (uint32_t)w.g[d];
+    if (g.amod(x, (int32_t)ax1 - 1) != 0) {
       fail(PE_CAND_INTERNAL);  // local_shape divisibility (REF mesh.cc:117-122)
       return 1;
     }
-    return w.g[d] / s;
+    return g.aquo(x, (int32_t)ax1 - 1);
   }
   PE_HD int64_t local_elems(const Low& w) {
     int64_t e = 1;
@@ -1067,7 +1065,7 @@ struct Cand {
     for (int d = 0; d < kMaxRank; ++d) r.g[d] = g.shape(xv)[d];
     if (l >= 0) {
       int32_t dd = (a.vaux()[v] & 7) - 1;
-      if (dd >= 0) r.g[dd] = (int32_t)(r.g[dd] / asz(lax));
+      if (dd >= 0) r.g[dd] = (int32_t)g.aquo((uint32_t)r.g[dd], lax);
     }
     r.spec = (uint32_t)rank << 24;
     r.acq = 0;
@@ -1275,7 +1273,7 @@ struct Cand {
       int32_t direct = a.uses()[x] - a.slcnt()[x] - (result_ref == x ? 1 : 0);
       if (direct == 0 && a.aslice()[x] >= 0) {
         int d = a.aslice()[x] & 7, ax = a.aslice()[x] >> 3;
-        if (w.g[d] % asz(ax) == 0) w.spec = spec_set_axis(w.spec, d, (uint32_t)(ax + 1));
+        if (g.amod((uint32_t)w.g[d], ax) == 0) w.spec = spec_set_axis(w.spec, d, (uint32_t)(ax + 1));
       }
       store(x, w);
       register_type(x, w);

@@ -376,6 +376,9 @@ void validate(const HostGraph& g) {
   for (size_t a = 0; a < g.axis_names.size(); ++a) {
     if (g.axis_names[a].empty()) invalid("mesh axis with empty name");
     if (g.axis_sizes[a] < 1) invalid("mesh axis \"" + g.axis_names[a] + "\" has size < 1");
+    if (g.axis_sizes[a] > kMaxDim)
+      invalid("mesh axis \"" + g.axis_names[a] + "\" size exceeds 2^31-1",
+              PE_ERR_INVALID_ARGUMENT);
     if (!names.insert(g.axis_names[a]).second)
       invalid("duplicate mesh axis \"" + g.axis_names[a] + "\"");
   }
@@ -384,8 +387,11 @@ void validate(const HostGraph& g) {
   if (g.name.empty()) invalid("program without a name");
   for (const HostArg& a : g.args) {
     if ((int)a.shape.size() > kMaxRank) invalid("argument %" + a.id + " rank exceeds 4");
-    for (int64_t d : a.shape)
+    for (int64_t d : a.shape) {
       if (d < 1) invalid("argument %" + a.id + " dimension < 1");
+      if (d > kMaxDim)
+        invalid("argument %" + a.id + " dimension exceeds 2^31-1", PE_ERR_INVALID_ARGUMENT);
+    }
   }
   auto fail = [](const HostOp& op, const std::string& m, int code = PE_ERR_VALIDATION) {
     invalid("op %" + op.id + ": " + m, code);
@@ -395,8 +401,10 @@ void validate(const HostGraph& g) {
   };
   for (const HostOp& op : g.ops) {
     if ((int)op.shape.size() > kMaxRank) fail(op, "rank exceeds 4");
-    for (int64_t d : op.shape)
+    for (int64_t d : op.shape) {
       if (d < 1) fail(op, "result dimension < 1");
+      if (d > kMaxDim) fail(op, "result dimension exceeds 2^31-1", PE_ERR_INVALID_ARGUMENT);
+    }
     std::vector<std::vector<int64_t>> in;
     for (int32_t v : op.operands) in.push_back(g.value_shape(v));
     auto arity = [&](size_t n) {
@@ -761,6 +769,10 @@ GraphView HostGraph::host_view() const {
   v.n_axes = (int32_t)axis_names.size();
   for (int a = 0; a < v.n_axes; ++a) {
     v.axis_size[a] = axis_sizes[a];
+    v.axis_sz32[a] = (uint32_t)axis_sizes[a];
+    v.axis_shift[a] = -1;
+    for (int sh = 0; sh < 31; ++sh)
+      if ((int64_t(1) << sh) == axis_sizes[a]) v.axis_shift[a] = sh;
     int rank = 0;
     for (int b = 0; b < v.n_axes; ++b)
       if (axis_names[b] < axis_names[a]) ++rank;

@@ -31,6 +31,7 @@ enum Role : uint8_t { kPass = 0, kContract = 1, kBlocked = 2 };
 
 constexpr int kMaxRank = 4;
 constexpr int kMaxAxes = 4;
+constexpr int64_t kMaxDim = 2147483647;  // dims and axis sizes fit int32
 
 struct GraphView {
   int32_t A;        // arguments
@@ -38,6 +39,21 @@ struct GraphView {
   int32_t E;        // operand slots
   int32_t n_axes;
   int64_t axis_size[kMaxAxes];
+  // 32-bit division by an axis size: dims and axis sizes are validated to
+  // fit int32 (pe_graph.cc validate), so q = x >> shift / x & (size-1) for
+  // power-of-two sizes (shift >= 0), else 32-bit x / size, x % size -- the
+  // same integers as the reference's int64 arithmetic, without the int64
+  // division subroutine on the device.
+  uint32_t axis_sz32[kMaxAxes];
+  int32_t axis_shift[kMaxAxes];
+  PE_HD uint32_t amod(uint32_t x, int32_t ax) const {
+    int32_t sh = axis_shift[ax];
+    return sh >= 0 ? (x & ((1u << sh) - 1u)) : x % axis_sz32[ax];
+  }
+  PE_HD uint32_t aquo(uint32_t x, int32_t ax) const {
+    int32_t sh = axis_shift[ax];
+    return sh >= 0 ? (x >> sh) : x / axis_sz32[ax];
+  }
   // rank of each axis name in lexicographic order: ShardingSpec::pending_sum
   // is kept sorted by NAME (REF mesh.cc:74-77), so `pending_sum.front()` is
   // the axis with the smallest name rank.

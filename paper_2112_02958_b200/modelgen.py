@@ -391,9 +391,10 @@ _BIN = ("add", "sub", "mul", "div", "maximum")
 _UN = ("neg", "exp", "tanh", "rsqrt")
 
 
-def random_program(seed: int, mesh=(("m", 2),), max_ops=15) -> str:
+def random_program(seed: int, mesh=(("m", 2),), max_ops=15, dims=_DIMS) -> str:
     """A random valid program over all 18 base kinds: rank
-    1-3, dims in {2,4,8}, 2-4 arguments, 4-15 ops."""
+    1-3, dims drawn from `dims` (default {2,4,8}), 2-4 arguments, 4-15 ops."""
+    _DIMS = dims  # noqa: N806
     rng = random.Random(seed)
     b = ProgramBuilder(f"rand{seed}", list(mesh))
     vals = []
@@ -440,7 +441,7 @@ def random_program(seed: int, mesh=(("m", 2),), max_ops=15) -> str:
                 d = rng.randrange(r - 1)
                 ns = s[:d] + [s[d] * s[d + 1]] + s[d + 2:]
             else:
-                cands = [i for i in range(r) if s[i] >= 4]
+                cands = [i for i in range(r) if s[i] >= 4 and s[i] % 2 == 0]
                 if not cands or r >= 4:
                     continue
                 d = rng.choice(cands)

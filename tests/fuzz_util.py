@@ -4,6 +4,10 @@ from __future__ import annotations
 from paper_2112_02958_b200 import modelgen
 
 MESHES = ((("m", 2),), (("a", 2), ("b", 4)), (("m", 8),))
+# non-power-of-two axis sizes (the device divides by them with 32-bit
+# division instead of shifts), with dims drawn to be divisible by them
+ODD_MESHES = ((("m", 3),), (("a", 3), ("b", 2)), (("m", 6),))
+ODD_DIMS = (3, 6, 12)
 
 
 def corpus(n_programs: int, seed0: int = 0, seqs_per_program: int = 4):

@@ -42,6 +42,9 @@ def test_parse_errors_map_to_reference_errors():
         engine.Graph("func @f(%x: f32[8,64]) -> f32[8,65] { %y = reshape(%x) : f32[8,65]\n return %y }")
     g = engine.Graph("func @id(%x: f32[4]) -> f32[4] { return %x }")
     assert g.n_ops == 0
+    # dims and axis sizes must fit int32 (the engine's value records)
+    with pytest.raises(engine.Error, match="exceeds 2\\^31-1"):
+        engine.Graph("func @f(%x: f32[4294967296]) -> f32[4294967296] { return %x }")
 
 
 def test_engine_refuses_without_device():

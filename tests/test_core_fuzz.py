@@ -24,6 +24,21 @@ def test_random_programs_match_oracle(oracle_lib, harness_lib, seed0):
     assert n_bad == 0
 
 
+def test_non_power_of_two_meshes_match_oracle(oracle_lib, harness_lib):
+    n_bad = n_tiled = 0
+    for i in range(150):
+        mesh = F.ODD_MESHES[i % 3]
+        text = modelgen.random_program(31000 + i, mesh, dims=F.ODD_DIMS)
+        seqs = F.legal_sequences(text, mesh, 31000 + i)
+        ro, to = H.eval_batch("oracle", text, seqs, trace_words=8192)
+        rh, th = H.eval_batch("harness", text, seqs, trace_words=8192)
+        for a, b, x, y in zip(ro, rh, to, th):
+            n_tiled += a.n_steps > 0 and a.status == 0
+            if H.compare_results(a, b) or F.first_trace_diff(x, y) >= 0:
+                n_bad += 1
+    assert n_bad == 0 and n_tiled > 100
+
+
 def test_illegal_and_unordered_actions_match(oracle_lib, harness_lib):
     bad = 0
     for text, mesh, seqs in F.corpus(150, 777):

@@ -37,8 +37,13 @@ def test_random_programs_device_vs_oracle(oracle_lib):
     bad = []
     total = 0
     for i in range(48):
-        mesh = F.MESHES[i % 3]
-        text = modelgen.random_program(9000 + i, mesh)
+        # every fourth program on a non-power-of-two mesh (32-bit division)
+        if i % 4 == 3:
+            mesh = F.ODD_MESHES[i % 3]
+            text = modelgen.random_program(9000 + i, mesh, dims=F.ODD_DIMS)
+        else:
+            mesh = F.MESHES[i % 3]
+            text = modelgen.random_program(9000 + i, mesh)
         seqs = F.legal_sequences(text, mesh, 4242 + i, n_seqs=6)
         seqs += [modelgen.random_actions(31 * i + k, text, mesh) for k in range(4)]
         eng = _engine(text)
