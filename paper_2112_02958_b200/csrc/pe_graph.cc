@@ -769,10 +769,15 @@ GraphView HostGraph::host_view() const {
   v.n_axes = (int32_t)axis_names.size();
   for (int a = 0; a < v.n_axes; ++a) {
     v.axis_size[a] = axis_sizes[a];
-    v.axis_sz32[a] = (uint32_t)axis_sizes[a];
-    v.axis_shift[a] = -1;
-    for (int sh = 0; sh < 31; ++sh)
-      if ((int64_t(1) << sh) == axis_sizes[a]) v.axis_shift[a] = sh;
+    {
+      uint64_t d = (uint64_t)axis_sizes[a];
+      int l = 0;
+      while ((uint64_t(1) << l) < d) ++l;  // ceil(log2 d)
+      int s = 31 + l;
+      v.axis_sz32[a] = (uint32_t)d;
+      v.axis_mshift[a] = s;
+      v.axis_magic[a] = (uint32_t)(((uint64_t(1) << s) + d - 1) / d);
+    }
     int rank = 0;
     for (int b = 0; b < v.n_axes; ++b)
       if (axis_names[b] < axis_names[a]) ++rank;

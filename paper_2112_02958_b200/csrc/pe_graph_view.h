@@ -39,21 +39,23 @@ struct GraphView {
   int32_t E;        // operand slots
   int32_t n_axes;
   int64_t axis_size[kMaxAxes];
-  // 32-bit division by an axis size: dims and axis sizes are validated to
-  // fit int32 (pe_graph.cc validate), so q = x >> shift / x & (size-1) for
-  // power-of-two sizes (shift >= 0), else 32-bit x / size, x % size -- the
-  // same integers as the reference's int64 arithmetic, without the int64
-  // division subroutine on the device.
+  // Division by an axis size d without a divide instruction sequence (the
+  // inlined 32-bit divide is ~25 SASS instructions and local_dim is inlined
+  // at many unrolled sites; code size is what bounds the rollout kernel --
+  // instruction-cache stalls).  Dims and axis sizes are
+  // validated to fit int32 (pe_graph.cc validate), so for 0 <= x < 2^31
+  //   x / d == (x * m) >> s,  m = ceil(2^s / d),  s = 31 + ceil(log2 d)
+  // exactly (Granlund & Montgomery 1994, Thm 4.2: the error m*d - 2^s < d
+  // <= 2^(s-31)); m < 2^32 for every d >= 1.  These are the same integers
+  // as the reference's int64 arithmetic (tests/test_semantics.py checks the
+  // identity; the fuzz runs power-of-two and other meshes).
   uint32_t axis_sz32[kMaxAxes];
-  int32_t axis_shift[kMaxAxes];
-  PE_HD uint32_t amod(uint32_t x, int32_t ax) const {
-    int32_t sh = axis_shift[ax];
-    return sh >= 0 ? (x & ((1u << sh) - 1u)) : x % axis_sz32[ax];
-  }
+  uint32_t axis_magic[kMaxAxes];
+  int32_t axis_mshift[kMaxAxes];
   PE_HD uint32_t aquo(uint32_t x, int32_t ax) const {
-    int32_t sh = axis_shift[ax];
-    return sh >= 0 ? (x >> sh) : x / axis_sz32[ax];
+    return (uint32_t)(((uint64_t)x * axis_magic[ax]) >> axis_mshift[ax]);
   }
+  PE_HD uint32_t amod(uint32_t x, int32_t ax) const { return x - aquo(x, ax) * axis_sz32[ax]; }
   // rank of each axis name in lexicographic order: ShardingSpec::pending_sum
   // is kept sorted by NAME (REF mesh.cc:74-77), so `pending_sum.front()` is
   // the axis with the smallest name rank.

@@ -31,3 +31,23 @@ def test_searched_plan_preserves_semantics(oracle_lib, harness_lib):
     assert megatron(p.result, 2)
     ok, diff, order_preserving = H.oracle_check_equivalence(text, search.plan_actions(p), trials=3)
     assert ok and not order_preserving  # Megatron has all_reduces: 1e-5 tolerance path
+
+
+def test_axis_division_magic_is_exact():
+    # pe_graph_view.h aquo/amod: x / d == (x * m) >> s for 0 <= x < 2^31,
+    # m = ceil(2^s / d), s = 31 + ceil(log2 d) (same constants as
+    # pe_graph.cc host_view)
+    import random
+    rng = random.Random(5)
+    ds = list(range(1, 4097)) + [rng.randrange(4097, 2**31) for _ in range(2000)] + [2**31 - 1, 2**30,
+                                                                                      2**30 + 1]
+    for d in ds:
+        lg = (d - 1).bit_length()
+        s = 31 + lg
+        m = -(-(1 << s) // d)
+        assert m < 2**32
+        xs = [0, 1, d - 1, d, d + 1, 2**31 - 1, (2**31 - 1) // d * d, (2**31 - 1) // d * d - 1]
+        xs += [rng.randrange(0, 2**31) for _ in range(20)]
+        for x in xs:
+            if 0 <= x < 2**31:
+                assert (x * m) >> s == x // d, (d, x)
