@@ -920,20 +920,31 @@ struct Cand {
 
   // ------------------------------------------------------------ lowering
   PE_HD int32_t rank_of_spec(uint32_t spec) const { return (spec >> 24) & 7; }
+  // local_shape (REF mesh.cc:110-124): global dim / axis size, InternalError
+  // when not divisible.  Branch-free (an unsharded dim divides by 1): after
+  // a failure the candidate's outputs are discarded (finish), so only the
+  // status matters, not the quotient returned alongside it.
   PE_HD int64_t local_dim(const Low& w, int d) {
     uint32_t ax1 = spec_axis(w.spec, d);
-    if (!ax1) return w.g[d];
     uint32_t x = (uint32_t)w.g[d];
-    if (g.amod(x, (int32_t)ax1 - 1) != 0) {
-      fail(PE_CAND_INTERNAL);  // local_shape divisibility (REF mesh.cc:117-122)
-      return 1;
-    }
-    return g.aquo(x, (int32_t)ax1 - 1);
+    uint32_t q = g.quo1(x, ax1);
+    if (x != q * g.axis_sz32[ax1]) fail(PE_CAND_INTERNAL);
+    return q;
   }
   PE_HD int64_t local_elems(const Low& w) {
     int64_t e = 1;
+    uint32_t rem = 0;
     int r = rank_of_spec(w.spec);
-    for (int d = 0; d < r; ++d) e *= local_dim(w, d);
+#pragma unroll
+    for (int d = 0; d < kMaxRank; ++d) {
+      uint32_t ax1 = spec_axis(w.spec, d);
+      uint32_t x = (uint32_t)w.g[d];
+      uint32_t q = g.quo1(x, ax1);
+      bool in = d < r;
+      rem |= in ? x - q * g.axis_sz32[ax1] : 0u;
+      e *= in ? (int64_t)q : 1;
+    }
+    if (rem) fail(PE_CAND_INTERNAL);
     return e;
   }
   PE_HD int64_t global_bytes(const Low& w) const {
@@ -1026,6 +1037,7 @@ struct Cand {
     Low w = load(v);
     int32_t b0 = w.buf;
     int r = rank_of_spec(w.spec);
+#pragma unroll 1
     for (int d = 0; d < r; ++d) {
       uint32_t ax1 = spec_axis(w.spec, d);
       if (!ax1) continue;
@@ -1051,6 +1063,7 @@ struct Cand {
     int32_t lax = l >= 0 ? (int32_t)a.laxis()[l] : -1;
     uint8_t kind = g.okind[o];
     Low in0, in1;
+#pragma unroll 1
     for (int32_t k = 0; k < n; ++k) {
       Low w = materialize(a.opnd()[base + k], lax);
       if (bad()) return;
@@ -1070,6 +1083,7 @@ struct Cand {
     r.spec = (uint32_t)rank << 24;
     r.acq = 0;
     r.buf = -1;
+#pragma unroll 1
     for (int32_t k = 0; k < n; ++k) {
       Low w = k == 0 ? in0 : k == 1 ? in1 : load(a.opnd()[base + k]);
       r.spec |= spec_pending(w.spec) << 16;
@@ -1127,6 +1141,7 @@ struct Cand {
     }
     int32_t j = new_op(kind, -1, -1, n);
     if (j < 0) return;
+#pragma unroll 1
     for (int32_t k = 0; k < n; ++k)
       add_operand(j, k == 0 ? in0.buf : k == 1 ? in1.buf : a.lo_buf()[a.opnd()[base + k]]);
     int64_t out_elems = local_elems(r);
@@ -1173,6 +1188,7 @@ struct Cand {
       if (bad()) return;
     }
     int rk = rank_of_spec(src.spec);
+#pragma unroll 1
     for (int d2 = 0; d2 < rk; ++d2) {
       if ((int32_t)spec_axis(src.spec, d2) != lax + 1) continue;
       if ((src.acq >> d2) & 1) {

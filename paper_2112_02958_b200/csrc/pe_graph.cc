@@ -767,6 +767,9 @@ GraphView HostGraph::host_view() const {
   v.N = (int32_t)ops.size();
   v.E = (int32_t)oopnd.size();
   v.n_axes = (int32_t)axis_names.size();
+  v.axis_sz32[0] = 1;  // "no axis": divide by 1
+  v.axis_magic[0] = 1u << 31;
+  v.axis_mshift[0] = 31;
   for (int a = 0; a < v.n_axes; ++a) {
     v.axis_size[a] = axis_sizes[a];
     {
@@ -774,9 +777,9 @@ GraphView HostGraph::host_view() const {
       int l = 0;
       while ((uint64_t(1) << l) < d) ++l;  // ceil(log2 d)
       int s = 31 + l;
-      v.axis_sz32[a] = (uint32_t)d;
-      v.axis_mshift[a] = s;
-      v.axis_magic[a] = (uint32_t)(((uint64_t(1) << s) + d - 1) / d);
+      v.axis_sz32[a + 1] = (uint32_t)d;
+      v.axis_mshift[a + 1] = s;
+      v.axis_magic[a + 1] = (uint32_t)(((uint64_t(1) << s) + d - 1) / d);
     }
     int rank = 0;
     for (int b = 0; b < v.n_axes; ++b)

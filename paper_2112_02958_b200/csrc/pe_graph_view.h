@@ -49,13 +49,18 @@ struct GraphView {
   // <= 2^(s-31)); m < 2^32 for every d >= 1.  These are the same integers
   // as the reference's int64 arithmetic (tests/test_semantics.py checks the
   // identity; the fuzz runs power-of-two and other meshes).
-  uint32_t axis_sz32[kMaxAxes];
-  uint32_t axis_magic[kMaxAxes];
-  int32_t axis_mshift[kMaxAxes];
-  PE_HD uint32_t aquo(uint32_t x, int32_t ax) const {
-    return (uint32_t)(((uint64_t)x * axis_magic[ax]) >> axis_mshift[ax]);
+  // Tables are indexed by axis + 1 (the spec-word nibble); entry 0 is the
+  // divisor 1 (m = 2^31, s = 31), so an unsharded dim divides by 1.
+  uint32_t axis_sz32[kMaxAxes + 1];
+  uint32_t axis_magic[kMaxAxes + 1];
+  int32_t axis_mshift[kMaxAxes + 1];
+  PE_HD uint32_t quo1(uint32_t x, uint32_t ax1) const {
+    return (uint32_t)(((uint64_t)x * axis_magic[ax1]) >> axis_mshift[ax1]);
   }
-  PE_HD uint32_t amod(uint32_t x, int32_t ax) const { return x - aquo(x, ax) * axis_sz32[ax]; }
+  PE_HD uint32_t aquo(uint32_t x, int32_t ax) const { return quo1(x, (uint32_t)ax + 1); }
+  PE_HD uint32_t amod(uint32_t x, int32_t ax) const {
+    return x - aquo(x, ax) * axis_sz32[ax + 1];
+  }
   // rank of each axis name in lexicographic order: ShardingSpec::pending_sum
   // is kept sorted by NAME (REF mesh.cc:74-77), so `pending_sum.front()` is
   // the axis with the smallest name rank.
