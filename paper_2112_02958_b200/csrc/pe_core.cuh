@@ -1002,14 +1002,9 @@ struct Cand {
     // ops are emitted in order, so the current op is always the latest use
     if (buf >= g.A) a.em_last()[buf - g.A] = j;
   }
-  PE_HD int32_t pending_front(uint32_t spec) const {
-    uint32_t pm = spec_pending(spec);
-    int32_t best = -1;
-    for (int32_t ax = 0; ax < g.n_axes; ++ax)
-      if ((pm >> ax) & 1)
-        if (best < 0 || g.axis_name_rank[ax] < g.axis_name_rank[best]) best = ax;
-    return best;
-  }
+  // pending_sum.front(): the pending axis with the smallest name (table
+  // over the 4-bit pending mask, GraphView::pend_front)
+  PE_HD int32_t pending_front(uint32_t spec) const { return g.pend_front[spec_pending(spec)]; }
   // emit_gather (REF spmd.cc:85-99): updates the record in place
   PE_HD void emit_gather(Low& w, int d) {
     int32_t ax = (int32_t)spec_axis(w.spec, d) - 1;
@@ -1220,14 +1215,10 @@ struct Cand {
   }
 
   // lower_loop (REF spmd.cc:157-204)
-  PE_HD void lower_loop(int32_t v) {
-    int32_t l = a.vref()[v];
+  // (the body is lowered by lower(); this is the loop's result from its
+  // yield)
+  PE_HD void finish_loop(int32_t v, int32_t l) {
     int32_t lax = a.laxis()[l];
-    for (int32_t s = a.lhead()[l]; s >= 0; s = a.bnext()[s]) {
-      if (a.vk()[s] == VK_SLICE) lower_slice(s, l);
-      else lower_base(s, a.vref()[s], l);
-      if (bad()) return;
-    }
     Low yv = load(a.lyield()[l]);
     int32_t lt = a.ltype()[l];
     if (a.lkind()[l] == LK_TILE) {
@@ -1298,9 +1289,7 @@ struct Cand {
     }
     for_top([&](int32_t v) {
       uint8_t k = a.vk()[v];
-      if (k == VK_TOP) {
-        lower_base(v, a.vref()[v], -1);
-      } else if (k == VK_ATOMIC) {
+      if (k == VK_ATOMIC) {
         Low w = load(a.vref()[v]);
         int r = rank_of_spec(w.spec);
         bool rep = spec_pending(w.spec) == 0;
@@ -1310,9 +1299,22 @@ struct Cand {
           return;
         }
         store(v, w);
-      } else if (k == VK_LOOP) {
-        lower_loop(v);
+        return;
       }
+      if (k != VK_TOP && k != VK_LOOP) return;
+      // A top-level op is lowered as a one-item body, so top-level and
+      // per-iteration ops share one inlined lower_base (code size bounds
+      // this kernel: instruction-cache stalls).
+      int32_t l = k == VK_LOOP ? a.vref()[v] : -1;
+      int32_t s = l >= 0 ? a.lhead()[l] : v;
+      while (s >= 0) {
+        int32_t next = l >= 0 ? a.bnext()[s] : -1;
+        if (l >= 0 && a.vk()[s] == VK_SLICE) lower_slice(s, l);
+        else lower_base(s, a.vref()[s], l);
+        if (bad()) return;
+        s = next;
+      }
+      if (l >= 0) finish_loop(v, l);
     });
     if (bad()) return;
     Low res = load(result_ref);

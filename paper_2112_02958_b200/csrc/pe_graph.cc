@@ -786,6 +786,13 @@ GraphView HostGraph::host_view() const {
       if (axis_names[b] < axis_names[a]) ++rank;
     v.axis_name_rank[a] = rank;
   }
+  for (int pm = 0; pm < 16; ++pm) {
+    int best = -1;
+    for (int ax = 0; ax < v.n_axes; ++ax)
+      if ((pm >> ax) & 1)
+        if (best < 0 || v.axis_name_rank[ax] < v.axis_name_rank[best]) best = ax;
+    v.pend_front[pm] = (int8_t)best;
+  }
   v.result = result;
   v.vshape = vshape.data();
   v.vrank = vrank.data();

@@ -65,6 +65,8 @@ struct GraphView {
   // is kept sorted by NAME (REF mesh.cc:74-77), so `pending_sum.front()` is
   // the axis with the smallest name rank.
   int32_t axis_name_rank[kMaxAxes];
+  // pending mask (4 bits) -> its axis with the smallest name rank (-1 if 0)
+  int8_t pend_front[16];
   int32_t result;   // returned value index
 
   // values [A+N]: args first, then op results
