@@ -971,7 +971,11 @@ struct Cand {
     a.lo_g()[v] = gg;
   }
   PE_HD void register_type(int32_t buf, const Low& w) {
-    int64_t gb = global_bytes(w), lb = 4 * local_elems(w);
+    register_type(buf, w, 4 * local_elems(w));
+  }
+  // (lb = the record's local bytes when the caller already has them)
+  PE_HD void register_type(int32_t buf, const Low& w, int64_t lb) {
+    int64_t gb = global_bytes(w);
     if (buf < g.A) {
       a.arg_gb()[buf] = gb;
       a.arg_lb()[buf] = lb;
@@ -1005,43 +1009,56 @@ struct Cand {
   // pending_sum.front(): the pending axis with the smallest name (table
   // over the 4-bit pending mask, GraphView::pend_front)
   PE_HD int32_t pending_front(uint32_t spec) const { return g.pend_front[spec_pending(spec)]; }
-  // emit_gather (REF spmd.cc:85-99): updates the record in place
-  PE_HD void emit_gather(Low& w, int d) {
-    int32_t ax = (int32_t)spec_axis(w.spec, d) - 1;
-    int32_t j = new_op(kAllGather, ax, d, 1);
+  // emit_gather (REF spmd.cc:85-99) of dim d over axis ax,
+  // emit_all_reduce (REF spmd.cc:102-114) over axis ax (d = -1), or the
+  // slice_by_coord of lower_slice_axis (REF spmd.cc:240-252) of dim d by the
+  // loop axis ax; updates the record in place.  One function for the three
+  // so each emitting loop inlines a single copy (code size).
+  PE_HD void emit_coll(Low& w, int32_t kind, int32_t ax, int d) {
+    int32_t j = new_op(kind, ax, d, 1);
     if (j < 0) return;
     add_operand(j, w.buf);
-    w.spec = spec_set_axis(w.spec, d, 0);
-    w.acq &= ~(1u << d);
-    a.em_lb()[j] = 4 * local_elems(w);
+    if (kind == kAllGather) {
+      w.spec = spec_set_axis(w.spec, d, 0);
+      w.acq &= ~(1u << d);
+    } else if (kind == kAllReduce) {
+      w.spec &= ~(1u << (16 + ax));
+    } else {
+      w.spec = spec_set_axis(w.spec, d, (uint32_t)(ax + 1));
+      w.acq |= 1u << d;
+    }
+    int64_t lb = 4 * local_elems(w);
+    a.em_lb()[j] = lb;
     w.buf = g.A + j;
-    register_type(w.buf, w);
+    register_type(w.buf, w, lb);
   }
-  // emit_all_reduce (REF spmd.cc:102-114)
-  PE_HD void emit_all_reduce(Low& w, int32_t ax) {
-    int32_t j = new_op(kAllReduce, ax, -1, 1);
-    if (j < 0) return;
-    add_operand(j, w.buf);
-    w.spec &= ~(1u << (16 + ax));
-    a.em_lb()[j] = 4 * local_elems(w);
-    w.buf = g.A + j;
-    register_type(w.buf, w);
-  }
-  // materialize_for_direct_use (REF spmd.cc:119-129); loop_axis = -1 at top
+  PE_HD void emit_all_reduce(Low& w, int32_t ax) { emit_coll(w, kAllReduce, ax, -1); }
+  // materialize_for_direct_use (REF spmd.cc:119-129); loop_axis = -1 at top.
+  // Gathers every sharded dim in increasing order (a dim sharded by the
+  // enclosing loop's axis and acquired in it stays), then all-reduces the
+  // pending axes in name order -- one emission per iteration.
   PE_HD Low materialize(int32_t v, int32_t loop_axis) {
     Low w = load(v);
     int32_t b0 = w.buf;
     int r = rank_of_spec(w.spec);
+    while (true) {
+      int32_t ax = -1, dd = -1;
 #pragma unroll 1
-    for (int d = 0; d < r; ++d) {
-      uint32_t ax1 = spec_axis(w.spec, d);
-      if (!ax1) continue;
-      bool live = loop_axis >= 0 && (int32_t)ax1 - 1 == loop_axis && ((w.acq >> d) & 1);
-      if (!live) emit_gather(w, d);
-      if (bad()) return w;
-    }
-    while (spec_pending(w.spec)) {
-      emit_all_reduce(w, pending_front(w.spec));
+      for (int d = 0; d < r; ++d) {
+        uint32_t ax1 = spec_axis(w.spec, d);
+        if (!ax1) continue;
+        bool live = loop_axis >= 0 && (int32_t)ax1 - 1 == loop_axis && ((w.acq >> d) & 1);
+        if (!live) {
+          dd = d;
+          ax = (int32_t)ax1 - 1;
+          break;
+        }
+      }
+      if (dd < 0) {
+        if (!spec_pending(w.spec)) break;
+        ax = pending_front(w.spec);
+      }
+      emit_coll(w, dd >= 0 ? kAllGather : kAllReduce, ax, dd);
       if (bad()) return w;
     }
     // every gather / all_reduce moves the record to a new buffer
@@ -1162,7 +1179,7 @@ struct Cand {
         break;
     }
     r.buf = g.A + j;
-    register_type(r.buf, r);
+    register_type(r.buf, r, 4 * out_elems);
     store(v, r);
   }
 
@@ -1178,32 +1195,34 @@ struct Cand {
       store(s, r);
       return;
     }
-    if (spec_axis(src.spec, d) != 0) {
-      emit_gather(src, d);
-      if (bad()) return;
-    }
+    // gather dim d if sharded (by another axis), then every dim sharded by
+    // the loop axis in increasing order (InternalError if acquired), then
+    // the slice itself -- one emission per iteration
     int rk = rank_of_spec(src.spec);
+    while (true) {
+      int32_t kind = kSliceByCoord, ax = lax, dd = d;
+      if (spec_axis(src.spec, d) != 0) {
+        kind = kAllGather;
+        ax = (int32_t)spec_axis(src.spec, d) - 1;
+      } else {
 #pragma unroll 1
-    for (int d2 = 0; d2 < rk; ++d2) {
-      if ((int32_t)spec_axis(src.spec, d2) != lax + 1) continue;
-      if ((src.acq >> d2) & 1) {
-        fail(PE_CAND_INTERNAL);
-        return;
+        for (int d2 = 0; d2 < rk; ++d2) {
+          if ((int32_t)spec_axis(src.spec, d2) != lax + 1) continue;
+          if ((src.acq >> d2) & 1) {
+            fail(PE_CAND_INTERNAL);
+            return;
+          }
+          kind = kAllGather;
+          dd = d2;
+          break;
+        }
       }
-      emit_gather(src, d2);
+      if (kind == kSliceByCoord) store(u, src);
+      emit_coll(src, kind, ax, dd);
       if (bad()) return;
+      if (kind == kSliceByCoord) break;
     }
-    store(u, src);
-    int32_t j = new_op(kSliceByCoord, lax, d, 1);
-    if (j < 0) return;
-    add_operand(j, src.buf);
-    Low r = src;
-    r.spec = spec_set_axis(r.spec, d, (uint32_t)(lax + 1));
-    r.acq |= 1u << d;
-    a.em_lb()[j] = 4 * local_elems(r);
-    r.buf = g.A + j;
-    register_type(r.buf, r);
-    store(s, r);
+    store(s, src);
   }
 
   PE_HD bool has_axis(uint32_t spec, int32_t ax) const {
