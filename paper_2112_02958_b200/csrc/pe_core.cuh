@@ -90,6 +90,19 @@ using LF = Field<T, kLanes * (int)sizeof(T)>;
 struct alignas(16) G4 {
   int32_t v[kMaxRank];
 };
+// a 32-byte record as two 16-byte halves (whole-record writes keep every
+// L2 sector fully written: no partial-sector read-modify-write in DRAM)
+struct alignas(16) V4 {
+  int32_t x, y, z, w;
+};
+// first half of a LowRec (buf, spec, acq, 0): written and read as one
+// 16-byte access so the record's 32-byte sector is always written whole
+struct alignas(16) LowHead {
+  int32_t buf;
+  uint32_t spec;
+  uint32_t acq;
+  int32_t pad;
+};
 
 struct Layout {
   Caps caps;
@@ -128,10 +141,13 @@ struct Arena {
   PE_REC(bnext, int32_t, r32, vrec, 20, kLanes * kRec)
   PE_REC(bprev, int32_t, r32, vrec, 24, kLanes * kRec)
   PE_REC(vpos, int32_t, r32, vrec, 28, kLanes * kRec)
+  PE_REC(vr0, V4, r32, vrec, 0, kLanes * kRec)   // vhdr vref vaux uses
+  PE_REC(vr1, V4, r32, vrec, 16, kLanes * kRec)  // slcnt bnext bprev vpos
   PE_REC(lo_buf, int32_t, r32, lrec, 0, kLanes * kRec)
   PE_REC(lo_spec, uint32_t, r32, lrec, 4, kLanes * kRec)
   PE_REC(lo_acq, uint32_t, r32, lrec, 8, kLanes * kRec)
   PE_REC(lo_g, G4, r32, lrec, 16, kLanes * kRec)
+  PE_REC(lo_h, LowHead, r32, lrec, 0, kLanes * kRec)
   PE_REC(adirect, int32_t, r64, arec, 0, kLanes * kRec64)
   PE_REC(aslice, int32_t, r64, arec, 4, kLanes * kRec64)
   PE_REC(awrapped, uint8_t, r64, arec, 8, kLanes * kRec64)
@@ -140,6 +156,7 @@ struct Arena {
   PE_REC(arg_gb, int64_t, r64, arec, 24, kLanes * kRec64)
   PE_REC(arg_lb, int64_t, r64, arec, 32, kLanes * kRec64)
   PE_REC(arg_spec, uint32_t, r64, arec, 40, kLanes * kRec64)
+  PE_REC(ar0, V4, r64, arec, 0, kLanes * kRec64)
   PE_REC(lkind, uint8_t, r32, looprec, 0, kLanes * kRec)
   PE_REC(laxis, uint8_t, r32, looprec, 1, kLanes * kRec)
   PE_REC(ldim, int8_t, r32, looprec, 2, kLanes * kRec)
@@ -339,18 +356,21 @@ struct Cand {
     if (k == VK_ATOMIC) return a.vref()[v];
     return v;  // ARG / TOP
   }
-  PE_HD int32_t alloc_slot() {
+  // a new value slot, written whole: header, vref, vaux, use count; no
+  // slices, unlinked, no position
+  PE_HD int32_t alloc_slot(uint32_t hdr, int32_t ref, int32_t aux, int32_t uses) {
     if (nslots >= caps.V) {
       fail(PE_CAND_CAPACITY);
       return -1;
     }
     int32_t s = nslots++;
-    a.slcnt()[s] = 0;
-    a.uses()[s] = 0;
-    a.bnext()[s] = -1;
-    a.bprev()[s] = -1;
-    a.vpos()[s] = 0;
+    a.vr0()[s] = V4{(int32_t)hdr, ref, aux, uses};
+    a.vr1()[s] = V4{0, -1, -1, 0};
     return s;
+  }
+  PE_HD static uint32_t loop_hdr(bool tile, int32_t axis, int32_t dim) {
+    return (uint32_t)VK_LOOP | ((tile ? 1u : 0u) << 8) | ((uint32_t)(uint8_t)axis << 16) |
+           ((uint32_t)(uint8_t)(int8_t)dim << 24);
   }
   PE_HD int32_t alloc_loop() {
     if (nloops >= caps.L) {
@@ -439,21 +459,14 @@ struct Cand {
   PE_HD void init() {
     int32_t A = g.A, N = g.N;
     for (int32_t v = 0; v < A; ++v) {
-      a.vk()[v] = VK_ARG;
-      a.vref()[v] = v;
-      a.uses()[v] = g.init_uses[v];
-      a.slcnt()[v] = 0;
-      a.adirect()[v] = 0;
-      a.aslice()[v] = -1;
-      a.awrapped()[v] = 0;
+      a.vr0()[v] = V4{VK_ARG, v, 0, g.init_uses[v]};
+      a.vr1()[v] = V4{0, -1, -1, 0};
+      a.ar0()[v] = V4{0, -1, 0, 0};  // adirect, aslice, awrapped (+aspec0)
     }
     for (int32_t o = 0; o < N; ++o) {
       int32_t v = A + o;
-      a.vk()[v] = VK_TOP;
-      a.vref()[v] = o;
-      a.uses()[v] = g.init_uses[v];
-      a.slcnt()[v] = 0;
-      a.vpos()[v] = 2 * o;
+      a.vr0()[v] = V4{VK_TOP, o, 0, g.init_uses[v]};
+      a.vr1()[v] = V4{0, -1, -1, 2 * o};
       a.pos()[2 * o] = v;
       a.pos()[2 * o + 1] = -1;
     }
@@ -492,21 +505,14 @@ struct Cand {
     if (g.amod((uint32_t)g.shape(v)[dim], axis) != 0) return false;
     if (carries(v)) return false;
     int32_t l = alloc_loop();
-    int32_t ls = alloc_slot();
-    int32_t s = alloc_slot();
+    int32_t ls = l < 0 ? -1 : alloc_slot(loop_hdr(true, axis, dim), l, 0, a.uses()[v]);
+    int32_t s = ls < 0 ? -1 : alloc_slot(VK_SLICE, v, dim | (l << 3), 1);  // used by the yield
     if (bad()) return false;
     a.lkind()[l] = LK_TILE;
     a.laxis()[l] = (uint8_t)axis;
     a.ldim()[l] = (int8_t)dim;
     a.ltype()[l] = v;
     a.lyield()[l] = s;
-    a.vref()[ls] = l;
-    mark_loop_value(ls, l);
-    a.uses()[ls] = a.uses()[v];
-    a.vk()[s] = VK_SLICE;
-    a.vref()[s] = v;
-    a.vaux()[s] = dim | (l << 3);
-    a.uses()[s] = 1;  // the loop yield
     body_append(l, s);
     push_pending(s);
     a.uses()[v] = 1;  // the slice
@@ -604,18 +610,14 @@ struct Cand {
     int32_t rd = g.cls_rdim[gc];
     int32_t lv0 = p.drive;
     bool extend = !contracting && a.uses()[lv0] == 1;
-    int32_t f = alloc_slot();
     int32_t l = extend ? a.vref()[lv0] : alloc_loop();
+    int32_t f = l < 0 ? -1 : alloc_slot(VK_LOCAL, o, (contracting ? 0 : rd + 1) | (l << 3), 1);
     if (bad()) return;
     if (!extend) {
       a.lkind()[l] = contracting ? LK_SUM : LK_TILE;
       a.laxis()[l] = (uint8_t)p.axis;
       a.ldim()[l] = (int8_t)(contracting ? -1 : rd);
     }
-    a.vk()[f] = VK_LOCAL;
-    a.vref()[f] = o;
-    a.vaux()[f] = (contracting ? 0 : rd + 1) | (l << 3);
-    a.uses()[f] = 1;  // yielded
     // slice cache: members of one class reference at most its member count
     int32_t cache_u[8], cache_d[8], cache_s[8];
     int32_t nc = 0;
@@ -644,14 +646,12 @@ struct Cand {
         }
       }
       if (sl < 0) {
-        sl = alloc_slot();
+        // a new slice takes this operand's use of u: u's count is
+        // unchanged (+1 slice, -1 operand slot), the slice has one use
+        sl = alloc_slot(VK_SLICE, u, d | (l << 3), 1);
         if (bad()) return;
-        a.vk()[sl] = VK_SLICE;
-        a.vref()[sl] = u;
-        a.vaux()[sl] = d | (l << 3);
         body_append(l, sl);
         push_pending(sl);
-        a.uses()[u]++;
         slice_created(u, d, p.axis);
         if (nc < 8) {
           cache_u[nc] = u;
@@ -659,10 +659,11 @@ struct Cand {
           cache_s[nc] = sl;
           nc++;
         }
+      } else {
+        a.uses()[u]--;
+        a.uses()[sl]++;
       }
       a.opnd()[ps] = sl;
-      a.uses()[u]--;
-      a.uses()[sl]++;
     }
     for (int32_t k = 0; k < n; ++k) {
       int32_t u = a.opnd()[base + k];
@@ -679,7 +680,7 @@ struct Cand {
     }
     int32_t xv = g.A + o;
     a.vref()[xv] = l;
-    mark_loop_value(xv, l);
+    a.vh()[xv] = loop_hdr(!contracting, p.axis, contracting ? -1 : rd);
     mark_users(xv);
   }
 
@@ -773,14 +774,11 @@ struct Cand {
                   }
                 }
                 if (sl < 0) {
-                  sl = alloc_slot();
+                  // takes this operand's use of w (count unchanged)
+                  sl = alloc_slot(VK_SLICE, w, dd | (l << 3), 1);
                   if (bad()) return;
-                  a.vk()[sl] = VK_SLICE;
-                  a.vref()[sl] = w;
-                  a.vaux()[sl] = dd | (l << 3);
                   body_insert_before(l, s, sl);
                   push_pending(sl);
-                  a.uses()[w]++;
                   slice_created(w, dd, sz_axis);
                   if (nc < 8) {
                     cache_u[nc] = w;
@@ -788,10 +786,11 @@ struct Cand {
                     cache_s[nc] = sl;
                     nc++;
                   }
+                } else {
+                  a.uses()[w]--;
+                  a.uses()[sl]++;
                 }
                 a.opnd()[pb + k] = sl;
-                a.uses()[w]--;
-                a.uses()[sl]++;
               }
             }
             for (int32_t k = 0; k < pn; ++k) {
@@ -844,11 +843,8 @@ struct Cand {
   PE_HD void wrap() {
     for (int32_t x = 0; x < g.A; ++x) {
       if (a.adirect()[x] == 0 || a.slcnt()[x] != 0 || a.awrapped()[x]) continue;
-      int32_t t = alloc_slot();
+      int32_t t = alloc_slot(VK_ATOMIC, x, 0, a.uses()[x]);
       if (bad()) return;
-      a.vk()[t] = VK_ATOMIC;
-      a.vref()[t] = x;
-      a.uses()[t] = a.uses()[x];
       replace_uses(x, t);
       a.uses()[x] = 1;
       a.awrapped()[x] = 1;
@@ -955,17 +951,21 @@ struct Cand {
   }
   PE_HD Low load(int32_t v) const {
     Low w;
-    w.buf = a.lo_buf()[v];
-    w.spec = a.lo_spec()[v];
-    w.acq = a.lo_acq()[v];
+    LowHead h = a.lo_h()[v];
+    w.buf = h.buf;
+    w.spec = h.spec;
+    w.acq = h.acq;
     G4 gg = a.lo_g()[v];
     for (int d = 0; d < kMaxRank; ++d) w.g[d] = gg.v[d];
     return w;
   }
   PE_HD void store(int32_t v, const Low& w) {
-    a.lo_buf()[v] = w.buf;
-    a.lo_spec()[v] = w.spec;
-    a.lo_acq()[v] = w.acq;
+    LowHead h;
+    h.buf = w.buf;
+    h.spec = w.spec;
+    h.acq = w.acq;
+    h.pad = 0;
+    a.lo_h()[v] = h;
     G4 gg;
     for (int d = 0; d < kMaxRank; ++d) gg.v[d] = w.g[d];
     a.lo_g()[v] = gg;
