@@ -95,6 +95,9 @@ struct alignas(16) G4 {
 struct alignas(16) V4 {
   int32_t x, y, z, w;
 };
+struct alignas(16) I64x2 {
+  int64_t x, y;
+};
 // first half of a LowRec (buf, spec, acq, 0): written and read as one
 // 16-byte access so the record's 32-byte sector is always written whole
 struct alignas(16) LowHead {
@@ -164,6 +167,8 @@ struct Arena {
   PE_REC(ltail, int32_t, r32, looprec, 8, kLanes * kRec)
   PE_REC(lyield, int32_t, r32, looprec, 12, kLanes * kRec)
   PE_REC(ltype, int32_t, r32, looprec, 16, kLanes * kRec)
+  PE_REC(lq0, V4, r32, looprec, 0, kLanes * kRec)   // kind|axis|dim, head, tail, yield
+  PE_REC(lq1, V4, r32, looprec, 16, kLanes * kRec)  // result type
   PE_REC(em_head, int32_t, r64, emrec, 0, kLanes * kRec64)
   PE_REC(em_op0, int32_t, r64, emrec, 4, kLanes * kRec64)
   PE_REC(em_last, int32_t, r64, emrec, 8, kLanes * kRec64)
@@ -173,6 +178,10 @@ struct Arena {
   PE_REC(em_gb, int64_t, r64, emrec, 32, kLanes * kRec64)
   PE_REC(em_blb, int64_t, r64, emrec, 40, kLanes * kRec64)
   PE_REC(em_spec, uint32_t, r64, emrec, 48, kLanes * kRec64)
+  PE_REC(em_q0, V4, r64, emrec, 0, kLanes * kRec64)      // head op0 last ooff
+  PE_REC(em_q1, I64x2, r64, emrec, 16, kLanes * kRec64)  // local bytes, delta
+  PE_REC(em_q2, I64x2, r64, emrec, 32, kLanes * kRec64)  // final gb, lb
+  PE_REC(em_q3, V4, r64, emrec, 48, kLanes * kRec64)     // final spec
   PE_REC(opnd, int32_t, b4, opnd, 0, kLanes * 4)
   PE_REC(pos, int32_t, b4, pos, 0, kLanes * 4)
   PE_REC(fs, int32_t, b4, fs, 0, kLanes * 4)
@@ -372,14 +381,16 @@ struct Cand {
     return (uint32_t)VK_LOOP | ((tile ? 1u : 0u) << 8) | ((uint32_t)(uint8_t)axis << 16) |
            ((uint32_t)(uint8_t)(int8_t)dim << 24);
   }
-  PE_HD int32_t alloc_loop() {
+  // a new loop record, written whole: kind, axis, dim (-1 for sum loops),
+  // empty body, no yield yet, result type
+  PE_HD int32_t alloc_loop(int32_t kind, int32_t axis, int32_t dim, int32_t type) {
     if (nloops >= caps.L) {
       fail(PE_CAND_CAPACITY);
       return -1;
     }
     int32_t l = nloops++;
-    a.lhead()[l] = -1;
-    a.ltail()[l] = -1;
+    a.lq0()[l] = V4{kind | (axis << 8) | ((int32_t)(uint8_t)(int8_t)dim << 16), -1, -1, -1};
+    a.lq1()[l] = V4{type, 0, 0, 0};
     return l;
   }
   PE_HD void body_append(int32_t l, int32_t s) {
@@ -504,14 +515,10 @@ struct Cand {
     if (dim < 0 || dim >= g.vrank[v]) return false;
     if (g.amod((uint32_t)g.shape(v)[dim], axis) != 0) return false;
     if (carries(v)) return false;
-    int32_t l = alloc_loop();
+    int32_t l = alloc_loop(LK_TILE, axis, dim, v);
     int32_t ls = l < 0 ? -1 : alloc_slot(loop_hdr(true, axis, dim), l, 0, a.uses()[v]);
     int32_t s = ls < 0 ? -1 : alloc_slot(VK_SLICE, v, dim | (l << 3), 1);  // used by the yield
     if (bad()) return false;
-    a.lkind()[l] = LK_TILE;
-    a.laxis()[l] = (uint8_t)axis;
-    a.ldim()[l] = (int8_t)dim;
-    a.ltype()[l] = v;
     a.lyield()[l] = s;
     body_append(l, s);
     push_pending(s);
@@ -610,14 +617,11 @@ struct Cand {
     int32_t rd = g.cls_rdim[gc];
     int32_t lv0 = p.drive;
     bool extend = !contracting && a.uses()[lv0] == 1;
-    int32_t l = extend ? a.vref()[lv0] : alloc_loop();
+    int32_t l = extend ? a.vref()[lv0]
+                       : alloc_loop(contracting ? LK_SUM : LK_TILE, p.axis, contracting ? -1 : rd,
+                                    g.A + o);
     int32_t f = l < 0 ? -1 : alloc_slot(VK_LOCAL, o, (contracting ? 0 : rd + 1) | (l << 3), 1);
     if (bad()) return;
-    if (!extend) {
-      a.lkind()[l] = contracting ? LK_SUM : LK_TILE;
-      a.laxis()[l] = (uint8_t)p.axis;
-      a.ldim()[l] = (int8_t)(contracting ? -1 : rd);
-    }
     // slice cache: members of one class reference at most its member count
     int32_t cache_u[8], cache_d[8], cache_s[8];
     int32_t nc = 0;
@@ -981,27 +985,26 @@ struct Cand {
       a.arg_lb()[buf] = lb;
       a.arg_spec()[buf] = w.spec;
     } else {
-      a.em_gb()[buf - g.A] = gb;
-      a.em_blb()[buf - g.A] = lb;
-      a.em_spec()[buf - g.A] = w.spec;
+      a.em_q2()[buf - g.A] = I64x2{gb, lb};
+      a.em_q3()[buf - g.A] = V4{(int32_t)w.spec, 0, 0, 0};
     }
   }
-  // opens an SPMD op; operands appended with add_operand
-  PE_HD int32_t new_op(int32_t kind, int32_t axis, int32_t dim, int32_t nopnd) {
+  // opens an SPMD op (first operand op0 or -1, local result bytes lb; the
+  // record's first 32 bytes are written whole); operands are then appended
+  // with add_operand
+  PE_HD int32_t new_op(int32_t kind, int32_t axis, int32_t dim, int32_t nopnd, int32_t op0,
+                       int64_t lb) {
     if (nem >= caps.EM || neo + nopnd > caps.EO) {
       fail(PE_CAND_CAPACITY);
       return -1;
     }
     int32_t j = nem++;
-    a.em_head()[j] = kind | ((axis + 1) << 8) | ((dim + 1) << 12) | (nopnd << 16);
-    a.em_ooff()[j] = neo;
-    a.em_last()[j] = j;
-    a.em_op0()[j] = -1;
+    a.em_q0()[j] = V4{kind | ((axis + 1) << 8) | ((dim + 1) << 12) | (nopnd << 16), op0, j, neo};
+    a.em_q1()[j] = I64x2{lb, 0};
     return j;
   }
   PE_HD void add_operand(int32_t j, int32_t buf) {
     if (tracing) a.em_opnd()[neo] = buf;
-    if (a.em_op0()[j] < 0) a.em_op0()[j] = buf;
     ++neo;
     // ops are emitted in order, so the current op is always the latest use
     if (buf >= g.A) a.em_last()[buf - g.A] = j;
@@ -1015,9 +1018,7 @@ struct Cand {
   // loop axis ax; updates the record in place.  One function for the three
   // so each emitting loop inlines a single copy (code size).
   PE_HD void emit_coll(Low& w, int32_t kind, int32_t ax, int d) {
-    int32_t j = new_op(kind, ax, d, 1);
-    if (j < 0) return;
-    add_operand(j, w.buf);
+    int32_t src = w.buf;
     if (kind == kAllGather) {
       w.spec = spec_set_axis(w.spec, d, 0);
       w.acq &= ~(1u << d);
@@ -1028,7 +1029,9 @@ struct Cand {
       w.acq |= 1u << d;
     }
     int64_t lb = 4 * local_elems(w);
-    a.em_lb()[j] = lb;
+    int32_t j = new_op(kind, ax, d, 1, src, lb);
+    if (j < 0) return;
+    add_operand(j, src);
     w.buf = g.A + j;
     register_type(w.buf, w, lb);
   }
@@ -1151,13 +1154,12 @@ struct Cand {
       uint32_t ax1 = spec_axis(r.spec, d);
       if (ax1) r.g[d] = (int32_t)(r.g[d] * asz(ax1 - 1));
     }
-    int32_t j = new_op(kind, -1, -1, n);
+    int64_t out_elems = local_elems(r);
+    int32_t j = new_op(kind, -1, -1, n, n > 0 ? in0.buf : -1, 4 * out_elems);
     if (j < 0) return;
 #pragma unroll 1
     for (int32_t k = 0; k < n; ++k)
       add_operand(j, k == 0 ? in0.buf : k == 1 ? in1.buf : a.lo_buf()[a.opnd()[base + k]]);
-    int64_t out_elems = local_elems(r);
-    a.em_lb()[j] = 4 * out_elems;
     // flops on LOCAL operand shapes
     switch (kind) {
       case kDot: {
@@ -1375,7 +1377,7 @@ struct Cand {
     int64_t base = 0;
     for (int32_t x = 0; x < g.A; ++x) base += a.alb0()[x];
     if (result_buf >= g.A) a.em_last()[result_buf - g.A] = nem - 1;
-    for (int32_t j = 0; j <= nem; ++j) a.delta()[j] = 0;
+    a.delta()[nem] = 0;  // (new_op zeroed delta[0..nem))
     for (int32_t j = 0; j < nem; ++j) {
       a.delta()[j] += a.em_lb()[j];
       a.delta()[a.em_last()[j] + 1] -= a.em_lb()[j];
