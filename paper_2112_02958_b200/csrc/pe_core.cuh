@@ -622,8 +622,9 @@ struct Cand {
                                     g.A + o);
     int32_t f = l < 0 ? -1 : alloc_slot(VK_LOCAL, o, (contracting ? 0 : rd + 1) | (l << 3), 1);
     if (bad()) return;
-    // slice cache: members of one class reference at most its member count
-    int32_t cache_u[8], cache_d[8], cache_s[8];
+    // slice dedup per (operand, dim): a two-entry cache in registers, then
+    // a search over this op's earlier members (already rewritten to slices)
+    int32_t c0u = -1, c0d = 0, c0s = -1, c1u = -1, c1d = 0, c1s = -1;
     int32_t nc = 0;
     for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
       int32_t k = g.mem[m] >> 2, d = g.mem[m] & 3;
@@ -636,12 +637,10 @@ struct Cand {
         a.uses()[y]++;
         continue;
       }
-      int32_t sl = -1;
-      for (int32_t c = 0; c < nc; ++c)
-        if (cache_u[c] == u && cache_d[c] == d) sl = cache_s[c];
+      int32_t sl = c0u == u && c0d == d ? c0s : c1u == u && c1d == d ? c1s : -1;
       if (sl < 0) {
-        // linear search fallback for very wide concatenates
-        for (int32_t q = g.cls_moff[gc]; q < m && sl < 0 && nc >= 8; ++q) {
+        // search fallback once the cache is full
+        for (int32_t q = g.cls_moff[gc]; q < m && sl < 0 && nc >= 2; ++q) {
           int32_t k2 = g.mem[q] >> 2, d2 = g.mem[q] & 3;
           int32_t s2 = a.opnd()[base + k2];
           if (d2 == d && a.vk()[s2] == VK_SLICE && a.vref()[s2] == u &&
@@ -657,11 +656,16 @@ struct Cand {
         body_append(l, sl);
         push_pending(sl);
         slice_created(u, d, p.axis);
-        if (nc < 8) {
-          cache_u[nc] = u;
-          cache_d[nc] = d;
-          cache_s[nc] = sl;
-          nc++;
+        if (nc == 0) {
+          c0u = u;
+          c0d = d;
+          c0s = sl;
+          nc = 1;
+        } else if (nc == 1) {
+          c1u = u;
+          c1d = d;
+          c1s = sl;
+          nc = 2;
         }
       } else {
         a.uses()[u]--;
@@ -760,15 +764,13 @@ struct Cand {
           }
           if (go) {
             if (!simple) {
-              int32_t cache_u[8], cache_d[8], cache_s[8];
+              int32_t c0u = -1, c0d = 0, c0s = -1, c1u = -1, c1d = 0, c1s = -1;
               int32_t nc = 0;
               for (int32_t m = g.cls_moff[gc]; m < g.cls_moff[gc + 1]; ++m) {
                 int32_t k = g.mem[m] >> 2, dd = g.mem[m] & 3;
                 int32_t w = a.opnd()[pb + k];
-                int32_t sl = -1;
-                for (int32_t c = 0; c < nc; ++c)
-                  if (cache_u[c] == w && cache_d[c] == dd) sl = cache_s[c];
-                if (sl < 0 && nc >= 8) {
+                int32_t sl = c0u == w && c0d == dd ? c0s : c1u == w && c1d == dd ? c1s : -1;
+                if (sl < 0 && nc >= 2) {
                   for (int32_t q = g.cls_moff[gc]; q < m && sl < 0; ++q) {
                     int32_t k2 = g.mem[q] >> 2, d2 = g.mem[q] & 3;
                     int32_t s2 = a.opnd()[pb + k2];
@@ -784,11 +786,16 @@ struct Cand {
                   body_insert_before(l, s, sl);
                   push_pending(sl);
                   slice_created(w, dd, sz_axis);
-                  if (nc < 8) {
-                    cache_u[nc] = w;
-                    cache_d[nc] = dd;
-                    cache_s[nc] = sl;
-                    nc++;
+                  if (nc == 0) {
+                    c0u = w;
+                    c0d = dd;
+                    c0s = sl;
+                    nc = 1;
+                  } else if (nc == 1) {
+                    c1u = w;
+                    c1d = dd;
+                    c1s = sl;
+                    nc = 2;
                   }
                 } else {
                   a.uses()[w]--;
@@ -1077,16 +1084,16 @@ struct Cand {
     int32_t base = g.oopnd_off[o], n = g.oopnd_off[o + 1] - base;
     int32_t lax = l >= 0 ? (int32_t)a.laxis()[l] : -1;
     uint8_t kind = g.okind[o];
-    Low in0, in1;
+    // After materialisation every operand's record is in its LowRec (it
+    // is stored when a collective moved it), so the rest of the op re-reads
+    // the records instead of keeping them in (local-memory) temporaries; a
+    // repeated operand (mul(x, x)) thereby sees the record its last use
+    // stored, as in the reference.
 #pragma unroll 1
     for (int32_t k = 0; k < n; ++k) {
-      Low w = materialize(a.opnd()[base + k], lax);
+      materialize(a.opnd()[base + k], lax);
       if (bad()) return;
-      if (k == 0) in0 = w;
-      else if (k == 1) in1 = w;
     }
-    // a repeated operand (mul(x, x)) sees the record its first use stored
-    if (n > 1 && a.opnd()[base] == a.opnd()[base + 1]) in0 = in1;
     Low r;
     int32_t xv = g.A + o;
     int rank = g.vrank[xv];
@@ -1100,7 +1107,7 @@ struct Cand {
     r.buf = -1;
 #pragma unroll 1
     for (int32_t k = 0; k < n; ++k) {
-      Low w = k == 0 ? in0 : k == 1 ? in1 : load(a.opnd()[base + k]);
+      Low w = load(a.opnd()[base + k]);
       r.spec |= spec_pending(w.spec) << 16;
       if (kind == kConstant) continue;
       int wr = rank_of_spec(w.spec);
@@ -1155,14 +1162,14 @@ struct Cand {
       if (ax1) r.g[d] = (int32_t)(r.g[d] * asz(ax1 - 1));
     }
     int64_t out_elems = local_elems(r);
-    int32_t j = new_op(kind, -1, -1, n, n > 0 ? in0.buf : -1, 4 * out_elems);
+    int32_t j = new_op(kind, -1, -1, n, n > 0 ? a.lo_buf()[a.opnd()[base]] : -1, 4 * out_elems);
     if (j < 0) return;
 #pragma unroll 1
-    for (int32_t k = 0; k < n; ++k)
-      add_operand(j, k == 0 ? in0.buf : k == 1 ? in1.buf : a.lo_buf()[a.opnd()[base + k]]);
+    for (int32_t k = 0; k < n; ++k) add_operand(j, a.lo_buf()[a.opnd()[base + k]]);
     // flops on LOCAL operand shapes
     switch (kind) {
       case kDot: {
+        Low in0 = load(a.opnd()[base]), in1 = load(a.opnd()[base + 1]);
         int64_t f = 2 * local_elems(in0);
         int rr2 = rank_of_spec(in1.spec);
         for (int d = 0; d < rr2; ++d)
@@ -1175,7 +1182,7 @@ struct Cand {
         flops += out_elems;
         break;
       case kReduceSum: case kReduceMax:
-        flops += local_elems(in0);
+        flops += local_elems(load(a.opnd()[base]));
         break;
       default:
         break;
