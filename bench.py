@@ -281,7 +281,7 @@ def run_engine(args):
         import helpers as H
         if os.path.exists(H.ORACLE_SO):
             threads = os.cpu_count() or 1
-            n_cpu = 24 * threads  # ~10 s of reference CPU work on this path
+            n_cpu = 48 * threads  # ~12 s of reference CPU work on this path
             v_cpu, dt = cpu_reference(text, n_cpu, 30_000_000, threads)
             cpu = {"value": v_cpu, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"{n_cpu} rollouts of the bench workload ({dt:.1f} s)"}
