@@ -112,7 +112,7 @@ struct Layout {
   // byte offsets inside one group arena (kLanes candidates); record arrays
   // are interleaved [index][lane] at record granularity
   uint64_t vrec, lrec, arec, looprec, emrec;
-  uint64_t opnd, pos, fs, stk, seen, em_opnd, carry, lg, dirty;
+  uint64_t opnd, fs, stk, seen, em_opnd, carry, lg, dirty;
   uint64_t bytes;  // one group arena
 };
 
@@ -183,7 +183,6 @@ struct Arena {
   PE_REC(em_q2, I64x2, r64, emrec, 32, kLanes * kRec64)  // final gb, lb
   PE_REC(em_q3, V4, r64, emrec, 48, kLanes * kRec64)     // final spec
   PE_REC(opnd, int32_t, b4, opnd, 0, kLanes * 4)
-  PE_REC(pos, int32_t, b4, pos, 0, kLanes * 4)
   PE_REC(fs, int32_t, b4, fs, 0, kLanes * 4)
   PE_REC(stk, int32_t, b4, stk, 0, kLanes * 4)
   PE_REC(em_opnd, int32_t, b4, em_opnd, 0, kLanes * 4)
@@ -250,7 +249,6 @@ inline Layout relayout(const GraphView& g, const Caps& caps) {
   L.looprec = take(caps.L, kRec);
   L.emrec = take((int64_t)caps.EM + 1, kRec64);
   L.opnd = take(E, 4);
-  L.pos = take(2 * N, 4);
   L.fs = take(caps.FS, 4);
   L.stk = take(2 * N, 4);
   L.seen = take(N, 1);
@@ -408,9 +406,13 @@ struct Cand {
     if (p >= 0) a.bnext()[p] = s;
     else a.lhead()[l] = s;
   }
+  // Top-level order: even slot 2o is op o's own value
+  // A+o (absent once DEAD), odd slot 2o+1 the action loop tiled right
+  // after it, kept in vaux[A+o] (unused for top-level values; -1 = empty);
+  // negative codes are front-stack entries.
   PE_HD void set_pos(int32_t v, int32_t code) {
     a.vpos()[v] = code;
-    if (code >= 0) a.pos()[code] = v;
+    if (code >= 0) a.vaux()[g.A + (code >> 1)] = v;  // odd slots only
     else a.fs()[-code - 1] = v;
   }
   PE_HD void push_front(int32_t v) {
@@ -421,10 +423,11 @@ struct Cand {
     set_pos(v, -(nfs + 1));
     nfs++;
   }
+  // (callers mark v DEAD, which removes an even-slot value)
   PE_HD void clear_pos(int32_t v) {
     int32_t code = a.vpos()[v];
-    if (code >= 0) a.pos()[code] = -1;
-    else a.fs()[-code - 1] = -1;
+    if (code < 0) a.fs()[-code - 1] = -1;
+    else if (code & 1) a.vaux()[g.A + (code >> 1)] = -1;
   }
   // REF rewrite.cc:27-38 replace_uses: every operand occurrence of an
   // original value lives in one of its original operand slots.
@@ -476,10 +479,8 @@ struct Cand {
     }
     for (int32_t o = 0; o < N; ++o) {
       int32_t v = A + o;
-      a.vr0()[v] = V4{VK_TOP, o, 0, g.init_uses[v]};
+      a.vr0()[v] = V4{VK_TOP, o, -1, g.init_uses[v]};  // vaux: odd slot empty
       a.vr1()[v] = V4{0, -1, -1, 2 * o};
-      a.pos()[2 * o] = v;
-      a.pos()[2 * o + 1] = -1;
     }
     for (int32_t s = 0; s < g.E; ++s) a.opnd()[s] = g.oopnd[s];
     for (int32_t w = 0; w <= (A >> 5); ++w) a.carry()[w] = 0;
@@ -695,25 +696,49 @@ struct Cand {
   // REF propagate.cc:250-280: one in-order sweep over the top-level ops,
   // restricted to the ops whose operands changed (users are always later
   // in program order, so the sweep never has to look back).
+  //
+  // On the device the lanes that enter together step through the union of
+  // their dirty ops in lockstep: each iteration takes the warp-wide
+  // smallest next op, and the lanes holding it pull it together (same op,
+  // same rule tables, one code path) while the others wait.  Each lane
+  // still visits its own dirty ops in increasing order, so the result is
+  // the sequential sweep's.  A lane that fails keeps taking part with no
+  // op until every lane is done (the reduction needs all of them).
   PE_HD void forward() {
     int32_t nw = (g.N >> 5) + 1;
-    for (int32_t w = 0; w < nw; ++w) {
-      uint32_t bits;
-      while ((bits = a.dirty()[w]) != 0) {
-        int32_t b = pe_ctz(bits);
-        a.dirty()[w] = bits & (bits - 1);
-        int32_t o = (w << 5) + b;
-        if (a.vk()[g.A + o] != VK_TOP) continue;
-        if (!has_tiled_operand(o)) continue;
-        if (g.orule_err[o]) {
-          fail(PE_CAND_INTERNAL);
-          return;
-        }
-        Pull p = plan_pull(o);
-        if (!p.ok) continue;
-        pull(o, p);
-        if (bad()) return;
+    int32_t w = 0;
+    bool done = false;
+#ifdef __CUDA_ARCH__
+    const unsigned mask = __activemask();
+#endif
+    while (true) {
+      int32_t mine = INT32_MAX;
+      uint32_t bits = 0;
+      if (!done) {
+        while (w < nw && (bits = a.dirty()[w]) == 0) ++w;
+        if (w < nw) mine = (w << 5) + pe_ctz(bits);
+        else done = true;
       }
+#ifdef __CUDA_ARCH__
+      int32_t m = __reduce_min_sync(mask, mine);
+#else
+      int32_t m = mine;
+#endif
+      if (m == INT32_MAX) break;
+      if (mine != m) continue;
+      a.dirty()[w] = bits & (bits - 1);
+      int32_t o = m;
+      if (a.vk()[g.A + o] != VK_TOP) continue;
+      if (!has_tiled_operand(o)) continue;
+      if (g.orule_err[o]) {
+        fail(PE_CAND_INTERNAL);
+        done = true;
+        continue;
+      }
+      Pull p = plan_pull(o);
+      if (!p.ok) continue;
+      pull(o, p);
+      if (bad()) done = true;
     }
   }
 
@@ -821,6 +846,16 @@ struct Cand {
     }
   }
 
+  // Visits the top-level values in program order: the front stack (most
+  // recent first), then per op o its own value A+o (even slot, absent once
+  // DEAD) and the action loop tiled right after it (odd slot).
+  //
+  // The op walk is a loop of its own, entered by all lanes together after
+  // the front stack, so the lanes of a warp visit the same op in the same
+  // iteration (same kind, same code path, same graph data): a single merged
+  // loop over both sources offsets every lane by its front-stack length and
+  // measured 1.14M -> 0.81M cand/s.  The even/odd pair is a
+  // non-unrolled inner loop so f is inlined once for the op walk.
   template <typename F>
   PE_HD void for_top(F&& f) {
     for (int32_t i = nfs - 1; i >= 0; --i) {
@@ -830,9 +865,13 @@ struct Cand {
         if (bad()) return;
       }
     }
-    for (int32_t p = 0; p < 2 * g.N; ++p) {
-      int32_t v = a.pos()[p];
-      if (v >= 0) {
+    for (int32_t o = 0; o < g.N; ++o) {
+      V4 q = a.vr0()[g.A + o];  // header, vref, vaux = odd-slot occupant
+      int32_t even = (q.x & 0xFF) != VK_DEAD ? g.A + o : -1;
+#pragma unroll 1
+      for (int32_t h = 0; h < 2; ++h) {
+        int32_t v = h == 0 ? even : q.z;
+        if (v < 0) continue;
         f(v);
         if (bad()) return;
       }
@@ -1007,7 +1046,7 @@ struct Cand {
     }
     int32_t j = nem++;
     a.em_q0()[j] = V4{kind | ((axis + 1) << 8) | ((dim + 1) << 12) | (nopnd << 16), op0, j, neo};
-    a.em_q1()[j] = I64x2{lb, 0};
+    a.em_q1()[j] = I64x2{lb, lb};  // liveness delta starts at +lb (def at j)
     return j;
   }
   PE_HD void add_operand(int32_t j, int32_t buf) {
@@ -1364,31 +1403,31 @@ struct Cand {
       r.ag_cnt[x] = 0;
       r.sbc_cnt[x] = 0;
     }
-    // collective_stats (REF spmd.cc:405-434) over final registered types
+    // One pass over the SPMD ops: collective_stats (REF spmd.cc:405-434)
+    // over final registered types, and the liveness deltas (SURVEY.md
+    // B.5.1): new_op set delta[j] = +lb[j]; here -lb[j] lands after the
+    // buffer's last use.
+    if (result_buf >= g.A) a.em_last()[result_buf - g.A] = nem - 1;
+    a.delta()[nem] = 0;
     for (int32_t j = 0; j < nem; ++j) {
-      int32_t h = a.em_head()[j];
-      int32_t kind = h & 0xFF, ax = ((h >> 8) & 0xF) - 1;
+      V4 q = a.em_q0()[j];  // head, op0, last, operand offset
+      int64_t lb = a.em_lb()[j];
+      int32_t kind = q.x & 0xFF, ax = ((q.x >> 8) & 0xF) - 1;
       if (kind == kAllReduce) {
-        int32_t b = a.em_op0()[j];
+        int32_t b = q.y;
         r.ar_cnt[ax]++;
         r.ar_bytes[ax] += b < g.A ? a.arg_gb()[b] : a.em_gb()[b - g.A];
       } else if (kind == kAllGather) {
-        int32_t b = a.em_op0()[j];
+        int32_t b = q.y;
         r.ag_cnt[ax]++;
         r.ag_bytes[ax] += (b < g.A ? a.arg_lb()[b] : a.em_blb()[b - g.A]) * (asz(ax) - 1);
       } else if (kind == kSliceByCoord) {
         r.sbc_cnt[ax]++;
       }
+      a.delta()[q.z + 1] -= lb;
     }
-    // peak liveness
     int64_t base = 0;
     for (int32_t x = 0; x < g.A; ++x) base += a.alb0()[x];
-    if (result_buf >= g.A) a.em_last()[result_buf - g.A] = nem - 1;
-    a.delta()[nem] = 0;  // (new_op zeroed delta[0..nem))
-    for (int32_t j = 0; j < nem; ++j) {
-      a.delta()[j] += a.em_lb()[j];
-      a.delta()[a.em_last()[j] + 1] -= a.em_lb()[j];
-    }
     int64_t run = 0, best = 0;
     for (int32_t j = 0; j < nem; ++j) {
       run += a.delta()[j];
