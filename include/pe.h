@@ -128,6 +128,17 @@ typedef struct pe_search_config {
   uint32_t scoped_only;    /* 1 = worklist holds only arguments with a scope
                               (parameters); unscoped inputs are left to manual
                               decisions, as automap's batch axis (PAPER §2.2) */
+  uint32_t resurface_stuck; /* 1 = stuck nodes resurface into the worklist
+                              (SPEC Worklist: "plus stuck nodes resurfaced by
+                              propagation"; REF propagate.cc:412-454): after
+                              every decision, the ops of the fixpoint's stuck
+                              list join the worklist in discovery order, once
+                              each, as TileValue(op result) entries.  Their
+                              ordinals follow the static entries:
+                              (n_entries + op) * 4 * n_auto + dim * n_auto + ai.
+                              Rollouts enumerate legal actions in worklist
+                              order (static entries, then resurfaced ones in
+                              discovery order).  0 (default) = static worklist */
 } pe_search_config;
 
 void pe_default_cost_params(pe_cost_params* out);

@@ -398,11 +398,47 @@ uint64_t splitmix_next(uint64_t& st) {
   return z ^ (z >> 31);
 }
 
-uint32_t num_ordinals(const Setup& s) {
-  return (uint32_t)(s.entries.size() * PE_MAX_RANK * s.auto_axes.size());
+// Stuck resurfacing (pe.h resurface_stuck; SPEC Worklist "plus stuck nodes
+// resurfaced by propagation", "deterministic order (argument order, then
+// stuck discovery order)"): after every decision the ops of the fixpoint's
+// stuck list (REF propagate.cc:412-454, in its order) join the worklist
+// once each.
+struct Resurfaced {
+  std::vector<int> ops;     // op indices in discovery order
+  std::vector<char> seen;   // per op
+};
+
+void resurface(const Setup& s, const std::vector<StuckNode>& stuck, Resurfaced& R) {
+  if (!s.cfg.resurface_stuck) return;
+  if (R.seen.empty()) R.seen.assign(s.root.ops.size(), 0);
+  for (const StuckNode& sn : stuck) {
+    auto it = s.op_index.find(sn.op_id);
+    if (it == s.op_index.end() || R.seen[it->second]) continue;
+    R.seen[it->second] = 1;
+    R.ops.push_back(it->second);
+  }
 }
 
-std::vector<uint32_t> legal_ordinals(const Setup& s, const Program& p) {
+uint32_t num_ordinals(const Setup& s) {
+  size_t entries = s.entries.size() + (s.cfg.resurface_stuck ? s.root.ops.size() : 0);
+  return (uint32_t)(entries * PE_MAX_RANK * s.auto_axes.size());
+}
+
+// TileValue(op result, d, axis) is legal when apply_tile_action would
+// accept it (REF rewrite.cc:53-75): the value exists at top level, the dim
+// divides, and it carries no tiling yet.
+bool op_value_legal(const Setup& s, const Program& p, int o, int d, int axis) {
+  const Operation& op0 = s.root.ops[o];
+  if (d >= op0.result_type.rank()) return false;
+  if (op0.result_type.shape[d] % s.root.mesh.axes[axis].size != 0) return false;
+  bool exists = false;
+  for (const Operation& op : p.ops)
+    if (op.id == op0.id) exists = true;
+  return exists && !carries_tiling(p, op0.id);
+}
+
+std::vector<uint32_t> legal_ordinals(const Setup& s, const Program& p,
+                                     const Resurfaced& R = Resurfaced()) {
   std::vector<uint32_t> out;
   std::vector<char> carries(s.root.args.size());
   for (size_t a = 0; a < s.root.args.size(); ++a) carries[a] = carries_tiling(p, s.root.args[a].id);
@@ -422,6 +458,13 @@ std::vector<uint32_t> legal_ordinals(const Setup& s, const Program& p) {
         }
         if (ok) out.push_back((uint32_t)((e * PE_MAX_RANK + d) * na + ai));
       }
+  // resurfaced stuck nodes, in discovery order
+  size_t E = s.entries.size();
+  for (int o : R.ops)
+    for (int d = 0; d < PE_MAX_RANK; ++d)
+      for (uint32_t ai = 0; ai < na; ++ai)
+        if (op_value_legal(s, p, o, d, s.auto_axes[ai]))
+          out.push_back((uint32_t)(((E + o) * PE_MAX_RANK + d) * na + ai));
   return out;
 }
 
@@ -433,6 +476,11 @@ pe_action ordinal_action(const Setup& s, uint32_t ord) {
   uint32_t e = ord / na / PE_MAX_RANK;
   a.axis = (uint8_t)s.auto_axes[ai];
   a.dim = (uint8_t)d;
+  if (e >= s.entries.size()) {  // resurfaced stuck node: TileValue(op result)
+    a.kind = PE_ACT_TILE;
+    a.value = (uint32_t)(s.root.args.size() + (e - s.entries.size()));
+    return a;
+  }
   a.kind = s.cfg.group_scopes ? PE_ACT_TILE_GROUP : PE_ACT_TILE;
   a.value = (uint32_t)s.entry_val[e];
   return a;
@@ -444,6 +492,7 @@ void rollout_one(const Setup& s, const pe_action* prefix, uint32_t n_prefix, uin
   r.fail_step = -1;
   Program p = s.root;
   std::vector<StuckNode> stuck;
+  Resurfaced R;
   uint32_t nacts = 0;
   uint32_t maxd = s.cfg.max_decisions;
   uint32_t nwords = (num_ordinals(s) + 63) / 64;
@@ -461,12 +510,13 @@ void rollout_one(const Setup& s, const pe_action* prefix, uint32_t n_prefix, uin
         terminal = true;
         break;
       }
+      resurface(s, stuck, R);
       if (nacts < maxd) acts_out[nacts] = prefix[k];
       ++nacts;
       r.n_steps++;
     }
     if (r.status == PE_CAND_OK) {
-      std::vector<uint32_t> legal = legal_ordinals(s, p);
+      std::vector<uint32_t> legal = legal_ordinals(s, p, R);
       if (legal_out)
         for (uint32_t o : legal) legal_out[o / 64] |= 1ull << (o % 64);
       uint64_t st = seed;
@@ -482,10 +532,11 @@ void rollout_one(const Setup& s, const pe_action* prefix, uint32_t n_prefix, uin
           r.fail_step = (int32_t)nacts;
           break;
         }
+        resurface(s, stuck, R);
         if (nacts < maxd) acts_out[nacts] = a;
         ++nacts;
         r.n_steps++;
-        legal = legal_ordinals(s, p);
+        legal = legal_ordinals(s, p, R);
       }
     }
     *n_out = std::min(nacts, maxd);
@@ -635,14 +686,17 @@ int oracle_legal(const char* pir, size_t len, const pe_search_config* cfg, const
   if (rc) return rc;
   Program p = s.root;
   std::vector<StuckNode> stuck;
+  Resurfaced R;
   try {
-    for (uint32_t k = 0; k < n; ++k)
+    for (uint32_t k = 0; k < n; ++k) {
       if (!apply_action(s, p, stuck, acts[k])) return 3;
+      resurface(s, stuck, R);
+    }
   } catch (const Error& e) {
     if (err) std::snprintf(err, errcap, "%s", e.what());
     return 70;
   }
-  std::vector<uint32_t> l = legal_ordinals(s, p);
+  std::vector<uint32_t> l = legal_ordinals(s, p, R);
   *n_out = (uint32_t)l.size();
   for (uint32_t i = 0; i < l.size() && i < cap; ++i) ords_out[i] = l[i];
   return 0;

@@ -78,7 +78,8 @@ class PeSearchConfig(C.Structure):
     _fields_ = [("auto_axes_mask", C.c_uint32), ("max_decisions", C.c_uint32),
                 ("group_scopes", C.c_uint32), ("episodes", C.c_uint32),
                 ("seed", C.c_uint64), ("uct_c", C.c_double),
-                ("leaf_batch", C.c_uint32), ("scoped_only", C.c_uint32)]
+                ("leaf_batch", C.c_uint32), ("scoped_only", C.c_uint32),
+                ("resurface_stuck", C.c_uint32)]
 
 
 PE_PLAN_MAX_ACTIONS = 64
@@ -110,7 +111,7 @@ def default_cost_params() -> PeCostParams:
 
 
 def default_search_config(**kw) -> PeSearchConfig:
-    c = PeSearchConfig(0xFFFFFFFF, 32, 1, 500, 0, 1.414, 256, 0)
+    c = PeSearchConfig(0xFFFFFFFF, 32, 1, 500, 0, 1.414, 256, 0, 0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c

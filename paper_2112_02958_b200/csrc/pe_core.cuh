@@ -112,6 +112,7 @@ struct Layout {
   // byte offsets inside one group arena (kLanes candidates); record arrays
   // are interleaved [index][lane] at record granularity
   uint64_t vrec, lrec, arec, looprec, emrec;
+  uint64_t rs, rsb;
   uint64_t opnd, fs, stk, seen, em_opnd, carry, lg, dirty;
   uint64_t bytes;  // one group arena
 };
@@ -189,6 +190,8 @@ struct Arena {
   PE_REC(lg, int32_t, b4, lg, 0, kLanes * 4)
   PE_REC(carry, uint32_t, b4, carry, 0, kLanes * 4)
   PE_REC(dirty, uint32_t, b4, dirty, 0, kLanes * 4)
+  PE_REC(rs, int32_t, b4, rs, 0, kLanes * 4)      // resurfaced ops, discovery order
+  PE_REC(rsb, uint32_t, b4, rsb, 0, kLanes * 4)   // resurfaced-op bitmap
   PE_REC(seen, uint8_t, b1, seen, 0, kLanes * 1)
 #undef PE_REC
 };
@@ -254,8 +257,11 @@ inline Layout relayout(const GraphView& g, const Caps& caps) {
   L.seen = take(N, 1);
   L.em_opnd = take(caps.EO, 4);
   L.carry = take(A / 32 + 1, 4);
-  L.lg = take(g.n_ord, 4);
+  // legal list: static ordinals, plus every resurfaced op's when enabled
+  L.lg = take(g.n_ord + (g.resurface ? N * kMaxRank * g.n_auto : 0), 4);
   L.dirty = take(N / 32 + 1, 4);
+  L.rs = take(g.resurface ? N : 0, 4);
+  L.rsb = take(g.resurface ? N / 32 + 1 : 0, 4);
   L.bytes = align128(o);
   return L;
 }
@@ -308,6 +314,7 @@ struct Cand {
   int32_t nslots, nloops, nfs, nem, neo, nstk;
   int32_t result_ref;
   int32_t pend;  // head of the pending-slice list (linked through vpos)
+  int32_t nrs;   // resurfaced stuck ops (g.resurface)
   int32_t status;
   int64_t flops;
   int32_t result_buf;
@@ -485,6 +492,9 @@ struct Cand {
     for (int32_t s = 0; s < g.E; ++s) a.opnd()[s] = g.oopnd[s];
     for (int32_t w = 0; w <= (A >> 5); ++w) a.carry()[w] = 0;
     for (int32_t w = 0; w <= (N >> 5); ++w) a.dirty()[w] = 0;
+    if (g.resurface)
+      for (int32_t w = 0; w <= (N >> 5); ++w) a.rsb()[w] = 0;
+    nrs = 0;
     pend = -1;
     nslots = A + N;
     nloops = 0;
@@ -1577,6 +1587,24 @@ struct Cand {
   // legal_actions (SPEC search module): a TileValue ordinal is legal when at
   // least one statically legal member does not carry tiling yet
   // (REF rewrite.cc:75-76).  Fills a.lg with the legal ordinals in order.
+  // Stuck resurfacing (pe.h resurface_stuck; SPEC Worklist): the ops of
+  // the current fixpoint's stuck list (REF propagate.cc:412-454, discovery
+  // order) join the worklist once each.  Called at every decision boundary.
+  PE_HD void resurface_update() {
+    analyze();
+    if (bad()) return;
+    for (int32_t i = 0; i < nstk; ++i) {
+      int32_t o = a.stk()[2 * i];
+      uint32_t bit = 1u << (o & 31);
+      if (a.rsb()[o >> 5] & bit) continue;
+      a.rsb()[o >> 5] |= bit;
+      a.rs()[nrs++] = o;
+    }
+  }
+  // Legal TileValue ordinals in worklist order (SPEC legal_actions): the
+  // static entries, then the resurfaced ops in discovery order; a
+  // resurfaced op is legal as apply_tile_action would accept it (still at
+  // top level and carrying no tiling: TOP without slices; the dim divides).
   PE_HD int32_t build_legal() {
     int32_t n = 0;
     for (int32_t o = 0; o < g.n_ord; ++o) {
@@ -1588,6 +1616,15 @@ struct Cand {
         }
       }
     }
+    for (int32_t i = 0; i < nrs; ++i) {
+      int32_t o = a.rs()[i], v = g.A + o;
+      if (a.vk()[v] != VK_TOP || a.slcnt()[v] != 0) continue;
+      int32_t rank = g.vrank[v];
+      for (int32_t d = 0; d < rank; ++d)
+        for (int32_t ai = 0; ai < g.n_auto; ++ai)
+          if (g.amod((uint32_t)g.shape(v)[d], g.auto_axes[ai]) == 0)
+            a.lg()[n++] = ((g.n_entries + o) * kMaxRank + d) * g.n_auto + ai;
+    }
     return n;
   }
   PE_HD pe_action ordinal_action(int32_t ord) const {
@@ -1597,6 +1634,11 @@ struct Cand {
     x.axis = (uint8_t)g.auto_axes[ai];
     x.dim = (uint8_t)d;
     x.pad = 0;
+    if (e >= g.n_entries) {  // resurfaced stuck op: TileValue(op result)
+      x.kind = PE_ACT_TILE;
+      x.value = (uint32_t)(g.A + (e - g.n_entries));
+      return x;
+    }
     x.kind = g.entries_are_groups ? PE_ACT_TILE_GROUP : PE_ACT_TILE;
     x.value = (uint32_t)g.ent_val[e];
     return x;
@@ -1622,7 +1664,17 @@ struct Cand {
     bool propagated = false, terminal = false;
     if (legal_out)
       for (int32_t w = 0; w < legal_words; ++w) legal_out[w] = 0;
+    // resurfacing runs at decision boundaries: before the next decision of
+    // the prefix (tiles an INFER_REST expansion inferred belong to it) and
+    // before enumerating legal actions -- i.e. after every whole decision,
+    // as the oracle does after each apply_action
+    bool rs_due = false;
     for (int32_t k = 0; k < np; ++k) {
+      if (rs_due && !(prefix[k].pad & PE_ACT_FLAG_INFERRED)) {
+        resurface_update();
+        rs_due = false;
+        if (bad()) break;
+      }
       if (prefix[k].kind == PE_ACT_STOP) {
         terminal = true;
         break;
@@ -1651,10 +1703,12 @@ struct Cand {
       propagate();
       propagated = true;
       if (bad()) break;
+      rs_due = g.resurface != 0;
       if (nacts < maxd) acts_out[nacts] = prefix[k];
       ++nacts;
       if (!(prefix[k].pad & PE_ACT_FLAG_INFERRED)) ++steps;
     }
+    if (rs_due && !bad() && status == PE_CAND_OK) resurface_update();
     if (!bad() && status == PE_CAND_OK) {
       if (legal_out) {
         int32_t nl = build_legal();
@@ -1681,6 +1735,10 @@ struct Cand {
         propagate();
         propagated = true;
         if (bad()) break;
+        if (g.resurface) {
+          resurface_update();
+          if (bad()) break;
+        }
         if (nacts < maxd) acts_out[nacts] = x;
         ++nacts;
         ++steps;

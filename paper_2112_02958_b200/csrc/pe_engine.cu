@@ -303,7 +303,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   const pe::HostGraph& g = graph->g;
   // worklist entries (SPEC build_worklist: arguments, optionally grouped)
   e->wl = pe::build_worklist(g, e->cfg.auto_axes_mask, e->cfg.group_scopes != 0,
-                             e->cfg.scoped_only != 0);
+                             e->cfg.scoped_only != 0, e->cfg.resurface_stuck != 0);
   const pe::Worklist& w = e->wl;
   e->n_ordinals = (uint32_t)w.n_ordinals();
 
@@ -446,6 +446,11 @@ pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* 
   out->axis = (uint8_t)w.auto_axes[ai];
   out->dim = (uint8_t)d;
   out->pad = 0;
+  if ((int32_t)ent >= w.n_entries()) {  // resurfaced stuck op: TileValue(op result)
+    out->kind = PE_ACT_TILE;
+    out->value = (uint32_t)(e->graph->g.args.size() + (ent - (uint32_t)w.n_entries()));
+    return PE_OK;
+  }
   out->kind = w.groups ? PE_ACT_TILE_GROUP : PE_ACT_TILE;
   out->value = (uint32_t)w.ent_val[ent];
   return PE_OK;

@@ -816,9 +816,11 @@ GraphView HostGraph::host_view() const {
 }
 
 Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes,
-                        bool scoped_only) {
+                        bool scoped_only, bool resurface) {
   Worklist w;
   w.groups = group_scopes;
+  w.resurface = resurface;
+  w.n_ops = (int32_t)g.ops.size();
   for (int32_t a = 0; a < (int32_t)g.axis_names.size(); ++a)
     if (auto_axes_mask & (1u << a)) w.auto_axes.push_back(a);
   w.grp_off.push_back(0);
@@ -868,7 +870,8 @@ void attach_worklist(GraphView& v, const Worklist& w) {
   v.n_groups = (int32_t)w.grp_off.size() - 1;
   v.grp_off = w.grp_off.data();
   v.grp_mem = w.grp_mem.data();
-  v.n_ord = w.n_ordinals();
+  v.n_ord = w.n_static_ordinals();
+  v.resurface = w.resurface ? 1 : 0;
   v.ord_off = w.ord_off.data();
   v.ord_mem = w.ord_mem.data();
 }

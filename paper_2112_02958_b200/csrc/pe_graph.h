@@ -81,13 +81,21 @@ struct Worklist {
   std::vector<int32_t> auto_axes, ent_off, ent_mem, grp_off, grp_mem, ord_off, ord_mem;
   std::vector<int32_t> ent_val;  // action value per entry: group index or argument
   bool groups = true;
+  bool resurface = false;  // stuck resurfacing (pe.h resurface_stuck)
+  int32_t n_ops = 0;
   int32_t n_entries() const { return (int32_t)ent_off.size() - 1; }
-  int32_t n_ordinals() const {
+  // ordinals of the static entries (arguments / groups)
+  int32_t n_static_ordinals() const {
     return n_entries() * kMaxRank * (int32_t)auto_axes.size();
+  }
+  // all ordinals: static entries, then one block per op when stuck nodes
+  // can resurface
+  int32_t n_ordinals() const {
+    return (n_entries() + (resurface ? n_ops : 0)) * kMaxRank * (int32_t)auto_axes.size();
   }
 };
 Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes,
-                        bool scoped_only = false);
+                        bool scoped_only = false, bool resurface = false);
 // points the worklist fields of `v` at the (host) vectors of `w`
 void attach_worklist(GraphView& v, const Worklist& w);
 

@@ -108,7 +108,10 @@ struct GraphView {
   int32_t n_groups;
   const int32_t* grp_off;    // [n_groups+1]
   const int32_t* grp_mem;
-  // TileValue ordinals: statically legal members per ordinal
+  // stuck resurfacing (pe.h resurface_stuck): resurfaced op o's ordinals
+  // are ((n_entries + o) * kMaxRank + dim) * n_auto + ai
+  int32_t resurface;
+  // TileValue ordinals of the static entries: statically legal members
   int32_t n_ord;
   const int32_t* ord_off;    // [n_ord+1]
   const int32_t* ord_mem;

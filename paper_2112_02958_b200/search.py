@@ -137,6 +137,12 @@ def ordinal_actions(graph, cfg) -> list:
         for d in range(capi.PE_MAX_RANK):
             for ax in auto:
                 out.append(PeAction(val, d, ax, kind, 0))
+    if getattr(cfg, "resurface_stuck", 0):
+        # one block per op for stuck nodes that resurface: TileValue(op result)
+        for o in range(graph.n_ops):
+            for d in range(capi.PE_MAX_RANK):
+                for ax in auto:
+                    out.append(PeAction(graph.n_args + o, d, ax, capi.PE_ACT_TILE, 0))
     out.append(PeAction(0, 0, 0, capi.PE_ACT_STOP, 0))
     return out
 

@@ -55,7 +55,7 @@ int setup(Harness& h, const char* pir, size_t len, const pe_search_config* cfg,
   if (cp) h.cp = *cp;
   h.v = h.g.host_view();
   h.w = pe::build_worklist(h.g, h.cfg.auto_axes_mask, h.cfg.group_scopes != 0,
-                           h.cfg.scoped_only != 0);
+                           h.cfg.scoped_only != 0, h.cfg.resurface_stuck != 0);
   pe::attach_worklist(h.v, h.w);
   h.L = pe::make_layout(h.v);
   h.arena.assign(h.L.bytes, 0);
@@ -94,7 +94,7 @@ int harness_rollout_batch(const char* pir, size_t len, const pe_search_config* c
   if (rc) return rc;
   pe::Cand c(h.v, h.L, h.arena.data());
   int32_t maxd = (int32_t)h.cfg.max_decisions;
-  int32_t nord = h.v.n_entries * pe::kMaxRank * h.v.n_auto;
+  int32_t nord = h.w.n_ordinals();
   int32_t lw = (nord + 63) / 64;
   for (uint32_t i = 0; i < n; ++i)
     c.rollout(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, h.cp,

@@ -74,6 +74,40 @@ def test_rollouts_device_vs_oracle(oracle_lib, cfgno, group):
     assert all(not H.compare_results(a, b) for a, b in zip(res, ref))
 
 
+def test_resurfacing_rollouts_device_vs_oracle(oracle_lib):
+    # stuck resurfacing (pe.h resurface_stuck; tests/test_resurface.py):
+    # rollouts from the root and from prefixes that contain resurfaced
+    # TileValue(op result) actions, legal bitmasks included
+    nthr = os.cpu_count() or 1
+    picked = 0
+    for i in range(24):
+        if i < 2:
+            text = modelgen.config_program(2)
+            cfg = capi.default_search_config(group_scopes=i, resurface_stuck=1)
+        else:
+            mesh = F.MESHES[i % 3]
+            text = modelgen.random_program(70000 + i, mesh)
+            cfg = capi.default_search_config(group_scopes=0, resurface_stuck=1)
+        n_args = text.split("->")[0].count("%")
+        eng = _engine(text, cfg)
+        seeds = list(range(64))
+        res, seqs, legal = eng.rollout_batch([[]] * 64, seeds, legal=True)
+        ref, rseqs, rlegal = H.rollout_batch("oracle", text, [[]] * 64, seeds, cfg,
+                                             legal_words=eng.legal_words, threads=nthr)
+        assert seqs == rseqs and legal == rlegal
+        assert all(not H.compare_results(a, b) for a, b in zip(res, ref))
+        picked += sum(1 for s in seqs for a in s if a[3] == capi.PE_ACT_TILE and a[0] >= n_args)
+        prefixes = [s[:k] for s in seqs[:8] for k in range(1, len(s) + 1)]
+        if prefixes:
+            ps = [500 + k for k in range(len(prefixes))]
+            res, seqs2, legal = eng.rollout_batch(prefixes, ps, legal=True)
+            ref, rseqs2, rlegal = H.rollout_batch("oracle", text, prefixes, ps, cfg,
+                                                  legal_words=eng.legal_words, threads=nthr)
+            assert seqs2 == rseqs2 and legal == rlegal
+            assert all(not H.compare_results(a, b) for a, b in zip(res, ref))
+    assert picked > 50
+
+
 def test_gpt2_medium_24_layer_rollouts(oracle_lib):
     # config 3: 24-layer GPT-2-medium graph on [batch=4, model=2]
     text = modelgen.config_program(3)

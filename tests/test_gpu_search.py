@@ -28,6 +28,26 @@ def test_gpu_search_equals_oracle_search(oracle_lib):
     assert not H.compare_results(gp.result, op.result)
 
 
+def test_gpu_search_with_resurfacing_equals_oracle_search(oracle_lib):
+    # worklist with stuck resurfacing (pe.h resurface_stuck)
+    text = modelgen.build_transformer(**TWO_LAYER)
+    g = engine.Graph(text)
+    cfg = capi.default_search_config(group_scopes=1, resurface_stuck=1)
+    cp = capi.default_cost_params()
+    cp.memory_budget_bytes = int(0.6 * H.oracle_info(text, cfg)["baseline_bytes"])
+    ords = search.ordinal_actions(g, cfg)
+    lw = (len(ords) - 1 + 63) // 64
+    eng = _engine(text, cfg, cp)
+    assert eng.n_ordinals == len(ords) - 1
+    assert [(eng.ordinal_action(o).value, eng.ordinal_action(o).kind) for o in range(len(ords) - 1)] \
+        == [(a.value, a.kind) for a in ords[:-1]]
+    gp = search.mcts_search(eng, episodes=192, seed=9, leaf_batch=32)
+    op = search.run_mcts(evaluator("oracle", text, cfg, cp, lw), len(ords) - 1, ords,
+                         episodes=192, seed=9, leaf_batch=32)
+    assert search.plan_actions(gp) == search.plan_actions(op)
+    assert not H.compare_results(gp.result, op.result)
+
+
 def test_gpu_megatron_recovery_20_seeds():
     # SPEC acceptance 3: >= 80% of 20 seeds at budget 500; 9: 2-20 decisions
     text = modelgen.build_transformer(**TWO_LAYER)
