@@ -139,6 +139,14 @@ typedef struct pe_search_config {
                               Rollouts enumerate legal actions in worklist
                               order (static entries, then resurfaced ones in
                               discovery order).  0 (default) = static worklist */
+  const uint32_t* worklist_args; /* optional (NULL = all): the ranker's top-k
+                              argument indices (SPEC build_worklist "optionally
+                              filtered to ranker top-k").  Static entries are
+                              restricted to them: an argument entry is kept when
+                              listed, a scope group when any member is listed
+                              (a TILE_GROUP action still tiles every member).
+                              Read once at engine / oracle setup. */
+  uint32_t n_worklist_args;
 } pe_search_config;
 
 void pe_default_cost_params(pe_cost_params* out);

@@ -98,17 +98,28 @@ void build_groups(Setup& s) {
       s.groups[it->second].push_back((int)a);
     }
   }
+  // ranker top-k filter (pe.h worklist_args; SPEC build_worklist "optionally
+  // filtered to ranker top-k"): an argument entry is kept when listed, a
+  // group when any member is listed
+  std::vector<char> keep(s.root.args.size(), s.cfg.worklist_args ? 0 : 1);
+  for (uint32_t i = 0; s.cfg.worklist_args && i < s.cfg.n_worklist_args; ++i)
+    if (s.cfg.worklist_args[i] < keep.size()) keep[s.cfg.worklist_args[i]] = 1;
+  s.cfg.worklist_args = nullptr;  // read once
   // worklist entries and the action value each one decodes to (the group
   // index for TILE_GROUP, the argument for TILE)
   if (s.cfg.group_scopes) {
     for (size_t gi = 0; gi < s.groups.size(); ++gi) {
       if (s.cfg.scoped_only && s.root.args[s.groups[gi][0]].scope.empty()) continue;
+      bool any = false;
+      for (int m : s.groups[gi]) any = any || keep[m];
+      if (!any) continue;
       s.entries.push_back(s.groups[gi]);
       s.entry_val.push_back((int)gi);
     }
   } else {
     for (size_t a = 0; a < s.root.args.size(); ++a) {
       if (s.cfg.scoped_only && s.root.args[a].scope.empty()) continue;
+      if (!keep[a]) continue;
       s.entries.push_back({(int)a});
       s.entry_val.push_back((int)a);
     }

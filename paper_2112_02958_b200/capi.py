@@ -79,7 +79,17 @@ class PeSearchConfig(C.Structure):
                 ("group_scopes", C.c_uint32), ("episodes", C.c_uint32),
                 ("seed", C.c_uint64), ("uct_c", C.c_double),
                 ("leaf_batch", C.c_uint32), ("scoped_only", C.c_uint32),
-                ("resurface_stuck", C.c_uint32)]
+                ("resurface_stuck", C.c_uint32),
+                ("worklist_args", C.POINTER(C.c_uint32)), ("n_worklist_args", C.c_uint32)]
+
+    def restrict_worklist(self, args) -> "PeSearchConfig":
+        """Restrict the static worklist to these argument indices (ranker
+        top-k); the array is kept alive by this config object."""
+        arr = (C.c_uint32 * max(1, len(args)))(*args)
+        self._worklist_keep = arr
+        self.worklist_args = C.cast(arr, C.POINTER(C.c_uint32))
+        self.n_worklist_args = len(args)
+        return self
 
 
 PE_PLAN_MAX_ACTIONS = 64
@@ -111,7 +121,7 @@ def default_cost_params() -> PeCostParams:
 
 
 def default_search_config(**kw) -> PeSearchConfig:
-    c = PeSearchConfig(0xFFFFFFFF, 32, 1, 500, 0, 1.414, 256, 0, 0)
+    c = PeSearchConfig(0xFFFFFFFF, 32, 1, 500, 0, 1.414, 256, 0, 0, None, 0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c

@@ -303,7 +303,9 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   const pe::HostGraph& g = graph->g;
   // worklist entries (SPEC build_worklist: arguments, optionally grouped)
   e->wl = pe::build_worklist(g, e->cfg.auto_axes_mask, e->cfg.group_scopes != 0,
-                             e->cfg.scoped_only != 0, e->cfg.resurface_stuck != 0);
+                             e->cfg.scoped_only != 0, e->cfg.resurface_stuck != 0,
+                             pe::worklist_filter(g, e->cfg));
+  e->cfg.worklist_args = nullptr;  // read once; the caller's array may go away
   const pe::Worklist& w = e->wl;
   e->n_ordinals = (uint32_t)w.n_ordinals();
 

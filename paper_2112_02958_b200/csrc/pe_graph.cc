@@ -815,8 +815,18 @@ GraphView HostGraph::host_view() const {
   return v;
 }
 
+std::vector<char> worklist_filter(const HostGraph& g, const pe_search_config& cfg) {
+  std::vector<char> keep;
+  if (!cfg.worklist_args) return keep;
+  keep.assign(g.args.size(), 0);
+  for (uint32_t i = 0; i < cfg.n_worklist_args; ++i)
+    if (cfg.worklist_args[i] < g.args.size()) keep[cfg.worklist_args[i]] = 1;
+  return keep;
+}
+
 Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes,
-                        bool scoped_only, bool resurface) {
+                        bool scoped_only, bool resurface, const std::vector<char>& keep) {
+  auto kept = [&](int32_t a) { return keep.empty() || keep[a]; };
   Worklist w;
   w.groups = group_scopes;
   w.resurface = resurface;
@@ -833,6 +843,9 @@ Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_
     for (int32_t gi = 0; gi < (int32_t)g.groups.size(); ++gi) {
       const auto& grp = g.groups[gi];
       if (scoped_only && g.args[grp[0]].scope.empty()) continue;
+      bool any = false;
+      for (int32_t m : grp) any = any || kept(m);
+      if (!any) continue;
       for (int32_t m : grp) w.ent_mem.push_back(m);
       w.ent_off.push_back((int32_t)w.ent_mem.size());
       w.ent_val.push_back(gi);
@@ -840,6 +853,7 @@ Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_
   } else {
     for (int32_t a = 0; a < (int32_t)g.args.size(); ++a) {
       if (scoped_only && g.args[a].scope.empty()) continue;
+      if (!kept(a)) continue;
       w.ent_mem.push_back(a);
       w.ent_off.push_back((int32_t)w.ent_mem.size());
       w.ent_val.push_back(a);

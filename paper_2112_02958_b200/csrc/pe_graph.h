@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "pe.h"
 #include "pe_graph_view.h"
 
 namespace pe {
@@ -94,8 +95,12 @@ struct Worklist {
     return (n_entries() + (resurface ? n_ops : 0)) * kMaxRank * (int32_t)auto_axes.size();
   }
 };
+// keep = per-argument filter (empty = all arguments; ranker top-k)
 Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes,
-                        bool scoped_only = false, bool resurface = false);
+                        bool scoped_only = false, bool resurface = false,
+                        const std::vector<char>& keep = std::vector<char>());
+// the argument filter a search config asks for (empty = all)
+std::vector<char> worklist_filter(const HostGraph& g, const pe_search_config& cfg);
 // points the worklist fields of `v` at the (host) vectors of `w`
 void attach_worklist(GraphView& v, const Worklist& w);
 

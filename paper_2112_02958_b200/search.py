@@ -131,6 +131,9 @@ def ordinal_actions(graph, cfg) -> list:
         entries = [(a, [a]) for a in range(graph.n_args)]
     if cfg.scoped_only:
         entries = [(v, m) for v, m in entries if graph.scopes[m[0]]]
+    if cfg.worklist_args:  # ranker top-k (pe.h worklist_args)
+        keep = {cfg.worklist_args[i] for i in range(cfg.n_worklist_args)}
+        entries = [(v, m) for v, m in entries if keep & set(m)]
     kind = capi.PE_ACT_TILE_GROUP if cfg.group_scopes else capi.PE_ACT_TILE
     out = []
     for val, _mem in entries:

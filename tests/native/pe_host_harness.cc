@@ -55,7 +55,9 @@ int setup(Harness& h, const char* pir, size_t len, const pe_search_config* cfg,
   if (cp) h.cp = *cp;
   h.v = h.g.host_view();
   h.w = pe::build_worklist(h.g, h.cfg.auto_axes_mask, h.cfg.group_scopes != 0,
-                           h.cfg.scoped_only != 0, h.cfg.resurface_stuck != 0);
+                           h.cfg.scoped_only != 0, h.cfg.resurface_stuck != 0,
+                           pe::worklist_filter(h.g, h.cfg));
+  h.cfg.worklist_args = nullptr;
   pe::attach_worklist(h.v, h.w);
   h.L = pe::make_layout(h.v);
   h.arena.assign(h.L.bytes, 0);
