@@ -1605,6 +1605,7 @@ struct Cand {
   // static entries, then the resurfaced ops in discovery order; a
   // resurfaced op is legal as apply_tile_action would accept it (still at
   // top level and carrying no tiling: TOP without slices; the dim divides).
+  template <bool RS>
   PE_HD int32_t build_legal() {
     int32_t n = 0;
     for (int32_t o = 0; o < g.n_ord; ++o) {
@@ -1616,7 +1617,7 @@ struct Cand {
         }
       }
     }
-    for (int32_t i = 0; i < nrs; ++i) {
+    for (int32_t i = 0; RS && i < nrs; ++i) {
       int32_t o = a.rs()[i], v = g.A + o;
       if (a.vk()[v] != VK_TOP || a.slcnt()[v] != 0) continue;
       int32_t rank = g.vrank[v];
@@ -1651,6 +1652,11 @@ struct Cand {
     return z ^ (z >> 31);
   }
 
+  // RS = stuck resurfacing compiled in (pe.h resurface_stuck); the engine
+  // launches the RS instantiation only when the worklist asks for it, so
+  // the default kernel carries none of its code (code size bounds this
+  // kernel: instruction-cache stalls).
+  template <bool RS>
   PE_HD void rollout(const pe_action* prefix, int32_t np, uint64_t seed, int32_t maxd,
                      const pe_cost_params& cp, int64_t baseline, pe_action* acts_out,
                      uint32_t* n_out, pe_result& r, uint64_t* legal_out, int32_t legal_words) {
@@ -1670,7 +1676,7 @@ struct Cand {
     // as the oracle does after each apply_action
     bool rs_due = false;
     for (int32_t k = 0; k < np; ++k) {
-      if (rs_due && !(prefix[k].pad & PE_ACT_FLAG_INFERRED)) {
+      if (RS && rs_due && !(prefix[k].pad & PE_ACT_FLAG_INFERRED)) {
         resurface_update();
         rs_due = false;
         if (bad()) break;
@@ -1703,22 +1709,22 @@ struct Cand {
       propagate();
       propagated = true;
       if (bad()) break;
-      rs_due = g.resurface != 0;
+      rs_due = RS;
       if (nacts < maxd) acts_out[nacts] = prefix[k];
       ++nacts;
       if (!(prefix[k].pad & PE_ACT_FLAG_INFERRED)) ++steps;
     }
-    if (rs_due && !bad() && status == PE_CAND_OK) resurface_update();
+    if (RS && rs_due && !bad() && status == PE_CAND_OK) resurface_update();
     if (!bad() && status == PE_CAND_OK) {
       if (legal_out) {
-        int32_t nl = build_legal();
+        int32_t nl = build_legal<RS>();
         for (int32_t i = 0; i < nl; ++i) legal_out[a.lg()[i] >> 6] |= 1ull << (a.lg()[i] & 63);
       }
       uint64_t st = seed;
       while (!terminal) {
         if (steps >= maxd) break;
         tick(4);
-        int32_t nl = build_legal();
+        int32_t nl = build_legal<RS>();
         if (nl == 0) break;
         uint64_t ws = steps >= 1 ? 2 : 1;
         uint64_t pick = splitmix(st) % ((uint64_t)nl + ws);
@@ -1735,7 +1741,7 @@ struct Cand {
         propagate();
         propagated = true;
         if (bad()) break;
-        if (g.resurface) {
+        if (RS) {
           resurface_update();
           if (bad()) break;
         }

@@ -128,7 +128,7 @@ pe_eval_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ 
   }
 }
 
-template <bool RETRY>
+template <bool RETRY, bool RS>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
 pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
                   uint8_t* arena, uint32_t slots,
@@ -148,7 +148,8 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
   for (uint32_t i = slot; i < n; i = next_cand<RETRY>(i, slots, ctr)) {
     if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
-    c.rollout(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, cp, baseline,
+    c.template rollout<RS>(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd,
+                           cp, baseline,
               acts_out + (uint64_t)i * maxd, n_out + i, r,
               legal_out ? legal_out + (uint64_t)i * legal_words : nullptr, legal_words);
     out[i] = r;
@@ -713,14 +714,22 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   if (!cuda_ok(cudaMemsetAsync(e->d_ctr + 1, 0, sizeof(uint32_t), st), err,
                "reset work counter"))
     return PE_ERR_CUDA;
-  pe_rollout_kernel<false>
-      <<<(slots * kThreadsPerSlot + kBlock - 1) / kBlock, kBlock, 0, st>>>(
-      e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff, d_seeds, n, maxd, e->cp,
-      e->baseline, d_acts, d_nacts, d_out, d_legal, lw, e->d_ctr + 1);
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
-  pe_rollout_kernel<true><<<(bs * kThreadsPerSlot + kBlock - 1) / kBlock, kBlock, 0, st>>>(
-      e->dview, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff, d_seeds, n, maxd, e->cp,
-      e->baseline, d_acts, d_nacts, d_out, d_legal, lw, nullptr);
+  uint32_t grid = (slots * kThreadsPerSlot + kBlock - 1) / kBlock;
+  uint32_t bgrid = (bs * kThreadsPerSlot + kBlock - 1) / kBlock;
+  // (the stuck-resurfacing instantiation only when the worklist uses it)
+  auto launch = [&](auto main_k, auto retry_k) {
+    main_k<<<grid, kBlock, 0, st>>>(e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
+                                    d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts, d_out,
+                                    d_legal, lw, e->d_ctr + 1);
+    retry_k<<<bgrid, kBlock, 0, st>>>(e->dview, e->big_layout, e->d_big_arena, bs, d_prefix,
+                                      d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
+                                      d_nacts, d_out, d_legal, lw, nullptr);
+  };
+  if (e->wl.resurface)
+    launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>);
+  else
+    launch(pe_rollout_kernel<false, false>, pe_rollout_kernel<true, false>);
   e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "pe_rollout_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {

@@ -98,10 +98,11 @@ int harness_rollout_batch(const char* pir, size_t len, const pe_search_config* c
   int32_t maxd = (int32_t)h.cfg.max_decisions;
   int32_t nord = h.w.n_ordinals();
   int32_t lw = (nord + 63) / 64;
+  auto ro = h.v.resurface ? &pe::Cand::rollout<true> : &pe::Cand::rollout<false>;
   for (uint32_t i = 0; i < n; ++i)
-    c.rollout(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, h.cp,
-              h.baseline, acts_out + (size_t)i * maxd, n_out + i, out[i],
-              legal_out ? legal_out + (size_t)i * lw : nullptr, lw);
+    (c.*ro)(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, h.cp,
+            h.baseline, acts_out + (size_t)i * maxd, n_out + i, out[i],
+            legal_out ? legal_out + (size_t)i * lw : nullptr, lw);
   return 0;
 }
 
@@ -119,7 +120,8 @@ int harness_highwater(const char* pir, size_t len, const pe_search_config* cfg,
   for (uint32_t i = 0; i < n; ++i) {
     uint32_t na;
     pe_result r;
-    c.rollout(nullptr, 0, seeds[i], maxd, h.cp, h.baseline, acts.data(), &na, r, nullptr, 0);
+    c.rollout<false>(nullptr, 0, seeds[i], maxd, h.cp, h.baseline, acts.data(), &na, r, nullptr,
+                     0);
     out5[0] = std::max<int64_t>(out5[0], c.nslots - (h.v.A + h.v.N));
     out5[1] = std::max<int64_t>(out5[1], c.nloops);
     out5[2] = std::max<int64_t>(out5[2], c.nfs);

@@ -23,6 +23,6 @@ for l in dis:
         per[curf][key] += 1
 for f, c in cnt.most_common(8):
     print(c, f[:90])
-k = [f for f in cnt if 'pe_rollout_kernelILb0' in f][0]
+k = [f for f in cnt if 'pe_rollout_kernelILb0ELb0' in f or f.endswith('pe_rollout_kernelILb0EEEvN2pe9GraphVie')][0] if any('ILb0ELb0' in f for f in cnt) else [f for f in cnt if 'pe_rollout_kernelILb0' in f][0]
 print("rollout<false> by function:")
 for fn_, c in per[k].most_common(30): print(f"  {c:6d} {fn_}")
