@@ -186,14 +186,14 @@ def run_engine(args):
     base = 1_000_003 * (rank + 1)
     seeds = (torch.arange((K + W) * B, dtype=torch.int64, device=dev) + base).view(K + W, B)
     poff = torch.zeros(B + 1, dtype=torch.int32, device=dev)
-    prefix = torch.zeros(2, dtype=torch.int64, device=dev)
     acts_out = torch.empty(B * maxd * 8, dtype=torch.uint8, device=dev)
     nacts = torch.empty(B, dtype=torch.int32, device=dev)
     res = torch.empty(B * C.sizeof(capi.PeResult), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(i):
-        eng.rollout_batch_device(prefix.data_ptr(), poff.data_ptr(), seeds[i].data_ptr(), B,
+        # prefix = NULL: every prefix is empty (root rollouts; pe.h)
+        eng.rollout_batch_device(None, poff.data_ptr(), seeds[i].data_ptr(), B,
                                  acts_out.data_ptr(), nacts.data_ptr(), res.data_ptr(),
                                  stream=sp)
 

@@ -273,6 +273,16 @@ uint32_t pe_engine_slots(const pe_engine* e);
 int64_t pe_engine_graph_bytes(const pe_engine* e);
 /* kernel launches issued by this engine since creation */
 uint64_t pe_engine_launch_count(const pe_engine* e);
+/* Prefix-trie scheduling: a batch of root rollouts (every
+ * prefix empty; in device mode pass prefix = NULL) of at least 8192
+ * candidates is evaluated in an order that groups candidates by their first
+ * decisions, predicted from the seeds through a trie of legal sets after
+ * short decision prefixes (depth 3).  The trie is cached by the engine and
+ * grows by one level per call.  Results are unaffected (each candidate is
+ * independent; outputs stay in candidate order).  Env PE_SCHED_DEPTH (0 =
+ * off) and PE_SCHED_MIN_BATCH override at engine creation.  Returns the
+ * number of trie nodes (prefix states probed). */
+int64_t pe_engine_sched_nodes(const pe_engine* e);
 
 /* ---- search (SPEC search module: mcts_search / emit_plan) ---- */
 #define PE_PLAN_MAX_ACTIONS 64

@@ -53,6 +53,23 @@ struct pe_engine {
   size_t io_cap = 0;
   // work counters of the main-pass kernels (zeroed before each launch)
   uint32_t* d_ctr = nullptr;
+  // prefix-trie scheduling: legal sets after short
+  // decision prefixes (deterministic for the graph and config), per node:
+  // legal-ordinal count, child offset, depth; children per legal index
+  int sched_depth = 3;
+  uint32_t sched_min_batch = 8192;
+  std::vector<int32_t> t_nl, t_child_off, t_depth, t_parent, t_pick;
+  std::vector<int32_t> t_legal_off, t_legal, t_child;
+  bool t_dirty = true;
+  int32_t* d_tnode = nullptr;  // int4 per node: nl, child offset, depth, 0
+  int32_t* d_tchild = nullptr;
+  uint32_t* d_tmiss = nullptr;
+  size_t tnode_cap = 0, tchild_cap = 0;
+  uint32_t* d_keys = nullptr;
+  uint32_t* d_perm = nullptr;
+  uint32_t* d_hist = nullptr;
+  size_t sched_cap = 0, perm_cap = 0, hist_cap = 0;
+  uint64_t sched_probes = 0;  // prefix states probed (diagnostic)
 };
 
 namespace {
@@ -135,7 +152,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                   const pe_action* prefix, const uint32_t* poff, const uint64_t* seeds,
                   uint32_t n, int32_t maxd, pe_cost_params cp, int64_t baseline,
                   pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
-                  int32_t legal_words, uint32_t* ctr) {
+                  int32_t legal_words, uint32_t* ctr, const uint32_t* perm) {
 #if PE_SOLO
   // experiment: one active lane per warp (no SIMT divergence across candidates)
   if (threadIdx.x % 32) return;
@@ -145,7 +162,11 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
 #endif
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
-  for (uint32_t i = slot; i < n; i = next_cand<RETRY>(i, slots, ctr)) {
+  // k = schedule position; perm (prefix-trie scheduling) maps it to the
+  // candidate, so lanes of a warp run candidates that share their first
+  // decisions; results stay in candidate order
+  for (uint32_t k = slot; k < n; k = next_cand<RETRY>(k, slots, ctr)) {
+    uint32_t i = perm ? perm[k] : k;
     if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
     pe_result r;
     c.template rollout<RS>(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd,
@@ -157,6 +178,78 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
 #if defined(PE_PHASE_TIMERS) && defined(__CUDA_ARCH__)
   for (int k = 0; k < 9; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)c.ph[k]);
 #endif
+}
+
+// ---- prefix-trie scheduling kernels ----
+// Walks candidate i's seed through the trie with exactly the rollout's
+// draws (Cand::rollout: no draw when nothing is legal; Stop weight 1 before
+// the first decision, 2 after) and keys it by the deepest known node (odd
+// key: the rollout stops there).  Unprobed children that are reached are
+// flagged for the host to probe.
+__global__ void pe_sched_key_kernel(uint32_t n, const uint64_t* seeds, int32_t depth,
+                                    const int4* tnode, const int32_t* tchild, uint32_t* tmiss,
+                                    uint32_t* nmiss, uint32_t* keys, uint32_t* hist) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t st = seeds[i];
+  int32_t node = 0, steps = 0;
+  uint32_t key;
+  while (true) {
+    int4 nd = tnode[node];
+    if (steps >= depth || nd.x == 0) {
+      key = 2u * (uint32_t)node;
+      break;
+    }
+    uint64_t ws = steps >= 1 ? 2 : 1;
+    uint64_t pick = pe::Cand::splitmix(st) % ((uint64_t)nd.x + ws);
+    if (pick >= (uint64_t)nd.x) {
+      key = 2u * (uint32_t)node + 1u;
+      break;
+    }
+    int32_t c = tchild[nd.y + (int32_t)pick];
+    if (c < 0) {
+      tmiss[nd.y + (int32_t)pick] = 1u;
+      atomicAdd(nmiss, 1u);  // candidates that would group deeper after a probe
+      key = 2u * (uint32_t)node;
+      break;
+    }
+    node = c;
+    ++steps;
+  }
+  keys[i] = key;
+  atomicAdd(&hist[key], 1u);
+}
+
+// exclusive scan of hist[0, m) in place (one block)
+__global__ void pe_sched_scan_kernel(uint32_t* hist, uint32_t m) {
+  __shared__ uint32_t part[1024];
+  uint32_t t = threadIdx.x, chunk = (m + blockDim.x - 1) / blockDim.x;
+  uint32_t lo = min(m, t * chunk), hi = min(m, lo + chunk), sum = 0;
+  for (uint32_t k = lo; k < hi; ++k) sum += hist[k];
+  part[t] = sum;
+  __syncthreads();
+  if (t == 0) {
+    uint32_t run = 0;
+    for (uint32_t k = 0; k < blockDim.x; ++k) {
+      uint32_t v = part[k];
+      part[k] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  uint32_t run = part[t];
+  for (uint32_t k = lo; k < hi; ++k) {
+    uint32_t v = hist[k];
+    hist[k] = run;
+    run += v;
+  }
+}
+
+__global__ void pe_sched_scatter_kernel(uint32_t n, const uint32_t* keys, uint32_t* offs,
+                                        uint32_t* perm) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  perm[atomicAdd(&offs[keys[i]], 1u)] = i;
 }
 
 // Append a host vector to the device image; returns its offset.
@@ -365,6 +458,8 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   // per-candidate arenas: one per thread slot, bounded by an HBM budget
   e->layout = pe::make_layout(v, /*tight=*/true);
   e->big_layout = pe::make_layout(v, /*tight=*/false);
+  if (const char* sd = std::getenv("PE_SCHED_DEPTH")) e->sched_depth = std::atoi(sd);
+  if (const char* sm = std::getenv("PE_SCHED_MIN_BATCH")) e->sched_min_batch = (uint32_t)std::atoi(sm);
   if (const char* dbg = std::getenv("PE_DEBUG_TIGHT_EM_CAP")) {
     // test hook: shrink the tight arena so candidates overflow and take the
     // retry path (tests/test_gpu_parity.py::test_capacity_retry_path)
@@ -427,6 +522,9 @@ void pe_engine_destroy(pe_engine* e) {
   if (e->d_arena) cudaFree(e->d_arena);
   if (e->d_big_arena) cudaFree(e->d_big_arena);
   if (e->d_ctr) cudaFree(e->d_ctr);
+  for (void* q : {(void*)e->d_tnode, (void*)e->d_tchild, (void*)e->d_tmiss, (void*)e->d_keys,
+                  (void*)e->d_perm, (void*)e->d_hist})
+    if (q) cudaFree(q);
   if (e->d_io) cudaFree(e->d_io);
   delete e;
 }
@@ -439,6 +537,7 @@ int64_t pe_engine_arena_bytes(const pe_engine* e) {
 }
 uint32_t pe_engine_slots(const pe_engine* e) { return e->slots; }
 uint64_t pe_engine_launch_count(const pe_engine* e) { return e->launches; }
+int64_t pe_engine_sched_nodes(const pe_engine* e) { return (int64_t)e->t_nl.size(); }
 int64_t pe_engine_graph_bytes(const pe_engine* e) { return e->graph_bytes; }
 
 pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* out) {
@@ -654,6 +753,222 @@ pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* 
   return PE_OK;
 }
 
+}  // extern "C"
+
+// ---- prefix-trie scheduling, host side ----
+namespace {
+
+constexpr int32_t kMaxTrieNodes = 1 << 16;
+
+// Legal TileValue ordinals (ascending: the rollout's enumeration order
+// without resurfacing) after each prefix: one rollout launch whose legal
+// output is taken right after the prefix.  Own buffers: the caller's inputs
+// may live in the staging buffer.
+bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefixes,
+                 std::vector<std::vector<int32_t>>& legal, cudaStream_t st, pe_error* err) {
+  uint32_t n = (uint32_t)prefixes.size();
+  std::vector<pe_action> acts;
+  std::vector<uint32_t> off{0};
+  int32_t maxlen = 0;
+  for (const auto& pr : prefixes) {
+    acts.insert(acts.end(), pr.begin(), pr.end());
+    off.push_back((uint32_t)acts.size());
+    maxlen = std::max(maxlen, (int32_t)pr.size());
+  }
+  int32_t maxd = std::max(1, maxlen);
+  int32_t lw = (int32_t)pe_engine_legal_words(e);
+  size_t b_acts = std::max<size_t>(1, acts.size()) * sizeof(pe_action);
+  size_t sizes[7] = {b_acts, (n + 1) * 4ull, n * 8ull, (size_t)n * maxd * sizeof(pe_action),
+                     n * 4ull, n * sizeof(pe_result), (size_t)n * lw * 8};
+  void* buf[7] = {};
+  bool ok = true;
+  for (int k = 0; k < 7 && ok; ++k) ok = cuda_ok(cudaMalloc(&buf[k], sizes[k]), err, "cudaMalloc(probe)");
+  std::vector<uint64_t> lg((size_t)n * lw);
+  if (ok) {
+    ok = (acts.empty() || cuda_ok(cudaMemcpyAsync(buf[0], acts.data(), acts.size() * sizeof(pe_action),
+                                                  cudaMemcpyHostToDevice, st), err, "H2D probe")) &&
+         cuda_ok(cudaMemcpyAsync(buf[1], off.data(), off.size() * 4, cudaMemcpyHostToDevice, st),
+                 err, "H2D probe") &&
+         cuda_ok(cudaMemsetAsync(buf[2], 0, sizes[2], st), err, "probe seeds") &&
+         cuda_ok(cudaMemsetAsync(e->d_ctr + 2, 0, 4, st), err, "probe counter");
+  }
+  if (ok) {
+    uint32_t slots = launch_slots(e, n), bs = std::min<uint32_t>(e->big_slots, n);
+    pe_rollout_kernel<false, false><<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+        e->dview, e->layout, e->d_arena, slots, (const pe_action*)buf[0], (const uint32_t*)buf[1],
+        (const uint64_t*)buf[2], n, maxd, e->cp, e->baseline, (pe_action*)buf[3],
+        (uint32_t*)buf[4], (pe_result*)buf[5], (uint64_t*)buf[6], lw, e->d_ctr + 2, nullptr);
+    pe_rollout_kernel<true, false><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+        e->dview, e->big_layout, e->d_big_arena, bs, (const pe_action*)buf[0],
+        (const uint32_t*)buf[1], (const uint64_t*)buf[2], n, maxd, e->cp, e->baseline,
+        (pe_action*)buf[3], (uint32_t*)buf[4], (pe_result*)buf[5], (uint64_t*)buf[6], lw,
+        nullptr, nullptr);
+    e->launches += 2;
+    ok = cuda_ok(cudaGetLastError(), err, "probe launch") &&
+         cuda_ok(cudaMemcpyAsync(lg.data(), buf[6], sizes[6], cudaMemcpyDeviceToHost, st), err,
+                 "D2H probe") &&
+         cuda_ok(cudaStreamSynchronize(st), err, "probe sync");
+  }
+  for (int k = 0; k < 7; ++k)
+    if (buf[k]) cudaFree(buf[k]);
+  if (!ok) return false;
+  legal.assign(n, {});
+  for (uint32_t i = 0; i < n; ++i)
+    for (int32_t o = 0; o < (int32_t)e->n_ordinals; ++o)
+      if ((lg[(size_t)i * lw + o / 64] >> (o % 64)) & 1ull) legal[i].push_back(o);
+  e->sched_probes += n;
+  return true;
+}
+
+int32_t sched_add_node(pe_engine* e, int32_t parent, int32_t pick,
+                       const std::vector<int32_t>& legal) {
+  int32_t id = (int32_t)e->t_nl.size();
+  e->t_nl.push_back((int32_t)legal.size());
+  e->t_legal_off.push_back((int32_t)e->t_legal.size());
+  e->t_legal.insert(e->t_legal.end(), legal.begin(), legal.end());
+  e->t_child_off.push_back((int32_t)e->t_child.size());
+  e->t_child.insert(e->t_child.end(), legal.size(), -1);
+  e->t_depth.push_back(parent < 0 ? 0 : e->t_depth[parent] + 1);
+  e->t_parent.push_back(parent);
+  e->t_pick.push_back(pick);
+  if (parent >= 0) e->t_child[e->t_child_off[parent] + pick] = id;
+  e->t_dirty = true;
+  return id;
+}
+
+// decision path from the root to `node`
+std::vector<pe_action> sched_path(pe_engine* e, int32_t node) {
+  std::vector<pe_action> path;
+  for (int32_t v = node; e->t_parent[v] >= 0; v = e->t_parent[v]) {
+    int32_t par = e->t_parent[v];
+    pe_action a;
+    pe_engine_ordinal_action(e, (uint32_t)e->t_legal[e->t_legal_off[par] + e->t_pick[v]], &a);
+    path.push_back(a);
+  }
+  std::reverse(path.begin(), path.end());
+  return path;
+}
+
+template <typename T>
+bool ensure_dev(T*& p, size_t& cap, size_t need, pe_error* err, const char* what) {
+  if (need <= cap) return true;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  size_t c = std::max<size_t>(need, 1024);
+  if (!cuda_ok(cudaMalloc(&p, c * sizeof(T)), err, what)) return false;
+  cap = c;
+  return true;
+}
+
+bool sched_upload(pe_engine* e, cudaStream_t st, pe_error* err) {
+  if (!e->t_dirty) return true;
+  size_t nodes = e->t_nl.size(), nch = std::max<size_t>(1, e->t_child.size());
+  size_t tcap = e->tchild_cap;
+  if (!ensure_dev(e->d_tnode, e->tnode_cap, nodes * 4, err, "cudaMalloc(trie)") ||
+      !ensure_dev(e->d_tchild, e->tchild_cap, nch, err, "cudaMalloc(trie)"))
+    return false;
+  if (e->tchild_cap != tcap || !e->d_tmiss) {
+    if (e->d_tmiss) cudaFree(e->d_tmiss);
+    e->d_tmiss = nullptr;
+    if (!cuda_ok(cudaMalloc(&e->d_tmiss, e->tchild_cap * 4), err, "cudaMalloc(trie)")) return false;
+  }
+  std::vector<int32_t> tn(nodes * 4, 0);
+  for (size_t v = 0; v < nodes; ++v) {
+    tn[4 * v] = e->t_nl[v];
+    tn[4 * v + 1] = e->t_child_off[v];
+    tn[4 * v + 2] = e->t_depth[v];
+  }
+  if (!cuda_ok(cudaMemcpyAsync(e->d_tnode, tn.data(), tn.size() * 4, cudaMemcpyHostToDevice, st),
+               err, "H2D trie") ||
+      (!e->t_child.empty() &&
+       !cuda_ok(cudaMemcpyAsync(e->d_tchild, e->t_child.data(), e->t_child.size() * 4,
+                                cudaMemcpyHostToDevice, st), err, "H2D trie")) ||
+      !cuda_ok(cudaMemsetAsync(e->d_tmiss, 0, e->tchild_cap * 4, st), err, "trie misses"))
+    return false;
+  // (tn / t_child are read by the copies before this function returns)
+  if (!cuda_ok(cudaStreamSynchronize(st), err, "trie sync")) return false;
+  e->t_dirty = false;
+  return true;
+}
+
+// Candidate order for a batch of root rollouts: grouped by the deepest trie
+// node their first decisions reach.  Probes at most one new level per call
+// (the prefix states the batch reached but the trie lacks).  Returns the
+// device permutation, or nullptr (identity) when scheduling is off.
+bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
+                cudaStream_t st, const uint32_t** perm, pe_error* err) {
+  *perm = nullptr;
+  int32_t depth = std::min(e->sched_depth, maxd);
+  if (depth <= 0) return true;
+  if (e->t_nl.empty()) {
+    std::vector<std::vector<int32_t>> lg;
+    if (!sched_probe(e, {{}}, lg, st, err)) return false;
+    sched_add_node(e, -1, 0, lg[0]);
+  }
+  if (!ensure_dev(e->d_keys, e->sched_cap, n, err, "cudaMalloc(sched)") ||
+      !ensure_dev(e->d_perm, e->perm_cap, n, err, "cudaMalloc(sched)"))
+    return false;
+  uint32_t m = 0;
+  for (int round = 0; round < 2; ++round) {
+    if (!sched_upload(e, st, err)) return false;
+    m = 2 * (uint32_t)e->t_nl.size();
+    if (!ensure_dev(e->d_hist, e->hist_cap, m, err, "cudaMalloc(sched)") ||
+        !cuda_ok(cudaMemsetAsync(e->d_hist, 0, (size_t)m * 4, st), err, "sched hist") ||
+        !cuda_ok(cudaMemsetAsync(e->d_tmiss, 0, std::max<size_t>(1, e->t_child.size()) * 4, st),
+                 err, "sched misses") ||
+        !cuda_ok(cudaMemsetAsync(e->d_ctr + 3, 0, 4, st), err, "sched misses"))
+      return false;
+    pe_sched_key_kernel<<<(n + 255) / 256, 256, 0, st>>>(
+        n, d_seeds, depth, (const int4*)e->d_tnode, e->d_tchild, e->d_tmiss, e->d_ctr + 3,
+        e->d_keys, e->d_hist);
+    e->launches += 1;
+    if (!cuda_ok(cudaGetLastError(), err, "sched key launch")) return false;
+    if (round == 1 || (int32_t)e->t_nl.size() >= kMaxTrieNodes) break;
+    uint32_t nmiss = 0;
+    if (!cuda_ok(cudaMemcpyAsync(&nmiss, e->d_ctr + 3, 4, cudaMemcpyDeviceToHost, st), err,
+                 "D2H misses") ||
+        !cuda_ok(cudaStreamSynchronize(st), err, "sched sync"))
+      return false;
+    // a probe launch costs about one candidate's latency: only worth it when
+    // a noticeable share of the batch would group deeper
+    if ((uint64_t)nmiss * 64 < n) break;
+    std::vector<uint32_t> miss(e->t_child.size());
+    if (!cuda_ok(cudaMemcpyAsync(miss.data(), e->d_tmiss, miss.size() * 4, cudaMemcpyDeviceToHost,
+                                 st), err, "D2H misses") ||
+        !cuda_ok(cudaStreamSynchronize(st), err, "sched sync"))
+      return false;
+    std::vector<std::pair<int32_t, int32_t>> want;  // (parent, pick)
+    for (int32_t v = 0; v < (int32_t)e->t_nl.size(); ++v)
+      for (int32_t k = 0; k < e->t_nl[v]; ++k)
+        if (miss[e->t_child_off[v] + k] && e->t_child[e->t_child_off[v] + k] < 0)
+          want.push_back({v, k});
+    if (want.size() + e->t_nl.size() > (size_t)kMaxTrieNodes)
+      want.resize((size_t)kMaxTrieNodes - e->t_nl.size());
+    std::vector<std::vector<pe_action>> prefixes;
+    for (auto [v, k] : want) {
+      std::vector<pe_action> pth = sched_path(e, v);
+      pe_action a;
+      pe_engine_ordinal_action(e, (uint32_t)e->t_legal[e->t_legal_off[v] + k], &a);
+      pth.push_back(a);
+      prefixes.push_back(std::move(pth));
+    }
+    std::vector<std::vector<int32_t>> lg;
+    if (!sched_probe(e, prefixes, lg, st, err)) return false;
+    for (size_t q = 0; q < want.size(); ++q) sched_add_node(e, want[q].first, want[q].second, lg[q]);
+  }
+  pe_sched_scan_kernel<<<1, 1024, 0, st>>>(e->d_hist, m);
+  pe_sched_scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, e->d_keys, e->d_hist, e->d_perm);
+  e->launches += 2;
+  if (!cuda_ok(cudaGetLastError(), err, "sched sort launch")) return false;
+  *perm = e->d_perm;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
 pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t* prefix_off,
                            const uint64_t* seeds, uint32_t n, pe_action* acts_out,
                            uint32_t* n_acts_out, pe_result* out, uint64_t* legal_out,
@@ -710,6 +1025,13 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
                                  st), err, "H2D seeds"))
       return PE_ERR_CUDA;
   }
+  // prefix-trie scheduling for batches of root rollouts (all prefixes
+  // empty; a NULL prefix array in device mode), DESIGN.md §3.5
+  const uint32_t* perm = nullptr;
+  bool roots = (flags & PE_MEM_DEVICE) ? prefix == nullptr : prefix_off[n] == 0;
+  if (roots && e->sched_depth > 0 && !e->wl.resurface && n >= e->sched_min_batch &&
+      !sched_perm(e, n, d_seeds, maxd, st, &perm, err))
+    return PE_ERR_CUDA;
   uint32_t slots = launch_slots(e, n);
   if (!cuda_ok(cudaMemsetAsync(e->d_ctr + 1, 0, sizeof(uint32_t), st), err,
                "reset work counter"))
@@ -721,10 +1043,10 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   auto launch = [&](auto main_k, auto retry_k) {
     main_k<<<grid, kBlock, 0, st>>>(e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
                                     d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts, d_out,
-                                    d_legal, lw, e->d_ctr + 1);
+                                    d_legal, lw, e->d_ctr + 1, perm);
     retry_k<<<bgrid, kBlock, 0, st>>>(e->dview, e->big_layout, e->d_big_arena, bs, d_prefix,
                                       d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
-                                      d_nacts, d_out, d_legal, lw, nullptr);
+                                      d_nacts, d_out, d_legal, lw, nullptr, nullptr);
   };
   if (e->wl.resurface)
     launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>);

@@ -166,6 +166,10 @@ class Engine:
     def launch_count(self) -> int:
         return int(self.lib.pe_engine_launch_count(self.h))
 
+    def sched_nodes(self) -> int:
+        """Prefix states in the scheduling trie (pe.h pe_engine_sched_nodes)."""
+        return int(self.lib.pe_engine_sched_nodes(self.h))
+
     def graph_bytes(self) -> int:
         return int(self.lib.pe_engine_graph_bytes(self.h))
 

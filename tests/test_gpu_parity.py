@@ -108,6 +108,31 @@ def test_resurfacing_rollouts_device_vs_oracle(oracle_lib):
     assert picked > 50
 
 
+@pytest.mark.parametrize("cfgno", [2, 3])
+def test_trie_scheduling_preserves_results(oracle_lib, monkeypatch, cfgno):
+    # prefix-trie scheduling (pe.h pe_engine_sched_nodes) only reorders
+    # candidates: acts, legal sets and results equal an unscheduled engine's,
+    # call after call while the trie grows one level per call
+    text = modelgen.config_program(cfgno)
+    cfg = capi.default_search_config(group_scopes=1)
+    sched = _engine(text, cfg)
+    monkeypatch.setenv("PE_SCHED_DEPTH", "0")
+    plain = _engine(text, cfg)
+    n = 8192
+    for call in range(4):
+        seeds = [call * 100_000 + i for i in range(n)]
+        r1, s1, l1 = sched.rollout_batch([[]] * n, seeds, legal=True)
+        r2, s2, l2 = plain.rollout_batch([[]] * n, seeds, legal=True)
+        assert s1 == s2 and l1 == l2
+        assert all(not H.compare_results(a, b) for a, b in zip(r1, r2))
+    assert sched.sched_nodes() > 1 and plain.sched_nodes() == 0
+    if cfgno == 2:
+        ref, rseqs, _ = H.rollout_batch("oracle", text, [[]] * 256, seeds[:256], cfg,
+                                        threads=os.cpu_count() or 1)
+        assert rseqs == s1[:256]
+        assert all(not H.compare_results(a, b) for a, b in zip(r1[:256], ref))
+
+
 def test_gpt2_medium_24_layer_rollouts(oracle_lib):
     # config 3: 24-layer GPT-2-medium graph on [batch=4, model=2]
     text = modelgen.config_program(3)
