@@ -249,7 +249,9 @@ __global__ void pe_sched_scatter_kernel(uint32_t n, const uint32_t* keys, uint32
                                         uint32_t* perm) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  perm[atomicAdd(&offs[keys[i]], 1u)] = i;
+  // reversed: deeper trie nodes (candidates with more decisions, the longer
+  // rollouts) are handed out first, short ones fill the tail
+  perm[n - 1 - atomicAdd(&offs[keys[i]], 1u)] = i;
 }
 
 // Append a host vector to the device image; returns its offset.
