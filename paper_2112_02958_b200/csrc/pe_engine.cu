@@ -58,6 +58,7 @@ struct pe_engine {
   // legal-ordinal count, child offset, depth; children per legal index
   int sched_depth = 3;
   uint32_t sched_min_batch = 8192;
+  int32_t sched_max_nodes = 1 << 16;
   std::vector<int32_t> t_nl, t_child_off, t_depth, t_parent, t_pick;
   std::vector<int32_t> t_legal_off, t_legal, t_child;
   bool t_dirty = true;
@@ -462,6 +463,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   e->big_layout = pe::make_layout(v, /*tight=*/false);
   if (const char* sd = std::getenv("PE_SCHED_DEPTH")) e->sched_depth = std::atoi(sd);
   if (const char* sm = std::getenv("PE_SCHED_MIN_BATCH")) e->sched_min_batch = (uint32_t)std::atoi(sm);
+  if (const char* sn = std::getenv("PE_SCHED_MAX_NODES")) e->sched_max_nodes = std::atoi(sn);
   if (const char* dbg = std::getenv("PE_DEBUG_TIGHT_EM_CAP")) {
     // test hook: shrink the tight arena so candidates overflow and take the
     // retry path (tests/test_gpu_parity.py::test_capacity_retry_path)
@@ -760,7 +762,6 @@ pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* 
 // ---- prefix-trie scheduling, host side ----
 namespace {
 
-constexpr int32_t kMaxTrieNodes = 1 << 16;
 
 // Legal TileValue ordinals (ascending: the rollout's enumeration order
 // without resurfacing) after each prefix: one rollout launch whose legal
@@ -926,7 +927,7 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
         e->d_keys, e->d_hist);
     e->launches += 1;
     if (!cuda_ok(cudaGetLastError(), err, "sched key launch")) return false;
-    if (round == 1 || (int32_t)e->t_nl.size() >= kMaxTrieNodes) break;
+    if (round == 1 || (int32_t)e->t_nl.size() >= e->sched_max_nodes) break;
     uint32_t nmiss = 0;
     if (!cuda_ok(cudaMemcpyAsync(&nmiss, e->d_ctr + 3, 4, cudaMemcpyDeviceToHost, st), err,
                  "D2H misses") ||
@@ -945,8 +946,8 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
       for (int32_t k = 0; k < e->t_nl[v]; ++k)
         if (miss[e->t_child_off[v] + k] && e->t_child[e->t_child_off[v] + k] < 0)
           want.push_back({v, k});
-    if (want.size() + e->t_nl.size() > (size_t)kMaxTrieNodes)
-      want.resize((size_t)kMaxTrieNodes - e->t_nl.size());
+    if (want.size() + e->t_nl.size() > (size_t)e->sched_max_nodes)
+      want.resize((size_t)e->sched_max_nodes - e->t_nl.size());
     std::vector<std::vector<pe_action>> prefixes;
     for (auto [v, k] : want) {
       std::vector<pe_action> pth = sched_path(e, v);

@@ -12,7 +12,7 @@ acts = torch.empty(B * maxd * 8, dtype=torch.uint8, device=dev)
 na = torch.empty(B, dtype=torch.int32, device=dev)
 res = torch.empty(B * 192, dtype=torch.uint8, device=dev)
 st = torch.cuda.current_stream(); sp = C.c_void_p(st.cuda_stream)
-for k in range(7):
+for k in range(int(os.environ.get("CALLS", "7"))):
     sd = torch.arange(B, dtype=torch.int64, device=dev) + 10_000_000 + k * B
     torch.cuda.synchronize(); t = time.time()
     eng.rollout_batch_device(None, poff.data_ptr(), sd.data_ptr(), B, acts.data_ptr(), na.data_ptr(), res.data_ptr(), stream=sp)

@@ -32,7 +32,8 @@ for path in sys.argv[1:]:
     def run(k):
         eng.rollout_batch_device(None, poff.data_ptr(), (seeds + k * B).data_ptr(), B,
                                  acts.data_ptr(), na.data_ptr(), res.data_ptr(), stream=sp)
-    run(100)
+    for _w in range(int(os.environ.get("WARM", "1"))):
+        run(100 + _w)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
