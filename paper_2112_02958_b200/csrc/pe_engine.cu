@@ -165,16 +165,38 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
   // k = schedule position; perm (prefix-trie scheduling) maps it to the
   // candidate, so lanes of a warp run candidates that share their first
-  // decisions; results stay in candidate order
-  for (uint32_t k = slot; k < n; k = next_cand<RETRY>(k, slots, ctr)) {
+  // decisions; results stay in candidate order.
+  auto run = [&](uint32_t k) {
     uint32_t i = perm ? perm[k] : k;
-    if (RETRY && out[i].status != PE_CAND_CAPACITY) continue;
+    if (RETRY && out[i].status != PE_CAND_CAPACITY) return;
     pe_result r;
     c.template rollout<RS>(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd,
-                           cp, baseline,
-              acts_out + (uint64_t)i * maxd, n_out + i, r,
-              legal_out ? legal_out + (uint64_t)i * legal_words : nullptr, legal_words);
+                           cp, baseline, acts_out + (uint64_t)i * maxd, n_out + i, r,
+                           legal_out ? legal_out + (uint64_t)i * legal_words : nullptr,
+                           legal_words);
     out[i] = r;
+  };
+  if (RETRY || PE_SOLO) {
+    for (uint32_t k = slot; k < n; k += slots) run(k);
+  } else {
+    // Warp-chunked dynamic schedule: the first wave is position `slot`;
+    // afterwards the warp's lanes take the next consecutive positions
+    // together (lane 0 claims a chunk of the warp's width), so a warp keeps
+    // running neighbours in the sorted order instead of scattering.
+    const unsigned mask = __activemask();
+    const uint32_t width = __popc(mask);
+    const uint32_t rank = __popc(mask & ((1u << (threadIdx.x & 31)) - 1u));
+    // (every lane of `mask` stays in the loop until the warp-uniform exit)
+    uint32_t k = slot;
+    while (true) {
+      if (k < n) run(k);
+      __syncwarp(mask);
+      uint32_t base = 0;
+      if (rank == 0) base = slots + atomicAdd(ctr, width);
+      base = __shfl_sync(mask, base, __ffs(mask) - 1);
+      if (base >= n) break;
+      k = base + rank;
+    }
   }
 #if defined(PE_PHASE_TIMERS) && defined(__CUDA_ARCH__)
   for (int k = 0; k < 9; ++k) atomicAdd(&g_phase_cycles[k], (unsigned long long)c.ph[k]);
