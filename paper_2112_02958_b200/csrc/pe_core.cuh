@@ -935,8 +935,41 @@ struct Cand {
     a.stk()[2 * nstk + 1] = r;
     nstk++;
   }
+  // Stuck analysis (REF propagate.cc:412-454) of one loop-body slice:
+  // a single-use TOP producer whose rule blocks the sliced dim.
+  PE_HD void stuck_slice(int32_t s) {
+    int32_t u = a.vref()[s], d = a.vaux()[s] & 7;
+    if (a.vk()[u] != VK_TOP) return;
+    int32_t P = a.vref()[u];
+    uint8_t kind = g.okind[P];
+    if (kind == kConstant) return;
+    if (a.uses()[u] != 1) return;
+    if (kind == kBroadcastInDim && !((g.omask[P] >> d) & 1)) return;
+    if (g.orule_err[P]) {
+      fail(PE_CAND_INTERNAL);
+      return;
+    }
+    if (g.op_rcls[P * 4 + d] < 0) add_stuck(P, R_BLOCKED);
+  }
+  // ... and of one top-level op with a tiled operand that cannot be pulled
+  PE_HD void stuck_top(int32_t v) {
+    int32_t o = a.vref()[v];
+    if (!has_tiled_operand(o)) return;
+    if (g.orule_err[o]) {
+      fail(PE_CAND_INTERNAL);
+      return;
+    }
+    Pull p = plan_pull(o);
+    if (p.ok) {
+      fail(PE_CAND_INTERNAL);  // "pull available after fixpoint"
+      return;
+    }
+    add_stuck(o, p.reason);
+  }
+  // The stuck list as its own walk (the resurfacing kernel; finish() folds
+  // the same checks into lowering's walk).  `seen` is all-zero between uses
+  // (arenas start zeroed; clear_seen() after the list is consumed).
   PE_HD void analyze() {
-    for (int32_t o = 0; o < g.N; ++o) a.seen()[o] = 0;
     nstk = 0;
     for_top([&](int32_t v) {
       uint8_t k = a.vk()[v];
@@ -944,35 +977,18 @@ struct Cand {
         int32_t l = a.vref()[v];
         for (int32_t s = a.lhead()[l]; s >= 0; s = a.bnext()[s]) {
           if (a.vk()[s] != VK_SLICE) continue;
-          int32_t u = a.vref()[s], d = a.vaux()[s] & 7;
-          if (a.vk()[u] != VK_TOP) continue;
-          int32_t P = a.vref()[u];
-          uint8_t kind = g.okind[P];
-          if (kind == kConstant) continue;
-          if (a.uses()[u] != 1) continue;
-          if (kind == kBroadcastInDim && !((g.omask[P] >> d) & 1)) continue;
-          if (g.orule_err[P]) {
-            fail(PE_CAND_INTERNAL);
-            return;
-          }
-          if (g.op_rcls[P * 4 + d] < 0) add_stuck(P, R_BLOCKED);
+          stuck_slice(s);
+          if (bad()) return;
         }
       } else if (k == VK_TOP) {
-        int32_t o = a.vref()[v];
-        if (!has_tiled_operand(o)) return;
-        if (g.orule_err[o]) {
-          fail(PE_CAND_INTERNAL);
-          return;
-        }
-        Pull p = plan_pull(o);
-        if (p.ok) {
-          fail(PE_CAND_INTERNAL);  // "pull available after fixpoint"
-          return;
-        }
-        add_stuck(o, p.reason);
+        stuck_top(v);
       }
     });
   }
+  PE_HD void clear_seen() {
+    for (int32_t i = 0; i < nstk; ++i) a.seen()[a.stk()[2 * i]] = 0;
+  }
+
 
   // ------------------------------------------------------------ lowering
   PE_HD int32_t rank_of_spec(uint32_t spec) const { return (spec >> 24) & 7; }
@@ -1342,8 +1358,12 @@ struct Cand {
     }
   }
 
-  // lower_to_spmd (REF spmd.cc:328-403)
-  PE_HD void lower() {
+  // lower_to_spmd (REF spmd.cc:328-403).  stuck = also run the stuck
+  // analysis (stuck_top / stuck_slice) on the way: it reads propagation
+  // state only, which lowering never writes, and visits the same positions
+  // and loop bodies in the same order as analyze() -- one walk instead of
+  // two.
+  PE_HD void lower(bool stuck) {
     nem = 0;
     neo = 0;
     flops = 0;
@@ -1379,6 +1399,10 @@ struct Cand {
         return;
       }
       if (k != VK_TOP && k != VK_LOOP) return;
+      if (stuck && k == VK_TOP) {
+        stuck_top(v);
+        if (bad()) return;
+      }
       // A top-level op is lowered as a one-item body, so top-level and
       // per-iteration ops share one inlined lower_base (code size bounds
       // this kernel: instruction-cache stalls).
@@ -1386,8 +1410,15 @@ struct Cand {
       int32_t s = l >= 0 ? a.lhead()[l] : v;
       while (s >= 0) {
         int32_t next = l >= 0 ? a.bnext()[s] : -1;
-        if (l >= 0 && a.vk()[s] == VK_SLICE) lower_slice(s, l);
-        else lower_base(s, a.vref()[s], l);
+        if (l >= 0 && a.vk()[s] == VK_SLICE) {
+          if (stuck) {
+            stuck_slice(s);
+            if (bad()) return;
+          }
+          lower_slice(s, l);
+        } else {
+          lower_base(s, a.vref()[s], l);
+        }
         if (bad()) return;
         s = next;
       }
@@ -1503,13 +1534,23 @@ struct Cand {
   }
 
   // ------------------------------------------------------------ drivers
+  // separate = run analyze() as its own walk before lowering (the
+  // resurfacing kernel); otherwise the stuck analysis rides on lowering
   PE_HD void finish(const pe_cost_params& cp, int64_t baseline, int32_t steps,
-                    bool propagated, pe_result& r, int32_t* trace, uint32_t trace_words) {
+                    bool propagated, pe_result& r, int32_t* trace, uint32_t trace_words,
+                    bool separate = false) {
     tick(5);
-    if (!bad() && propagated) analyze();
+    nstk = 0;
+    if (separate && !bad() && propagated) analyze();
     tick(6);
-    if (!bad()) lower();
+    if (!bad()) lower(!separate && propagated);
     tick(7);
+    finish_result(cp, baseline, steps, propagated, r, trace, trace_words);
+    clear_seen();
+    tick(8);
+  }
+  PE_HD void finish_result(const pe_cost_params& cp, int64_t baseline, int32_t steps,
+                           bool propagated, pe_result& r, int32_t* trace, uint32_t trace_words) {
     if (bad()) {
       int32_t st = status;
       for (int x = 0; x < PE_MAX_AXES; ++x) {
@@ -1534,7 +1575,6 @@ struct Cand {
     r.status = status;
     r.fail_step = fs;
     if (trace && trace_words) write_trace(trace, trace_words);
-    tick(8);
   }
 
   // argflags (optional, A bytes): bit 0 = argument sliced, bit 1 = atomic
@@ -1592,14 +1632,14 @@ struct Cand {
   // order) join the worklist once each.  Called at every decision boundary.
   PE_HD void resurface_update() {
     analyze();
-    if (bad()) return;
-    for (int32_t i = 0; i < nstk; ++i) {
+    for (int32_t i = 0; i < nstk && !bad(); ++i) {
       int32_t o = a.stk()[2 * i];
       uint32_t bit = 1u << (o & 31);
       if (a.rsb()[o >> 5] & bit) continue;
       a.rsb()[o >> 5] |= bit;
       a.rs()[nrs++] = o;
     }
+    clear_seen();
   }
   // Legal TileValue ordinals in worklist order (SPEC legal_actions): the
   // static entries, then the resurfaced ops in discovery order; a

@@ -516,7 +516,12 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
                "cudaMalloc(arena)") ||
       !cuda_ok(cudaMalloc(&e->d_big_arena, (size_t)big_groups * e->big_layout.bytes), err,
                "cudaMalloc(big arena)") ||
-      !cuda_ok(cudaMalloc(&e->d_ctr, 4 * sizeof(uint32_t)), err, "cudaMalloc(counters)")) {
+      !cuda_ok(cudaMalloc(&e->d_ctr, 4 * sizeof(uint32_t)), err, "cudaMalloc(counters)") ||
+      // arenas start zeroed: the per-op `seen` marks of the stuck analysis
+      // are cleared by each candidate after use, never wholesale
+      !cuda_ok(cudaMemset(e->d_arena, 0, (size_t)groups * e->layout.bytes), err, "zero arena") ||
+      !cuda_ok(cudaMemset(e->d_big_arena, 0, (size_t)big_groups * e->big_layout.bytes), err,
+               "zero arena")) {
     pe_engine_destroy(e);
     return PE_ERR_CUDA;
   }

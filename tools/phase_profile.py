@@ -27,7 +27,8 @@ B = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 for cfgno in (3,):
     text = modelgen.config_program(cfgno)
     eng = engine.Engine(engine.Graph(text), cfg=capi.default_search_config(group_scopes=1))
-    eng.rollout_batch([[]] * 1024, list(range(1024)))
+    for w in range(4):  # warm the scheduling trie with full-size calls
+        eng.rollout_batch([[]] * B, list(range(10_000_000 + w * B, 10_000_000 + (w + 1) * B)))
     buf = (C.c_ulonglong * 9)()
     lib.pe_debug_phase_cycles(buf, 1)
     t = time.time()
