@@ -495,9 +495,11 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   }
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  // arena budget: up to 45 % of free HBM (two engines may coexist in one
-  // process), at most 96 GiB; PE_ARENA_BUDGET_GB overrides
-  size_t budget = std::min<size_t>((size_t)(free_b * 0.45), (size_t)96 << 30);
+  // arena budget: up to 70 % of free HBM, at most 120 GiB (a second engine
+  // created later sizes itself from what is then free; the rest is headroom
+  // for the caller's buffers); PE_ARENA_BUDGET_GB overrides.  Large graphs
+  // (config 4: 5.4 MB per candidate) are slot-limited by this budget.
+  size_t budget = std::min<size_t>((size_t)(free_b * 0.70), (size_t)120 << 30);
   if (const char* gb = std::getenv("PE_ARENA_BUDGET_GB"))
     budget = std::min<size_t>(free_b, (size_t)(std::atof(gb) * (double)(1ull << 30)));
   // one resident thread per slot: kMinBlocks blocks of kBlock threads per SM;
