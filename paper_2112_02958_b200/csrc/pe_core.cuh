@@ -508,6 +508,67 @@ struct Cand {
     result_buf = -1;
   }
 
+  // ------------------------------------------------------------ snapshots
+  // The state after a decision prefix (prefix-trie scheduling, DESIGN.md
+  // §3.5), compact and lane-independent: what init() sets up and apply /
+  // propagate write -- value, loop and argument records, operand slots,
+  // front stack, carry bits, counters.  Lowering state is rebuilt by
+  // lower(); after a whole propagate the dirty bits are clear and the
+  // pending-slice list is empty.  (Engines with stuck resurfacing do not
+  // schedule, so rs / rsb need no snapshot.)
+  PE_HD static uint64_t snap_bytes(const GraphView& g, const Caps& caps) {
+    return 16ull * (1 + 2ull * caps.V + 2ull * caps.L + (uint64_t)g.A) +
+           4ull * ((uint64_t)g.E + caps.FS + (uint64_t)(g.A >> 5) + 1);
+  }
+  PE_HD void save(uint8_t* dst) const {
+    V4* p = reinterpret_cast<V4*>(dst);
+    *p++ = V4{nslots, nloops, nfs, result_ref};
+    for (int32_t v = 0; v < nslots; ++v) {
+      *p++ = a.vr0()[v];
+      *p++ = a.vr1()[v];
+    }
+    for (int32_t l = 0; l < nloops; ++l) {
+      *p++ = a.lq0()[l];
+      *p++ = a.lq1()[l];
+    }
+    for (int32_t x = 0; x < g.A; ++x) *p++ = a.ar0()[x];
+    int32_t* q = reinterpret_cast<int32_t*>(p);
+    for (int32_t s = 0; s < g.E; ++s) *q++ = a.opnd()[s];
+    for (int32_t i = 0; i < nfs; ++i) *q++ = a.fs()[i];
+    for (int32_t w = 0; w <= (g.A >> 5); ++w) *q++ = (int32_t)a.carry()[w];
+  }
+  // init() for a candidate that starts from a saved prefix state
+  PE_HD void load(const uint8_t* src) {
+    const V4* p = reinterpret_cast<const V4*>(src);
+    V4 h = *p++;
+    nslots = h.x;
+    nloops = h.y;
+    nfs = h.z;
+    result_ref = h.w;
+    for (int32_t v = 0; v < nslots; ++v) {
+      a.vr0()[v] = *p++;
+      a.vr1()[v] = *p++;
+    }
+    for (int32_t l = 0; l < nloops; ++l) {
+      a.lq0()[l] = *p++;
+      a.lq1()[l] = *p++;
+    }
+    for (int32_t x = 0; x < g.A; ++x) a.ar0()[x] = *p++;
+    const int32_t* q = reinterpret_cast<const int32_t*>(p);
+    for (int32_t s = 0; s < g.E; ++s) a.opnd()[s] = *q++;
+    for (int32_t i = 0; i < nfs; ++i) a.fs()[i] = *q++;
+    for (int32_t w = 0; w <= (g.A >> 5); ++w) a.carry()[w] = (uint32_t)*q++;
+    for (int32_t w = 0; w <= (g.N >> 5); ++w) a.dirty()[w] = 0;
+    nrs = 0;
+    pend = -1;
+    nem = 0;
+    neo = 0;
+    nstk = 0;
+    status = PE_CAND_OK;
+    flops = 0;
+    result_buf = -1;
+  }
+
   // ------------------------------------------------------------ actions
   // carries_tiling (REF rewrite.cc:42-51) for an original value at top level
   PE_HD bool carries(int32_t v) const {
@@ -1697,17 +1758,33 @@ struct Cand {
   // the default kernel carries none of its code (code size bounds this
   // kernel: instruction-cache stalls).
   template <bool RS>
+  //
+  // snap (prefix-state reuse): start from the saved state
+  // after the candidate's first snap_d decisions -- `snap_path`, which its
+  // own seed draws (the scheduler matched them; snap_stop: its next draw is
+  // Stop) -- instead of init() and replaying them.  Only for root rollouts
+  // (np == 0) without legal output.
   PE_HD void rollout(const pe_action* prefix, int32_t np, uint64_t seed, int32_t maxd,
                      const pe_cost_params& cp, int64_t baseline, pe_action* acts_out,
-                     uint32_t* n_out, pe_result& r, uint64_t* legal_out, int32_t legal_words) {
+                     uint32_t* n_out, pe_result& r, uint64_t* legal_out, int32_t legal_words,
+                     const uint8_t* snap = nullptr, int32_t snap_d = 0,
+                     const pe_action* snap_path = nullptr, bool snap_stop = false) {
     tracing = false;
     tick_start();
-    init();
+    int32_t steps = 0, nacts = 0;
+    bool propagated = false, terminal = false;
+    if (snap) {
+      load(snap);
+      for (int32_t k = 0; k < snap_d && k < maxd; ++k) acts_out[k] = snap_path[k];
+      steps = nacts = snap_d;
+      propagated = snap_d > 0;
+      terminal = snap_stop;
+    } else {
+      init();
+    }
     tick(0);
     r.fail_step = -1;
     r.reserved = 0;
-    int32_t steps = 0, nacts = 0;
-    bool propagated = false, terminal = false;
     if (legal_out)
       for (int32_t w = 0; w < legal_words; ++w) legal_out[w] = 0;
     // resurfacing runs at decision boundaries: before the next decision of
@@ -1760,7 +1837,8 @@ struct Cand {
         int32_t nl = build_legal<RS>();
         for (int32_t i = 0; i < nl; ++i) legal_out[a.lg()[i] >> 6] |= 1ull << (a.lg()[i] & 63);
       }
-      uint64_t st = seed;
+      // (each decision draws once: splitmix adds the golden gamma per draw)
+      uint64_t st = seed + (uint64_t)snap_d * 0x9E3779B97F4A7C15ull;
       while (!terminal) {
         if (steps >= maxd) break;
         tick(4);

@@ -71,6 +71,16 @@ struct pe_engine {
   uint32_t* d_hist = nullptr;
   size_t sched_cap = 0, perm_cap = 0, hist_cap = 0;
   uint64_t sched_probes = 0;  // prefix states probed (diagnostic)
+  // prefix-state reuse: per node its decision path and snapshot index
+  int32_t path_cap = 3;
+  std::vector<pe_action> t_path;
+  std::vector<int32_t> t_snap;
+  pe_action* d_tpath = nullptr;
+  size_t tpath_cap = 0;
+  uint8_t* d_snap = nullptr;
+  uint64_t snap_stride = 0;
+  int32_t snap_cap = 0, snap_used = 0;
+  double snap_budget_gb = 8.0;
 };
 
 namespace {
@@ -146,6 +156,18 @@ pe_eval_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ 
   }
 }
 
+// Prefix-state reuse: per candidate its trie key (2 * node,
+// +1 when its next draw is Stop), per node {nl, child offset, depth,
+// snapshot index or -1} and its decision path, and the snapshot pool.
+struct SchedView {
+  const uint32_t* keys = nullptr;
+  const int4* tnode = nullptr;
+  const pe_action* tpath = nullptr;
+  int32_t path_cap = 0;
+  const uint8_t* snap = nullptr;
+  uint64_t stride = 0;
+};
+
 template <bool RETRY, bool RS>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
 pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
@@ -153,7 +175,8 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                   const pe_action* prefix, const uint32_t* poff, const uint64_t* seeds,
                   uint32_t n, int32_t maxd, pe_cost_params cp, int64_t baseline,
                   pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
-                  int32_t legal_words, uint32_t* ctr, const uint32_t* perm) {
+                  int32_t legal_words, uint32_t* ctr, const uint32_t* perm,
+                  const __grid_constant__ SchedView sv) {
 #if PE_SOLO
   // experiment: one active lane per warp (no SIMT divergence across candidates)
   if (threadIdx.x % 32) return;
@@ -169,11 +192,26 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
   auto run = [&](uint32_t k) {
     uint32_t i = perm ? perm[k] : k;
     if (RETRY && out[i].status != PE_CAND_CAPACITY) return;
+    // start from the saved state of the candidate's trie node when there is one
+    const uint8_t* snap = nullptr;
+    const pe_action* spath = nullptr;
+    int32_t sd = 0;
+    bool sstop = false;
+    if (sv.keys) {
+      uint32_t key = sv.keys[i];
+      int4 nd = sv.tnode[key >> 1];
+      if (nd.w >= 0) {
+        snap = sv.snap + sv.stride * (uint64_t)nd.w;
+        sd = nd.z;
+        spath = sv.tpath + (uint64_t)(key >> 1) * sv.path_cap;
+        sstop = (key & 1u) != 0;
+      }
+    }
     pe_result r;
     c.template rollout<RS>(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd,
                            cp, baseline, acts_out + (uint64_t)i * maxd, n_out + i, r,
                            legal_out ? legal_out + (uint64_t)i * legal_words : nullptr,
-                           legal_words);
+                           legal_words, snap, sd, spath, sstop);
     out[i] = r;
   };
   if (RETRY || PE_SOLO) {
@@ -204,6 +242,28 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
 }
 
 // ---- prefix-trie scheduling kernels ----
+// Probe: evaluates each prefix (no decisions after it), records the legal
+// set after it and saves the state after it as the node's snapshot.
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
+pe_probe_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
+                uint8_t* arena, uint32_t slots, const pe_action* prefix, const uint32_t* poff,
+                uint32_t n, int32_t acts_stride, pe_cost_params cp, int64_t baseline,
+                pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
+                int32_t legal_words, uint8_t* snap, uint64_t stride, const int32_t* snap_idx) {
+  uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= slots) return;
+  pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
+  for (uint32_t k = slot; k < n; k += slots) {
+    int32_t np = (int32_t)(poff[k + 1] - poff[k]);
+    pe_result r;
+    c.template rollout<false>(prefix + poff[k], np, 0, np, cp, baseline,
+                              acts_out + (uint64_t)k * acts_stride, n_out + k, r,
+                              legal_out + (uint64_t)k * legal_words, legal_words);
+    out[k] = r;
+    if (snap_idx[k] >= 0 && r.status == PE_CAND_OK) c.save(snap + stride * (uint64_t)snap_idx[k]);
+  }
+}
+
 // Walks candidate i's seed through the trie with exactly the rollout's
 // draws (Cand::rollout: no draw when nothing is legal; Stop weight 1 before
 // the first decision, 2 after) and keys it by the deepest known node (odd
@@ -486,6 +546,8 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   if (const char* sd = std::getenv("PE_SCHED_DEPTH")) e->sched_depth = std::atoi(sd);
   if (const char* sm = std::getenv("PE_SCHED_MIN_BATCH")) e->sched_min_batch = (uint32_t)std::atoi(sm);
   if (const char* sn = std::getenv("PE_SCHED_MAX_NODES")) e->sched_max_nodes = std::atoi(sn);
+  if (const char* sg = std::getenv("PE_SCHED_SNAP_GB")) e->snap_budget_gb = std::atof(sg);
+  e->path_cap = std::max(1, e->sched_depth);
   if (const char* dbg = std::getenv("PE_DEBUG_TIGHT_EM_CAP")) {
     // test hook: shrink the tight arena so candidates overflow and take the
     // retry path (tests/test_gpu_parity.py::test_capacity_retry_path)
@@ -556,7 +618,7 @@ void pe_engine_destroy(pe_engine* e) {
   if (e->d_big_arena) cudaFree(e->d_big_arena);
   if (e->d_ctr) cudaFree(e->d_ctr);
   for (void* q : {(void*)e->d_tnode, (void*)e->d_tchild, (void*)e->d_tmiss, (void*)e->d_keys,
-                  (void*)e->d_perm, (void*)e->d_hist})
+                  (void*)e->d_perm, (void*)e->d_hist, (void*)e->d_tpath, (void*)e->d_snap})
     if (q) cudaFree(q);
   if (e->d_io) cudaFree(e->d_io);
   delete e;
@@ -797,7 +859,8 @@ namespace {
 // output is taken right after the prefix.  Own buffers: the caller's inputs
 // may live in the staging buffer.
 bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefixes,
-                 std::vector<std::vector<int32_t>>& legal, cudaStream_t st, pe_error* err) {
+                 const std::vector<int32_t>& snap_idx, std::vector<std::vector<int32_t>>& legal,
+                 std::vector<int32_t>& status, cudaStream_t st, pe_error* err) {
   uint32_t n = (uint32_t)prefixes.size();
   std::vector<pe_action> acts;
   std::vector<uint32_t> off{0};
@@ -810,12 +873,16 @@ bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefix
   int32_t maxd = std::max(1, maxlen);
   int32_t lw = (int32_t)pe_engine_legal_words(e);
   size_t b_acts = std::max<size_t>(1, acts.size()) * sizeof(pe_action);
-  size_t sizes[7] = {b_acts, (n + 1) * 4ull, n * 8ull, (size_t)n * maxd * sizeof(pe_action),
-                     n * 4ull, n * sizeof(pe_result), (size_t)n * lw * 8};
-  void* buf[7] = {};
+  size_t sizes[8] = {b_acts, (n + 1) * 4ull, n * 8ull, (size_t)n * maxd * sizeof(pe_action),
+                     n * 4ull, n * sizeof(pe_result), (size_t)n * lw * 8, n * 4ull};
+  void* buf[8] = {};
   bool ok = true;
-  for (int k = 0; k < 7 && ok; ++k) ok = cuda_ok(cudaMalloc(&buf[k], sizes[k]), err, "cudaMalloc(probe)");
+  for (int k = 0; k < 8 && ok; ++k) ok = cuda_ok(cudaMalloc(&buf[k], sizes[k]), err, "cudaMalloc(probe)");
   std::vector<uint64_t> lg((size_t)n * lw);
+  std::vector<pe_result> res(n);
+  if (ok)
+    ok = cuda_ok(cudaMemcpyAsync(buf[7], snap_idx.data(), n * 4ull, cudaMemcpyHostToDevice, st),
+                 err, "H2D probe");
   if (ok) {
     ok = (acts.empty() || cuda_ok(cudaMemcpyAsync(buf[0], acts.data(), acts.size() * sizeof(pe_action),
                                                   cudaMemcpyHostToDevice, st), err, "H2D probe")) &&
@@ -826,24 +893,30 @@ bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefix
   }
   if (ok) {
     uint32_t slots = launch_slots(e, n), bs = std::min<uint32_t>(e->big_slots, n);
-    pe_rollout_kernel<false, false><<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+    pe_probe_kernel<<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
         e->dview, e->layout, e->d_arena, slots, (const pe_action*)buf[0], (const uint32_t*)buf[1],
-        (const uint64_t*)buf[2], n, maxd, e->cp, e->baseline, (pe_action*)buf[3],
-        (uint32_t*)buf[4], (pe_result*)buf[5], (uint64_t*)buf[6], lw, e->d_ctr + 2, nullptr);
+        n, maxd, e->cp, e->baseline, (pe_action*)buf[3], (uint32_t*)buf[4], (pe_result*)buf[5],
+        (uint64_t*)buf[6], lw, e->d_snap, e->snap_stride, (const int32_t*)buf[7]);
+    // overflowed probes: legal sets from full-size arenas (no snapshot); the
+    // uniform maxd only adds draws after the prefix, its legal set is final
     pe_rollout_kernel<true, false><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
         e->dview, e->big_layout, e->d_big_arena, bs, (const pe_action*)buf[0],
         (const uint32_t*)buf[1], (const uint64_t*)buf[2], n, maxd, e->cp, e->baseline,
         (pe_action*)buf[3], (uint32_t*)buf[4], (pe_result*)buf[5], (uint64_t*)buf[6], lw,
-        nullptr, nullptr);
+        nullptr, nullptr, SchedView());
     e->launches += 2;
     ok = cuda_ok(cudaGetLastError(), err, "probe launch") &&
          cuda_ok(cudaMemcpyAsync(lg.data(), buf[6], sizes[6], cudaMemcpyDeviceToHost, st), err,
                  "D2H probe") &&
+         cuda_ok(cudaMemcpyAsync(res.data(), buf[5], sizes[5], cudaMemcpyDeviceToHost, st), err,
+                 "D2H probe") &&
          cuda_ok(cudaStreamSynchronize(st), err, "probe sync");
   }
-  for (int k = 0; k < 7; ++k)
+  for (int k = 0; k < 8; ++k)
     if (buf[k]) cudaFree(buf[k]);
   if (!ok) return false;
+  status.assign(n, 0);
+  for (uint32_t i = 0; i < n; ++i) status[i] = res[i].status;
   legal.assign(n, {});
   for (uint32_t i = 0; i < n; ++i)
     for (int32_t o = 0; o < (int32_t)e->n_ordinals; ++o)
@@ -863,7 +936,17 @@ int32_t sched_add_node(pe_engine* e, int32_t parent, int32_t pick,
   e->t_depth.push_back(parent < 0 ? 0 : e->t_depth[parent] + 1);
   e->t_parent.push_back(parent);
   e->t_pick.push_back(pick);
-  if (parent >= 0) e->t_child[e->t_child_off[parent] + pick] = id;
+  e->t_snap.push_back(-1);
+  e->t_path.resize((size_t)(id + 1) * e->path_cap, pe_action{0, 0, 0, PE_ACT_STOP, 0});
+  if (parent >= 0) {
+    e->t_child[e->t_child_off[parent] + pick] = id;
+    for (int32_t k = 0; k < e->path_cap; ++k)
+      e->t_path[(size_t)id * e->path_cap + k] = e->t_path[(size_t)parent * e->path_cap + k];
+    int32_t d = e->t_depth[id];
+    if (d <= e->path_cap)
+      pe_engine_ordinal_action(e, (uint32_t)e->t_legal[e->t_legal_off[parent] + pick],
+                               &e->t_path[(size_t)id * e->path_cap + d - 1]);
+  }
   e->t_dirty = true;
   return id;
 }
@@ -910,7 +993,14 @@ bool sched_upload(pe_engine* e, cudaStream_t st, pe_error* err) {
     tn[4 * v] = e->t_nl[v];
     tn[4 * v + 1] = e->t_child_off[v];
     tn[4 * v + 2] = e->t_depth[v];
+    tn[4 * v + 3] = e->t_snap[v];
   }
+  if (!ensure_dev(e->d_tpath, e->tpath_cap, std::max<size_t>(1, e->t_path.size()), err,
+                  "cudaMalloc(trie)") ||
+      (!e->t_path.empty() &&
+       !cuda_ok(cudaMemcpyAsync(e->d_tpath, e->t_path.data(), e->t_path.size() * sizeof(pe_action),
+                                cudaMemcpyHostToDevice, st), err, "H2D trie")))
+    return false;
   if (!cuda_ok(cudaMemcpyAsync(e->d_tnode, tn.data(), tn.size() * 4, cudaMemcpyHostToDevice, st),
                err, "H2D trie") ||
       (!e->t_child.empty() &&
@@ -929,13 +1019,26 @@ bool sched_upload(pe_engine* e, cudaStream_t st, pe_error* err) {
 // (the prefix states the batch reached but the trie lacks).  Returns the
 // device permutation, or nullptr (identity) when scheduling is off.
 bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
-                cudaStream_t st, const uint32_t** perm, pe_error* err) {
+                cudaStream_t st, const uint32_t** perm, SchedView* sv, pe_error* err) {
   *perm = nullptr;
+  *sv = SchedView();
   int32_t depth = std::min(e->sched_depth, maxd);
   if (depth <= 0) return true;
+  if (!e->d_snap && e->snap_budget_gb > 0) {
+    // snapshot pool for prefix-state reuse: one slot per trie node while the
+    // budget lasts (nodes without one fall back to the full computation)
+    e->snap_stride = (pe::Cand::snap_bytes(e->dview, e->layout.caps) + 255) & ~uint64_t(255);
+    uint64_t cap = (uint64_t)(e->snap_budget_gb * (double)(1ull << 30)) / e->snap_stride;
+    e->snap_cap = (int32_t)std::min<uint64_t>(cap, (uint64_t)e->sched_max_nodes);
+    if (e->snap_cap > 0 &&
+        !cuda_ok(cudaMalloc(&e->d_snap, (size_t)e->snap_cap * e->snap_stride), err,
+                 "cudaMalloc(snapshots)"))
+      return false;
+  }
   if (e->t_nl.empty()) {
     std::vector<std::vector<int32_t>> lg;
-    if (!sched_probe(e, {{}}, lg, st, err)) return false;
+    std::vector<int32_t> stat;
+    if (!sched_probe(e, {{}}, {-1}, lg, stat, st, err)) return false;  // root: init() state
     sched_add_node(e, -1, 0, lg[0]);
   }
   if (!ensure_dev(e->d_keys, e->sched_cap, n, err, "cudaMalloc(sched)") ||
@@ -985,15 +1088,26 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
       pth.push_back(a);
       prefixes.push_back(std::move(pth));
     }
+    std::vector<int32_t> sidx(want.size(), -1), stat;
+    for (size_t q = 0; q < want.size() && e->snap_used < e->snap_cap; ++q) sidx[q] = e->snap_used++;
     std::vector<std::vector<int32_t>> lg;
-    if (!sched_probe(e, prefixes, lg, st, err)) return false;
-    for (size_t q = 0; q < want.size(); ++q) sched_add_node(e, want[q].first, want[q].second, lg[q]);
+    if (!sched_probe(e, prefixes, sidx, lg, stat, st, err)) return false;
+    for (size_t q = 0; q < want.size(); ++q) {
+      int32_t id = sched_add_node(e, want[q].first, want[q].second, lg[q]);
+      e->t_snap[id] = stat[q] == PE_CAND_OK ? sidx[q] : -1;
+    }
   }
   pe_sched_scan_kernel<<<1, 1024, 0, st>>>(e->d_hist, m);
   pe_sched_scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, e->d_keys, e->d_hist, e->d_perm);
   e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "sched sort launch")) return false;
   *perm = e->d_perm;
+  sv->keys = e->d_keys;
+  sv->tnode = (const int4*)e->d_tnode;
+  sv->tpath = e->d_tpath;
+  sv->path_cap = e->path_cap;
+  sv->snap = e->d_snap;
+  sv->stride = e->snap_stride;
   return true;
 }
 
@@ -1060,10 +1174,14 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   // prefix-trie scheduling for batches of root rollouts (all prefixes
   // empty; a NULL prefix array in device mode), DESIGN.md §3.5
   const uint32_t* perm = nullptr;
+  SchedView sv;
   bool roots = (flags & PE_MEM_DEVICE) ? prefix == nullptr : prefix_off[n] == 0;
   if (roots && e->sched_depth > 0 && !e->wl.resurface && n >= e->sched_min_batch &&
-      !sched_perm(e, n, d_seeds, maxd, st, &perm, err))
+      !sched_perm(e, n, d_seeds, maxd, st, &perm, &sv, err))
     return PE_ERR_CUDA;
+  // candidates start from their node's saved state unless legal sets after
+  // the (empty) prefix are requested
+  if (d_legal || !sv.snap) sv.keys = nullptr;
   uint32_t slots = launch_slots(e, n);
   if (!cuda_ok(cudaMemsetAsync(e->d_ctr + 1, 0, sizeof(uint32_t), st), err,
                "reset work counter"))
@@ -1075,10 +1193,11 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   auto launch = [&](auto main_k, auto retry_k) {
     main_k<<<grid, kBlock, 0, st>>>(e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
                                     d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts, d_out,
-                                    d_legal, lw, e->d_ctr + 1, perm);
+                                    d_legal, lw, e->d_ctr + 1, perm, sv);
     retry_k<<<bgrid, kBlock, 0, st>>>(e->dview, e->big_layout, e->d_big_arena, bs, d_prefix,
                                       d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
-                                      d_nacts, d_out, d_legal, lw, nullptr, nullptr);
+                                      d_nacts, d_out, d_legal, lw, nullptr, nullptr,
+                                      SchedView());
   };
   if (e->wl.resurface)
     launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>);

@@ -102,7 +102,7 @@ int harness_rollout_batch(const char* pir, size_t len, const pe_search_config* c
   for (uint32_t i = 0; i < n; ++i)
     (c.*ro)(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, h.cp,
             h.baseline, acts_out + (size_t)i * maxd, n_out + i, out[i],
-            legal_out ? legal_out + (size_t)i * lw : nullptr, lw);
+            legal_out ? legal_out + (size_t)i * lw : nullptr, lw, nullptr, 0, nullptr, false);
   return 0;
 }
 
@@ -127,6 +127,36 @@ int harness_highwater(const char* pir, size_t len, const pe_search_config* cfg,
     out5[2] = std::max<int64_t>(out5[2], c.nfs);
     out5[3] = std::max<int64_t>(out5[3], c.nem);
     out5[4] = std::max<int64_t>(out5[4], c.neo);
+  }
+  return 0;
+}
+
+// Prefix-state reuse check: every seed's rollout is run,
+// the state after its first min(d, decisions) decisions is saved from a
+// second candidate, and the rollout is resumed from that snapshot; the
+// resumed actions and results are returned (they must equal a rollout from
+// the root).
+int harness_resume_rollouts(const char* pir, size_t len, const pe_search_config* cfg,
+                            const pe_cost_params* cp, const uint64_t* seeds, uint32_t n, int32_t d,
+                            pe_action* acts_out, uint32_t* n_out, pe_result* out, char* err,
+                            size_t errcap) {
+  Harness h;
+  int rc = setup(h, pir, len, cfg, cp, err, errcap);
+  if (rc) return rc;
+  std::vector<uint8_t> arena2(h.L.bytes, 0);
+  pe::Cand c(h.v, h.L, h.arena.data()), c2(h.v, h.L, arena2.data());
+  int32_t maxd = (int32_t)h.cfg.max_decisions;
+  std::vector<pe_action> acts(maxd), tmp(maxd);
+  std::vector<uint8_t> snap(pe::Cand::snap_bytes(h.v, h.L.caps));
+  for (uint32_t i = 0; i < n; ++i) {
+    uint32_t na = 0, nt = 0;
+    pe_result r;
+    c.rollout<false>(nullptr, 0, seeds[i], maxd, h.cp, h.baseline, acts.data(), &na, r, nullptr, 0);
+    int32_t k = std::min<int32_t>(d, (int32_t)na);
+    c2.rollout<false>(acts.data(), k, 0, k, h.cp, h.baseline, tmp.data(), &nt, r, nullptr, 0);
+    c2.save(snap.data());
+    c.rollout<false>(nullptr, 0, seeds[i], maxd, h.cp, h.baseline, acts_out + (size_t)i * maxd,
+                     n_out + i, out[i], nullptr, 0, snap.data(), k, acts.data(), false);
   }
   return 0;
 }
