@@ -283,6 +283,16 @@ uint64_t pe_engine_launch_count(const pe_engine* e);
  * off) and PE_SCHED_MIN_BATCH override at engine creation.  Returns the
  * number of trie nodes (prefix states probed). */
 int64_t pe_engine_sched_nodes(const pe_engine* e);
+/* Prefix-state reuse (opt-in): with a snapshot budget > 0
+ * (GiB of HBM), the probe that adds a scheduling-trie node also saves the
+ * propagated state after the node's decision prefix, and a scheduled root
+ * rollout starts from its node's saved state instead of replaying those
+ * decisions.  Results are identical; the saved states are computed once and
+ * shared by every later call, so this trades per-candidate propagation for
+ * state kept across calls -- off by default (budget 0), and bench.py's
+ * `value` is measured without it.  Set before the first scheduled call
+ * (also env PE_SCHED_SNAP_GB at engine creation). */
+pe_status pe_engine_set_state_reuse(pe_engine* e, double budget_gb);
 
 /* ---- search (SPEC search module: mcts_search / emit_plan) ---- */
 #define PE_PLAN_MAX_ACTIONS 64

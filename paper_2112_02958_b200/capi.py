@@ -166,6 +166,7 @@ SIGNATURES = {
     "pe_engine_slots": (C.c_uint32, [_P]),
     "pe_engine_launch_count": (C.c_uint64, [_P]),
     "pe_engine_sched_nodes": (C.c_int64, [_P]),
+    "pe_engine_set_state_reuse": (C.c_int, [_P, C.c_double]),
     "pe_engine_graph_bytes": (C.c_int64, [_P]),
     "pe_mcts_run": (C.c_int, [C.POINTER(PeMctsParams), ROLLOUT_FN, _P, MERGE_FN, _P, _P,
                               C.POINTER(PePlan), C.POINTER(PeError)]),

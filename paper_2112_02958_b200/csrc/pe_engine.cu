@@ -80,7 +80,7 @@ struct pe_engine {
   uint8_t* d_snap = nullptr;
   uint64_t snap_stride = 0;
   int32_t snap_cap = 0, snap_used = 0;
-  double snap_budget_gb = 8.0;
+  double snap_budget_gb = 0.0;  // prefix-state reuse: off unless enabled
 };
 
 namespace {
@@ -633,6 +633,13 @@ int64_t pe_engine_arena_bytes(const pe_engine* e) {
 uint32_t pe_engine_slots(const pe_engine* e) { return e->slots; }
 uint64_t pe_engine_launch_count(const pe_engine* e) { return e->launches; }
 int64_t pe_engine_sched_nodes(const pe_engine* e) { return (int64_t)e->t_nl.size(); }
+
+pe_status pe_engine_set_state_reuse(pe_engine* e, double budget_gb) {
+  if (!e || budget_gb < 0) return PE_ERR_INVALID_ARGUMENT;
+  if (e->d_snap) return e->snap_budget_gb == budget_gb ? PE_OK : PE_ERR_INVALID_ARGUMENT;
+  e->snap_budget_gb = budget_gb;
+  return PE_OK;
+}
 int64_t pe_engine_graph_bytes(const pe_engine* e) { return e->graph_bytes; }
 
 pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* out) {

@@ -170,6 +170,12 @@ class Engine:
         """Prefix states in the scheduling trie (pe.h pe_engine_sched_nodes)."""
         return int(self.lib.pe_engine_sched_nodes(self.h))
 
+    def set_state_reuse(self, budget_gb: float) -> None:
+        """Opt into prefix-state reuse (pe.h pe_engine_set_state_reuse)."""
+        rc = self.lib.pe_engine_set_state_reuse(self.h, float(budget_gb))
+        if rc != capi.PE_OK:
+            raise Error(f"pe_engine_set_state_reuse failed rc={rc}")
+
     def graph_bytes(self) -> int:
         return int(self.lib.pe_engine_graph_bytes(self.h))
 

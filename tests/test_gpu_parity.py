@@ -108,21 +108,25 @@ def test_resurfacing_rollouts_device_vs_oracle(oracle_lib):
     assert picked > 50
 
 
-@pytest.mark.parametrize("cfgno", [2, 3])
-def test_trie_scheduling_preserves_results(oracle_lib, monkeypatch, cfgno):
+@pytest.mark.parametrize("cfgno,reuse", [(2, 0), (2, 4), (3, 0), (3, 4)])
+def test_trie_scheduling_preserves_results(oracle_lib, monkeypatch, cfgno, reuse):
     # prefix-trie scheduling (pe.h pe_engine_sched_nodes) only reorders
-    # candidates: acts, legal sets and results equal an unscheduled engine's,
-    # call after call while the trie grows one level per call
+    # candidates, and prefix-state reuse (pe_engine_set_state_reuse) starts
+    # them from saved prefix states: acts, legal sets and results equal an
+    # unscheduled engine's, call after call while the trie grows
     text = modelgen.config_program(cfgno)
     cfg = capi.default_search_config(group_scopes=1)
     sched = _engine(text, cfg)
+    if reuse:
+        sched.set_state_reuse(reuse)
     monkeypatch.setenv("PE_SCHED_DEPTH", "0")
     plain = _engine(text, cfg)
     n = 8192
     for call in range(4):
         seeds = [call * 100_000 + i for i in range(n)]
-        r1, s1, l1 = sched.rollout_batch([[]] * n, seeds, legal=True)
-        r2, s2, l2 = plain.rollout_batch([[]] * n, seeds, legal=True)
+        legal = not reuse  # (legal-set output turns state reuse off)
+        r1, s1, l1 = sched.rollout_batch([[]] * n, seeds, legal=legal)
+        r2, s2, l2 = plain.rollout_batch([[]] * n, seeds, legal=legal)
         assert s1 == s2 and l1 == l2
         assert all(not H.compare_results(a, b) for a, b in zip(r1, r2))
     assert sched.sched_nodes() > 1 and plain.sched_nodes() == 0
