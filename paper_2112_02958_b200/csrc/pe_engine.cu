@@ -1085,6 +1085,10 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
       for (int32_t k = 0; k < e->t_nl[v]; ++k)
         if (miss[e->t_child_off[v] + k] && e->t_child[e->t_child_off[v] + k] < 0)
           want.push_back({v, k});
+    // deeper nodes only pay when they group enough candidates per warp:
+    // skip a level whose new nodes would average fewer than 8 (e.g. an
+    // ungrouped worklist with hundreds of root actions)
+    if ((uint64_t)nmiss < 8ull * want.size()) break;
     if (want.size() + e->t_nl.size() > (size_t)e->sched_max_nodes)
       want.resize((size_t)e->sched_max_nodes - e->t_nl.size());
     std::vector<std::vector<pe_action>> prefixes;

@@ -4,7 +4,7 @@ import torch
 from paper_2112_02958_b200 import capi, engine, modelgen
 B = 262144
 text = modelgen.config_program(3)
-eng = engine.Engine(engine.Graph(text), cfg=capi.default_search_config(group_scopes=1))
+eng = engine.Engine(engine.Graph(text), cfg=capi.default_search_config(group_scopes=int(os.environ.get("GROUP", "1"))))
 dev = torch.device("cuda", 0)
 maxd = 32
 poff = torch.zeros(B + 1, dtype=torch.int32, device=dev)
