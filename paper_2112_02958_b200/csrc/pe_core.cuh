@@ -1112,14 +1112,17 @@ struct Cand {
   }
   // (lb = the record's local bytes when the caller already has them)
   PE_HD void register_type(int32_t buf, const Low& w, int64_t lb) {
-    int64_t gb = global_bytes(w);
+    register_type_gb(buf, w.spec, global_bytes(w), lb);
+  }
+  // (and gb = its global bytes)
+  PE_HD void register_type_gb(int32_t buf, uint32_t spec, int64_t gb, int64_t lb) {
     if (buf < g.A) {
       a.arg_gb()[buf] = gb;
       a.arg_lb()[buf] = lb;
-      a.arg_spec()[buf] = w.spec;
+      a.arg_spec()[buf] = spec;
     } else {
       a.em_q2()[buf - g.A] = I64x2{gb, lb};
-      a.em_q3()[buf - g.A] = V4{(int32_t)w.spec, 0, 0, 0};
+      a.em_q3()[buf - g.A] = V4{(int32_t)spec, 0, 0, 0};
     }
   }
   // opens an SPMD op (first operand op0 or -1, local result bytes lb; the
@@ -1283,11 +1286,22 @@ struct Cand {
         }
       }
     }
-    for (int d = 0; d < rank; ++d) {
+    // r.g holds the per-iteration (local) shape here; a sharded dim becomes
+    // local * axis size.  So the local element count is the product of the
+    // per-iteration dims (exact: no division, never a divisibility failure)
+    // and the global bytes are 4 * local * the sharded dims' axis sizes.
+    int64_t out_elems = 1, gmul = 1;
+#pragma unroll
+    for (int d = 0; d < kMaxRank; ++d) {
+      if (d >= rank) break;
+      out_elems *= r.g[d];
       uint32_t ax1 = spec_axis(r.spec, d);
-      if (ax1) r.g[d] = (int32_t)(r.g[d] * asz(ax1 - 1));
+      if (ax1) {
+        int64_t sz = asz(ax1 - 1);
+        r.g[d] = (int32_t)(r.g[d] * sz);
+        gmul *= sz;
+      }
     }
-    int64_t out_elems = local_elems(r);
     int32_t j = new_op(kind, -1, -1, n, n > 0 ? a.lo_buf()[a.opnd()[base]] : -1, 4 * out_elems);
     if (j < 0) return;
 #pragma unroll 1
@@ -1314,7 +1328,7 @@ struct Cand {
         break;
     }
     r.buf = g.A + j;
-    register_type(r.buf, r, 4 * out_elems);
+    register_type_gb(r.buf, r.spec, 4 * out_elems * gmul, 4 * out_elems);
     store(v, r);
   }
 
