@@ -1213,16 +1213,6 @@ struct Cand {
     int32_t base = g.oopnd_off[o], n = g.oopnd_off[o + 1] - base;
     int32_t lax = l >= 0 ? (int32_t)a.laxis()[l] : -1;
     uint8_t kind = g.okind[o];
-    // After materialisation every operand's record is in its LowRec (it
-    // is stored when a collective moved it), so the rest of the op re-reads
-    // the records instead of keeping them in (local-memory) temporaries; a
-    // repeated operand (mul(x, x)) thereby sees the record its last use
-    // stored, as in the reference.
-#pragma unroll 1
-    for (int32_t k = 0; k < n; ++k) {
-      materialize(a.opnd()[base + k], lax);
-      if (bad()) return;
-    }
     Low r;
     int32_t xv = g.A + o;
     int rank = g.vrank[xv];
@@ -1234,9 +1224,16 @@ struct Cand {
     r.spec = (uint32_t)rank << 24;
     r.acq = 0;
     r.buf = -1;
+    // Each operand is materialised and its sharding absorbed into the
+    // result in one pass (the reference materialises all operands first;
+    // a later operand's materialisation never changes an earlier operand's
+    // record -- a repeated operand, mul(x, x), finds its record already
+    // materialised -- so the order is immaterial).  The records stay in
+    // their LowRecs; the operand buffers are re-read below.
 #pragma unroll 1
     for (int32_t k = 0; k < n; ++k) {
-      Low w = load(a.opnd()[base + k]);
+      Low w = materialize(a.opnd()[base + k], lax);
+      if (bad()) return;
       r.spec |= spec_pending(w.spec) << 16;
       if (kind == kConstant) continue;
       int wr = rank_of_spec(w.spec);
