@@ -1178,6 +1178,7 @@ struct Cand {
   // pending axes in name order -- one emission per iteration.
   PE_HD Low materialize(int32_t v, int32_t loop_axis) {
     Low w = load(v);
+    if ((w.spec & 0x000FFFFFu) == 0) return w;  // replicated, nothing pending
     int32_t b0 = w.buf;
     int r = rank_of_spec(w.spec);
     while (true) {
