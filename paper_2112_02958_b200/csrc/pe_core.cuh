@@ -343,10 +343,11 @@ struct Cand {
   }
 
   // ------------------------------------------------------------ helpers
+  // (status codes are ordered: OK 0, ILLEGAL 1 < INTERNAL 2, CAPACITY 3)
   PE_HD void fail(int32_t st) {
-    if (status == PE_CAND_OK || status == PE_CAND_ILLEGAL) status = st;
+    if (status < PE_CAND_INTERNAL) status = st;
   }
-  PE_HD bool bad() const { return status == PE_CAND_INTERNAL || status == PE_CAND_CAPACITY; }
+  PE_HD bool bad() const { return status >= PE_CAND_INTERNAL; }
   PE_HD int32_t NV() const { return g.A + g.N; }
   PE_HD int64_t asz(int32_t ax) const { return g.axis_size[ax]; }
   // VRec header word: vk | tile-loop flag << 8 | loop axis << 16 | loop dim << 24
