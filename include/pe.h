@@ -249,7 +249,8 @@ pe_status pe_infer_rest(pe_engine* e, const pe_action* prefix, uint32_t n_prefix
  * with the rollout policy (uniform, Stop weight 2 after the first decision,
  * at most max_decisions) from a splitmix64 stream seeded with seeds[c], and
  * scores the terminal state.  acts_out receives prefix + sampled actions
- * (max_decisions per candidate), n_acts_out the count. */
+ * (row stride max_decisions per candidate; entries past a candidate's
+ * n_acts_out are unspecified), n_acts_out the count. */
 pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix,
                            const uint32_t* prefix_off, const uint64_t* seeds,
                            uint32_t n_cand, pe_action* acts_out,

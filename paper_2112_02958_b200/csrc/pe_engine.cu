@@ -176,7 +176,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                   uint32_t n, int32_t maxd, pe_cost_params cp, int64_t baseline,
                   pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
                   int32_t legal_words, uint32_t* ctr, const uint32_t* perm,
-                  const __grid_constant__ SchedView sv) {
+                  const __grid_constant__ SchedView sv, uint32_t* max_acts) {
 #if PE_SOLO
   // experiment: one active lane per warp (no SIMT divergence across candidates)
   if (threadIdx.x % 32) return;
@@ -213,6 +213,9 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                            legal_out ? legal_out + (uint64_t)i * legal_words : nullptr,
                            legal_words, snap, sd, spath, sstop);
     out[i] = r;
+    // longest action list of the batch (host mode copies only that many
+    // columns of acts_out back)
+    if (max_acts) atomicMax(max_acts, n_out[i]);
   };
   if (RETRY || PE_SOLO) {
     for (uint32_t k = slot; k < n; k += slots) run(k);
@@ -580,7 +583,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
                "cudaMalloc(arena)") ||
       !cuda_ok(cudaMalloc(&e->d_big_arena, (size_t)big_groups * e->big_layout.bytes), err,
                "cudaMalloc(big arena)") ||
-      !cuda_ok(cudaMalloc(&e->d_ctr, 4 * sizeof(uint32_t)), err, "cudaMalloc(counters)") ||
+      !cuda_ok(cudaMalloc(&e->d_ctr, 8 * sizeof(uint32_t)), err, "cudaMalloc(counters)") ||
       // arenas start zeroed: the per-op `seen` marks of the stuck analysis
       // are cleared by each candidate after use, never wholesale
       !cuda_ok(cudaMemset(e->d_arena, 0, (size_t)groups * e->layout.bytes), err, "zero arena") ||
@@ -910,7 +913,7 @@ bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefix
         e->dview, e->big_layout, e->d_big_arena, bs, (const pe_action*)buf[0],
         (const uint32_t*)buf[1], (const uint64_t*)buf[2], n, maxd, e->cp, e->baseline,
         (pe_action*)buf[3], (uint32_t*)buf[4], (pe_result*)buf[5], (uint64_t*)buf[6], lw,
-        nullptr, nullptr, SchedView());
+        nullptr, nullptr, SchedView(), nullptr);
     e->launches += 2;
     ok = cuda_ok(cudaGetLastError(), err, "probe launch") &&
          cuda_ok(cudaMemcpyAsync(lg.data(), buf[6], sizes[6], cudaMemcpyDeviceToHost, st), err,
@@ -1197,6 +1200,11 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   if (!cuda_ok(cudaMemsetAsync(e->d_ctr + 1, 0, sizeof(uint32_t), st), err,
                "reset work counter"))
     return PE_ERR_CUDA;
+  // host mode: the kernels record the longest action list so only that many
+  // columns of acts_out travel back
+  uint32_t* max_acts = (flags & PE_MEM_DEVICE) ? nullptr : e->d_ctr + 4;
+  if (max_acts && !cuda_ok(cudaMemsetAsync(max_acts, 0, 4, st), err, "reset max acts"))
+    return PE_ERR_CUDA;
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
   uint32_t grid = (slots * kThreadsPerSlot + kBlock - 1) / kBlock;
   uint32_t bgrid = (bs * kThreadsPerSlot + kBlock - 1) / kBlock;
@@ -1204,11 +1212,11 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   auto launch = [&](auto main_k, auto retry_k) {
     main_k<<<grid, kBlock, 0, st>>>(e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
                                     d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts, d_out,
-                                    d_legal, lw, e->d_ctr + 1, perm, sv);
+                                    d_legal, lw, e->d_ctr + 1, perm, sv, max_acts);
     retry_k<<<bgrid, kBlock, 0, st>>>(e->dview, e->big_layout, e->d_big_arena, bs, d_prefix,
                                       d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
                                       d_nacts, d_out, d_legal, lw, nullptr, nullptr,
-                                      SchedView());
+                                      SchedView(), max_acts);
   };
   if (e->wl.resurface)
     launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>);
@@ -1217,8 +1225,16 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "pe_rollout_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {
-    bool ok = cuda_ok(cudaMemcpyAsync(acts_out, d_acts, (size_t)n * maxd * sizeof(pe_action),
-                                      cudaMemcpyDeviceToHost, st), err, "D2H acts") &&
+    uint32_t kmax = 0;
+    bool ok = cuda_ok(cudaMemcpyAsync(&kmax, max_acts, 4, cudaMemcpyDeviceToHost, st), err,
+                      "D2H max acts") &&
+              cuda_ok(cudaStreamSynchronize(st), err, "sync");
+    kmax = std::min<uint32_t>(kmax, (uint32_t)maxd);
+    ok = ok && (kmax == 0 ||
+                cuda_ok(cudaMemcpy2DAsync(acts_out, (size_t)maxd * sizeof(pe_action), d_acts,
+                                          (size_t)maxd * sizeof(pe_action),
+                                          (size_t)kmax * sizeof(pe_action), n,
+                                          cudaMemcpyDeviceToHost, st), err, "D2H acts")) &&
               cuda_ok(cudaMemcpyAsync(n_acts_out, d_nacts, (size_t)n * 4,
                                       cudaMemcpyDeviceToHost, st), err, "D2H n_acts") &&
               cuda_ok(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(pe_result),
