@@ -244,6 +244,27 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
 #endif
 }
 
+// Arena calibration: root rollouts in full-size arenas, recording the
+// largest value-slot, loop, front-stack, SPMD-op and operand-log counts.
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
+pe_calib_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
+                uint8_t* arena, uint32_t slots, uint32_t n, int32_t maxd, pe_cost_params cp,
+                pe_action* acts, uint32_t* n_out, int32_t* hw) {
+  uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= slots) return;
+  pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
+  for (uint32_t k = slot; k < n; k += slots) {
+    pe_result r;
+    c.template rollout<false>(nullptr, 0, 0x5EEDull * (k + 1), maxd, cp, 1,
+                              acts + (uint64_t)k * maxd, n_out + k, r, nullptr, 0);
+    atomicMax(&hw[0], c.nslots);
+    atomicMax(&hw[1], c.nloops);
+    atomicMax(&hw[2], c.nfs);
+    atomicMax(&hw[3], c.nem);
+    atomicMax(&hw[4], c.neo);
+  }
+}
+
 // ---- prefix-trie scheduling kernels ----
 // Probe: evaluates each prefix (no decisions after it), records the legal
 // set after it and saves the state after it as the node's snapshot.
@@ -575,20 +596,69 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
       (uint64_t)e->sm_count * 8 / lanes,
       std::max<uint64_t>(1, (budget / 8) / std::max<uint64_t>(e->big_layout.bytes, 1)));
   e->big_slots = (uint32_t)(big_groups * lanes);
+  // arenas start zeroed: the per-op `seen` marks of the stuck analysis are
+  // cleared by each candidate after use, never wholesale
+  if (!cuda_ok(cudaMalloc(&e->d_big_arena, (size_t)big_groups * e->big_layout.bytes), err,
+               "cudaMalloc(big arena)") ||
+      !cuda_ok(cudaMalloc(&e->d_ctr, 8 * sizeof(uint32_t)), err, "cudaMalloc(counters)") ||
+      !cuda_ok(cudaMemset(e->d_big_arena, 0, (size_t)big_groups * e->big_layout.bytes), err,
+               "zero arena")) {
+    pe_engine_destroy(e);
+    return PE_ERR_CUDA;
+  }
   uint64_t fit_groups = (budget - big_groups * e->big_layout.bytes) /
                         std::max<uint64_t>(e->layout.bytes, 1);
+  const char* calib_env = std::getenv("PE_CALIBRATE");
+  bool calibrate = !(calib_env && std::atoi(calib_env) == 0) &&
+                   !std::getenv("PE_DEBUG_TIGHT_EM_CAP") && !e->wl.auto_axes.empty();
+  if (fit_groups < want / lanes && calibrate) {
+    // Slot-limited by the budget (large graphs): size the tight arena from
+    // measured high-water marks of root rollouts (x1.3 + margin) instead of
+    // the structural formula.  A candidate that still overflows takes the
+    // full-size retry path, so calibration changes footprint, never results.
+    const uint32_t nc = 2048;
+    int32_t* d_hw = nullptr;
+    pe_action* d_acts = nullptr;
+    uint32_t* d_na = nullptr;
+    int32_t hw[5] = {0, 0, 0, 0, 0};
+    int32_t maxd = (int32_t)e->cfg.max_decisions;
+    bool ok = cuda_ok(cudaMalloc(&d_hw, sizeof(hw)), err, "cudaMalloc(calibration)") &&
+              cuda_ok(cudaMalloc(&d_acts, (size_t)nc * maxd * sizeof(pe_action)), err,
+                      "cudaMalloc(calibration)") &&
+              cuda_ok(cudaMalloc(&d_na, nc * 4), err, "cudaMalloc(calibration)") &&
+              cuda_ok(cudaMemset(d_hw, 0, sizeof(hw)), err, "calibration");
+    if (ok) {
+      uint32_t bs = std::min<uint32_t>(e->big_slots, nc);
+      pe_calib_kernel<<<(bs + kBlock - 1) / kBlock, kBlock>>>(
+          v, e->big_layout, e->d_big_arena, bs, nc, maxd, e->cp, d_acts, d_na, d_hw);
+      e->launches += 1;
+      ok = cuda_ok(cudaGetLastError(), err, "calibration launch") &&
+           cuda_ok(cudaMemcpy(hw, d_hw, sizeof(hw), cudaMemcpyDeviceToHost), err,
+                   "calibration");
+    }
+    for (void* q : {(void*)d_hw, (void*)d_acts, (void*)d_na})
+      if (q) cudaFree(q);
+    if (!ok) {
+      pe_engine_destroy(e);
+      return PE_ERR_CUDA;
+    }
+    auto grow = [](int64_t x, int64_t pad) { return (int32_t)(x + x * 3 / 10 + pad); };
+    pe::Caps c = e->layout.caps;
+    const int32_t base_slots = v.A + v.N;
+    c.V = std::min(c.V, base_slots + grow(std::max(0, hw[0] - base_slots), 128));
+    c.L = std::min(c.L, grow(hw[1], 64));
+    c.FS = std::min(c.FS, grow(hw[2], 16));
+    c.EM = std::min(c.EM, grow(hw[3], 128));
+    c.EO = std::min(c.EO, grow(hw[4], 128));
+    e->layout = pe::relayout(v, c);
+    fit_groups = (budget - big_groups * e->big_layout.bytes) /
+                 std::max<uint64_t>(e->layout.bytes, 1);
+  }
   uint64_t groups = std::max<uint64_t>(1, std::min(want / lanes, fit_groups));
   e->slots = (uint32_t)(groups * lanes);
   if (!cuda_ok(cudaMalloc(&e->d_arena, (size_t)groups * e->layout.bytes), err,
                "cudaMalloc(arena)") ||
-      !cuda_ok(cudaMalloc(&e->d_big_arena, (size_t)big_groups * e->big_layout.bytes), err,
-               "cudaMalloc(big arena)") ||
-      !cuda_ok(cudaMalloc(&e->d_ctr, 8 * sizeof(uint32_t)), err, "cudaMalloc(counters)") ||
-      // arenas start zeroed: the per-op `seen` marks of the stuck analysis
-      // are cleared by each candidate after use, never wholesale
-      !cuda_ok(cudaMemset(e->d_arena, 0, (size_t)groups * e->layout.bytes), err, "zero arena") ||
-      !cuda_ok(cudaMemset(e->d_big_arena, 0, (size_t)big_groups * e->big_layout.bytes), err,
-               "zero arena")) {
+      !cuda_ok(cudaMemset(e->d_arena, 0, (size_t)groups * e->layout.bytes), err, "zero arena")) {
     pe_engine_destroy(e);
     return PE_ERR_CUDA;
   }
