@@ -611,7 +611,10 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   const char* calib_env = std::getenv("PE_CALIBRATE");
   bool calibrate = !(calib_env && std::atoi(calib_env) == 0) &&
                    !std::getenv("PE_DEBUG_TIGHT_EM_CAP") && !e->wl.auto_axes.empty();
-  if (fit_groups < want / lanes && calibrate) {
+  // (PE_CALIBRATE=2 forces it: tests exercise calibrated arenas on graphs
+  // small enough for the oracle)
+  bool force_calib = calib_env && std::atoi(calib_env) == 2;
+  if ((fit_groups < want / lanes || force_calib) && calibrate) {
     // Slot-limited by the budget (large graphs): size the tight arena from
     // measured high-water marks of root rollouts (x1.3 + margin) instead of
     // the structural formula.  A candidate that still overflows takes the

@@ -240,6 +240,28 @@ def test_training_step_device_vs_oracle(oracle_lib):
     assert all(x[:x[0]] == y[:y[0]] for x, y in zip(tr, rtr))
 
 
+def test_calibrated_arena_preserves_results(oracle_lib, monkeypatch):
+    # arena calibration (automatic when the budget limits
+    # slots, forced here): tighter caps, overflow through the retry path,
+    # identical results
+    text = modelgen.config_program(3)
+    cfg = capi.default_search_config(group_scopes=1)
+    plain = _engine(text, cfg)
+    monkeypatch.setenv("PE_CALIBRATE", "2")
+    calib = _engine(text, cfg)
+    assert calib.arena_bytes() < plain.arena_bytes()
+    n = 8192
+    seeds = [123_000 + i for i in range(n)]
+    r1, s1, _ = calib.rollout_batch([[]] * n, seeds)
+    r2, s2, _ = plain.rollout_batch([[]] * n, seeds)
+    assert s1 == s2
+    assert all(not H.compare_results(a, b) for a, b in zip(r1, r2))
+    ref, rseqs, _ = H.rollout_batch("oracle", text, [[]] * 64, seeds[:64], cfg,
+                                    threads=os.cpu_count() or 1)
+    assert rseqs == s1[:64]
+    assert all(not H.compare_results(a, b) for a, b in zip(r1[:64], ref))
+
+
 def test_config4_training_step_runs():
     # config 4 at full size (48 layers, 13,757 ops, 1,153 arguments): every
     # rollout evaluates (tight arena or retry), no failures
