@@ -166,6 +166,7 @@ struct SchedView {
   int32_t path_cap = 0;
   const uint8_t* snap = nullptr;
   uint64_t stride = 0;
+  uint32_t kstride = 1;  // keys are node * kstride + slot
 };
 
 template <bool RETRY, bool RS>
@@ -198,13 +199,13 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
     int32_t sd = 0;
     bool sstop = false;
     if (sv.keys) {
-      uint32_t key = sv.keys[i];
-      int4 nd = sv.tnode[key >> 1];
+      uint32_t key = sv.keys[i], node = key / sv.kstride;
+      int4 nd = sv.tnode[node];
       if (nd.w >= 0) {
         snap = sv.snap + sv.stride * (uint64_t)nd.w;
         sd = nd.z;
-        spath = sv.tpath + (uint64_t)(key >> 1) * sv.path_cap;
-        sstop = (key & 1u) != 0;
+        spath = sv.tpath + (uint64_t)node * sv.path_cap;
+        sstop = key % sv.kstride == 0;  // its next draw is Stop
       }
     }
     pe_result r;
@@ -294,35 +295,44 @@ pe_probe_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__
 // key: the rollout stops there).  Unprobed children that are reached are
 // flagged for the host to probe.
 __global__ void pe_sched_key_kernel(uint32_t n, const uint64_t* seeds, int32_t depth,
-                                    const int4* tnode, const int32_t* tchild, uint32_t* tmiss,
-                                    uint32_t* nmiss, uint32_t* keys, uint32_t* hist) {
+                                    int32_t maxd, uint32_t kstride, const int4* tnode,
+                                    const int32_t* tchild, uint32_t* tmiss, uint32_t* nmiss,
+                                    uint32_t* keys, uint32_t* hist) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint64_t st = seeds[i];
   int32_t node = 0, steps = 0;
-  uint32_t key;
+  uint32_t slot;  // 0: Stop drawn here, 1: the rollout ends here (nothing
+                  // legal / decision cap), 2 + p: its next action is legal[p]
   while (true) {
     int4 nd = tnode[node];
-    if (steps >= depth || nd.x == 0) {
-      key = 2u * (uint32_t)node;
+    if (nd.x == 0 || steps >= maxd) {
+      slot = 1;
       break;
     }
     uint64_t ws = steps >= 1 ? 2 : 1;
     uint64_t pick = pe::Cand::splitmix(st) % ((uint64_t)nd.x + ws);
     if (pick >= (uint64_t)nd.x) {
-      key = 2u * (uint32_t)node + 1u;
+      slot = 0;
+      break;
+    }
+    // at the trie's depth the next action is still known (the node's legal
+    // set); below, an unprobed child is flagged for the host to probe
+    if (steps >= depth) {
+      slot = 2 + (uint32_t)pick;
       break;
     }
     int32_t c = tchild[nd.y + (int32_t)pick];
     if (c < 0) {
       tmiss[nd.y + (int32_t)pick] = 1u;
       atomicAdd(nmiss, 1u);  // candidates that would group deeper after a probe
-      key = 2u * (uint32_t)node;
+      slot = 2 + (uint32_t)pick;
       break;
     }
     node = c;
     ++steps;
   }
+  uint32_t key = (uint32_t)node * kstride + slot;
   keys[i] = key;
   atomicAdd(&hist[key], 1u);
 }
@@ -1127,10 +1137,13 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
   if (!ensure_dev(e->d_keys, e->sched_cap, n, err, "cudaMalloc(sched)") ||
       !ensure_dev(e->d_perm, e->perm_cap, n, err, "cudaMalloc(sched)"))
     return false;
-  uint32_t m = 0;
+  uint32_t m = 0, kstride = 1;
   for (int round = 0; round < 2; ++round) {
     if (!sched_upload(e, st, err)) return false;
-    m = 2 * (uint32_t)e->t_nl.size();
+    int32_t max_nl = 0;
+    for (int32_t x : e->t_nl) max_nl = std::max(max_nl, x);
+    kstride = (uint32_t)max_nl + 2;
+    m = kstride * (uint32_t)e->t_nl.size();
     if (!ensure_dev(e->d_hist, e->hist_cap, m, err, "cudaMalloc(sched)") ||
         !cuda_ok(cudaMemsetAsync(e->d_hist, 0, (size_t)m * 4, st), err, "sched hist") ||
         !cuda_ok(cudaMemsetAsync(e->d_tmiss, 0, std::max<size_t>(1, e->t_child.size()) * 4, st),
@@ -1138,8 +1151,8 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
         !cuda_ok(cudaMemsetAsync(e->d_ctr + 3, 0, 4, st), err, "sched misses"))
       return false;
     pe_sched_key_kernel<<<(n + 255) / 256, 256, 0, st>>>(
-        n, d_seeds, depth, (const int4*)e->d_tnode, e->d_tchild, e->d_tmiss, e->d_ctr + 3,
-        e->d_keys, e->d_hist);
+        n, d_seeds, depth, maxd, kstride, (const int4*)e->d_tnode, e->d_tchild, e->d_tmiss,
+        e->d_ctr + 3, e->d_keys, e->d_hist);
     e->launches += 1;
     if (!cuda_ok(cudaGetLastError(), err, "sched key launch")) return false;
     if (round == 1 || (int32_t)e->t_nl.size() >= e->sched_max_nodes) break;
@@ -1195,6 +1208,7 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
   sv->path_cap = e->path_cap;
   sv->snap = e->d_snap;
   sv->stride = e->snap_stride;
+  sv->kstride = kstride;
   return true;
 }
 
