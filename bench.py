@@ -221,12 +221,22 @@ def run_engine(args):
     total_ms = _max_over_ranks(dist, sum(step_ms), dev)
     value = ws * K * B / (total_ms / 1e3)
 
-    # sanity: every candidate evaluated OK
+    # sanity: every candidate evaluated OK (numpy views of the pe_result
+    # fields; no per-candidate Python objects, whose garbage collection
+    # could land in the e2e timing below)
+    import gc
+
+    import numpy as np
     host = res.view(B, C.sizeof(capi.PeResult)).cpu().numpy()
-    results = [capi.PeResult.from_buffer_copy(host[i].tobytes()) for i in range(B)]
-    bad = sum(r.status != 0 for r in results)
-    mean_steps = sum(r.n_steps for r in results) / B
-    mean_ops = sum(r.n_spmd_ops for r in results) / B
+
+    def field(name):
+        f = getattr(capi.PeResult, name)
+        return np.frombuffer(host[:, f.offset:f.offset + 4].tobytes(), dtype=np.int32)
+    bad = int((field("status") != 0).sum())
+    mean_steps = float(field("n_steps").mean())
+    mean_ops = float(field("n_spmd_ops").mean())
+    del host
+    gc.collect()
 
     # e2e: the public C-ABI with HOST buffers (pinned), copies inside the region
     pin_seeds = torch.empty(B, dtype=torch.int64).pin_memory()
@@ -238,11 +248,8 @@ def run_engine(args):
     h2d = pin_seeds.numel() * 8 + pin_poff.numel() * 4
     d2h = None  # counted after the calls: the engine copies back only the action columns used
     e2e_k = max(1, min(K, 5))
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    for i in range(e2e_k):
+
+    def host_step(i):
         pin_seeds.copy_(torch.arange(B, dtype=torch.int64) + base + 7_000_000 * (i + 1))
         rc = lib.pe_rollout_batch(eng.h, None, C.c_void_p(pin_poff.data_ptr()),
                                   C.c_void_p(pin_seeds.data_ptr()), B, C.c_void_p(pin_acts.data_ptr()),
@@ -250,6 +257,14 @@ def run_engine(args):
                                   None, 0, sp, C.byref(err))
         assert rc == 0, err.message
         _ = pin_res[:8].numpy().tobytes()  # host read of the step's result
+
+    host_step(1000)  # untimed warm-up: the engine's host-mode staging buffers are allocated
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for i in range(e2e_k):
+        host_step(i)
     e2e_s = _max_over_ranks(dist, time.perf_counter() - t0, dev)
     kmax = int(pin_nacts.max().item())
     d2h = B * kmax * 8 + pin_nacts.numel() * 4 + pin_res.numel()  # acts columns, counts, results
