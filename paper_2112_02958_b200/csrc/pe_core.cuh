@@ -801,13 +801,15 @@ struct Cand {
       a.dirty()[w] = bits & (bits - 1);
       int32_t o = m;
       if (a.vk()[g.A + o] != VK_TOP) continue;
-      if (!has_tiled_operand(o)) continue;
+      // plan_pull sees every tiled operand: it either found a driving one
+      // or stopped, blocked, at one -- no separate has_tiled_operand scan
+      Pull p = plan_pull(o);
+      if (p.drive < 0 && p.reason != R_BLOCKED) continue;  // no tiled operand
       if (g.orule_err[o]) {
         fail(PE_CAND_INTERNAL);
         done = true;
         continue;
       }
-      Pull p = plan_pull(o);
       if (!p.ok) continue;
       pull(o, p);
       if (bad()) done = true;
@@ -1016,12 +1018,12 @@ struct Cand {
   // ... and of one top-level op with a tiled operand that cannot be pulled
   PE_HD void stuck_top(int32_t v) {
     int32_t o = a.vref()[v];
-    if (!has_tiled_operand(o)) return;
+    Pull p = plan_pull(o);
+    if (p.drive < 0 && p.reason != R_BLOCKED) return;  // no tiled operand
     if (g.orule_err[o]) {
       fail(PE_CAND_INTERNAL);
       return;
     }
-    Pull p = plan_pull(o);
     if (p.ok) {
       fail(PE_CAND_INTERNAL);  // "pull available after fixpoint"
       return;
