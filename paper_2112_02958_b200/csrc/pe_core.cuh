@@ -1234,6 +1234,11 @@ struct Cand {
     // record -- a repeated operand, mul(x, x), finds its record already
     // materialised -- so the order is immaterial).  The records stay in
     // their LowRecs; the operand buffers are re-read below.
+    // flops on LOCAL operand shapes, taken from the
+    // materialised records as they pass: dot = 2 * lhs elements * rhs free
+    // dims (omask), reduce = input elements
+    bool red = kind == kReduceSum || kind == kReduceMax;
+    int64_t fl = kind == kDot ? 2 : 1;
 #pragma unroll 1
     for (int32_t k = 0; k < n; ++k) {
       Low w = materialize(a.opnd()[base + k], lax);
@@ -1241,6 +1246,12 @@ struct Cand {
       r.spec |= spec_pending(w.spec) << 16;
       if (kind == kConstant) continue;
       int wr = rank_of_spec(w.spec);
+      if ((kind == kDot && k < 2) || (red && k == 0)) {
+        uint32_t m = k == 0 ? 0xFu : g.omask[o];
+#pragma unroll 1
+        for (int d = 0; d < wr; ++d)
+          if ((m >> d) & 1) fl *= local_dim(w, d);
+      }
       if ((w.spec & 0xFFFFu) == 0) continue;  // no sharded dim
       ReshapeRule rr;
       if (kind == kReshape) {
@@ -1307,23 +1318,13 @@ struct Cand {
     if (j < 0) return;
 #pragma unroll 1
     for (int32_t k = 0; k < n; ++k) add_operand(j, a.lo_buf()[a.opnd()[base + k]]);
-    // flops on LOCAL operand shapes
     switch (kind) {
-      case kDot: {
-        Low in0 = load(a.opnd()[base]), in1 = load(a.opnd()[base + 1]);
-        int64_t f = 2 * local_elems(in0);
-        int rr2 = rank_of_spec(in1.spec);
-        for (int d = 0; d < rr2; ++d)
-          if ((g.omask[o] >> d) & 1) f *= local_dim(in1, d);
-        flops += f;
+      case kDot: case kReduceSum: case kReduceMax:
+        flops += fl;
         break;
-      }
       case kAdd: case kSub: case kMul: case kDiv: case kMaximum:
       case kNeg: case kExp: case kTanh: case kRsqrt:
         flops += out_elems;
-        break;
-      case kReduceSum: case kReduceMax:
-        flops += local_elems(load(a.opnd()[base]));
         break;
       default:
         break;
@@ -1521,14 +1522,20 @@ struct Cand {
       r.sbc_cnt[x] = 0;
     }
     // One pass over the SPMD ops: collective_stats (REF spmd.cc:405-434)
-    // over final registered types, and the liveness deltas (SURVEY.md
-    // B.5.1): new_op set delta[j] = +lb[j]; here -lb[j] lands after the
-    // buffer's last use.
+    // over final registered types, and the liveness sweep (SURVEY.md
+    // B.5.1): new_op set delta[j] = +lb[j]; -lb[j] lands after the
+    // buffer's last use (> j), so by the time the sweep reaches j every
+    // subtraction landing there is already in delta[j] and the running sum
+    // is taken in the same pass.
     if (result_buf >= g.A) a.em_last()[result_buf - g.A] = nem - 1;
     a.delta()[nem] = 0;
+    int64_t run = 0, best = 0;
     for (int32_t j = 0; j < nem; ++j) {
       V4 q = a.em_q0()[j];  // head, op0, last, operand offset
-      int64_t lb = a.em_lb()[j];
+      I64x2 q1 = a.em_q1()[j];  // local bytes, liveness delta
+      int64_t lb = q1.x;
+      run += q1.y;
+      if (run > best) best = run;
       int32_t kind = q.x & 0xFF, ax = ((q.x >> 8) & 0xF) - 1;
       if (kind == kAllReduce) {
         int32_t b = q.y;
@@ -1545,11 +1552,6 @@ struct Cand {
     }
     int64_t base = 0;
     for (int32_t x = 0; x < g.A; ++x) base += a.alb0()[x];
-    int64_t run = 0, best = 0;
-    for (int32_t j = 0; j < nem; ++j) {
-      run += a.delta()[j];
-      if (run > best) best = run;
-    }
     r.peak_bytes = base + best;
     r.flops = flops;
     r.n_spmd_ops = nem;
