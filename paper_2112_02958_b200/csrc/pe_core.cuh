@@ -1391,35 +1391,33 @@ struct Cand {
     int32_t lax = a.laxis()[l];
     Low yv = load(a.lyield()[l]);
     int32_t lt = a.ltype()[l];
-    if (a.lkind()[l] == LK_TILE) {
+    bool tile = a.lkind()[l] == LK_TILE;
+    Low w = yv;
+    if (tile) {
       if (spec_pending(yv.spec)) {
         fail(PE_CAND_INTERNAL);
         return;
       }
-      Low r = yv;
       int dim = a.ldim()[l];
-      uint32_t have = spec_axis(r.spec, dim);
+      uint32_t have = spec_axis(w.spec, dim);
       if ((int32_t)have == lax + 1) {
-        r.acq &= ~(1u << dim);
-      } else if (have == 0 && !has_axis(r.spec, lax)) {
-        r.spec = spec_set_axis(r.spec, dim, (uint32_t)(lax + 1));
-        r.acq &= ~(1u << dim);
+        w.acq &= ~(1u << dim);
+      } else if (have == 0 && !has_axis(w.spec, lax)) {
+        w.spec = spec_set_axis(w.spec, dim, (uint32_t)(lax + 1));
+        w.acq &= ~(1u << dim);
       } else {
         fail(PE_CAND_INTERNAL);
         return;
       }
-      for (int d = 0; d < kMaxRank; ++d) r.g[d] = g.shape(lt)[d];
-      int rk = rank_of_spec(r.spec);
+      for (int d = 0; d < kMaxRank; ++d) w.g[d] = g.shape(lt)[d];
+      int rk = rank_of_spec(w.spec);
       for (int d = 0; d < rk; ++d)
-        if (local_dim(r, d) != local_dim(yv, d)) {
+        if (local_dim(w, d) != local_dim(yv, d)) {
           fail(PE_CAND_INTERNAL);
           return;
         }
       if (bad()) return;
-      store(v, r);
-      register_type(r.buf, r);
     } else {
-      Low w = yv;
       w.spec |= 1u << (16 + lax);
       int rk = rank_of_spec(w.spec);
       for (int d = 0; d < rk; ++d)
@@ -1428,11 +1426,15 @@ struct Cand {
           w.acq &= ~(1u << d);
         }
       for (int d = 0; d < kMaxRank; ++d) w.g[d] = g.shape(lt)[d];
-      register_type(w.buf, w);
+    }
+    // both kinds register the loop's result type (one inlined copy); a
+    // reduce loop then all-reduces it over the loop axis
+    register_type(w.buf, w);
+    if (!tile) {
       emit_all_reduce(w, lax);
       if (bad()) return;
-      store(v, w);
     }
+    store(v, w);
   }
 
   // lower_to_spmd (REF spmd.cc:328-403).  stuck = also run the stuck
@@ -1457,9 +1459,10 @@ struct Cand {
         if (g.amod((uint32_t)w.g[d], ax) == 0) w.spec = spec_set_axis(w.spec, d, (uint32_t)(ax + 1));
       }
       store(x, w);
-      register_type(x, w);
+      int64_t lb = 4 * local_elems(w);
+      register_type(x, w, lb);
       a.aspec0()[x] = w.spec;
-      a.alb0()[x] = 4 * local_elems(w);
+      a.alb0()[x] = lb;
     }
     for_top([&](int32_t v) {
       uint8_t k = a.vk()[v];
