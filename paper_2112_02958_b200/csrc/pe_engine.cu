@@ -113,6 +113,15 @@ constexpr int kBlock = 128;
 // measured 342K vs 277K cand/s for 4 blocks (128 registers) at config 3
 // despite the spills (profiles/r1_summary.md).
 constexpr int kMinBlocks = PE_MIN_BLOCKS;
+// The main rollout launch at full occupancy uses one block of all the SM's
+// resident threads (same 64-register bound), so the first wave of an SM is
+// kSmBlock consecutive positions of the trie-sorted order: neighbours share
+// code paths (the kernel is instruction-fetch bound) and
+// graph records.  Measured 3.05-3.09M vs 2.93-2.97M cand/s with 8 blocks of
+// 128 (whose first waves interleave positions 148 x 128 apart on an SM).
+// Smaller launches (fewer slots than the SMs' resident threads, e.g. a
+// memory-budget-limited config 4) keep 128-thread blocks so every SM works.
+constexpr int kSmBlock = kBlock * kMinBlocks;
 
 #ifdef PE_PHASE_TIMERS
 // profiling build only (tools/phase_profile.py): summed clock64 per phase
@@ -170,7 +179,7 @@ struct SchedView {
 };
 
 template <bool RETRY, bool RS>
-__global__ void __launch_bounds__(kBlock, kMinBlocks)
+__global__ void __launch_bounds__(kSmBlock, 1)
 pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
                   uint8_t* arena, uint32_t slots,
                   const pe_action* prefix, const uint32_t* poff, const uint64_t* seeds,
@@ -1293,11 +1302,14 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   if (max_acts && !cuda_ok(cudaMemsetAsync(max_acts, 0, 4, st), err, "reset max acts"))
     return PE_ERR_CUDA;
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
-  uint32_t grid = (slots * kThreadsPerSlot + kBlock - 1) / kBlock;
+  uint32_t threads = slots * kThreadsPerSlot;
+  uint32_t blk = threads % kSmBlock == 0 && threads >= (uint32_t)e->sm_count * kSmBlock
+                     ? kSmBlock : kBlock;
+  uint32_t grid = (threads + blk - 1) / blk;
   uint32_t bgrid = (bs * kThreadsPerSlot + kBlock - 1) / kBlock;
   // (the stuck-resurfacing instantiation only when the worklist uses it)
   auto launch = [&](auto main_k, auto retry_k) {
-    main_k<<<grid, kBlock, 0, st>>>(e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
+    main_k<<<grid, blk, 0, st>>>(e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
                                     d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts, d_out,
                                     d_legal, lw, e->d_ctr + 1, perm, sv, max_acts);
     retry_k<<<bgrid, kBlock, 0, st>>>(e->dview, e->big_layout, e->d_big_arena, bs, d_prefix,
