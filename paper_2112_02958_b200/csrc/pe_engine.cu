@@ -127,7 +127,22 @@ constexpr int kSmBlock = kBlock * kMinBlocks;
 // profiling build only (tools/phase_profile.py): summed clock64 per phase
 __device__ unsigned long long g_phase_cycles[9];
 #endif
+#ifdef PE_CAND_TIMES
+// profiling build only (tools/tail_profile.py): per schedule position its
+// start / end %globaltimer and SM
+constexpr uint32_t kCandTimesCap = 1u << 20;
+__device__ unsigned long long g_cand_times[kCandTimesCap * 2];
+__device__ uint32_t g_cand_sm[kCandTimesCap];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 
+#ifndef PE_FW_GROUP
+#define PE_FW_GROUP 1024
+#endif
 #ifndef PE_STATIC_SCHED
 #define PE_STATIC_SCHED 0
 #endif
@@ -217,12 +232,24 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
         sstop = key % sv.kstride == 0;  // its next draw is Stop
       }
     }
+#if defined(PE_CAND_TIMES) && defined(__CUDA_ARCH__)
+    unsigned long long t_begin = gtimer();
+#endif
     pe_result r;
     c.template rollout<RS>(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd,
                            cp, baseline, acts_out + (uint64_t)i * maxd, n_out + i, r,
                            legal_out ? legal_out + (uint64_t)i * legal_words : nullptr,
                            legal_words, snap, sd, spath, sstop);
     out[i] = r;
+#if defined(PE_CAND_TIMES) && defined(__CUDA_ARCH__)
+    if (!RETRY && k < kCandTimesCap) {
+      g_cand_times[2 * k] = t_begin;
+      g_cand_times[2 * k + 1] = gtimer();
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_cand_sm[k] = smid;
+    }
+#endif
     // longest action list of the batch (host mode copies only that many
     // columns of acts_out back)
     if (max_acts) atomicMax(max_acts, n_out[i]);
@@ -239,6 +266,14 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
     const uint32_t rank = __popc(mask & ((1u << (threadIdx.x & 31)) - 1u));
     // (every lane of `mask` stays in the loop until the warp-uniform exit)
     uint32_t k = slot;
+#if PE_FW_GROUP < 1024
+    // experiment: an SM-wide block's first wave as 1024 / PE_FW_GROUP runs of
+    // PE_FW_GROUP consecutive positions, spread over the order
+    if (blockDim.x == kSmBlock && slots == gridDim.x * kSmBlock) {
+      uint32_t t = threadIdx.x;
+      k = ((t / PE_FW_GROUP) * gridDim.x + blockIdx.x) * PE_FW_GROUP + t % PE_FW_GROUP;
+    }
+#endif
     while (true) {
       if (k < n) run(k);
       __syncwarp(mask);
@@ -1360,6 +1395,15 @@ extern "C" int pe_debug_phase_cycles(unsigned long long* out9, int reset) {
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
   }
   return 0;
+}
+#endif
+
+#ifdef PE_CAND_TIMES
+extern "C" int pe_debug_cand_times(unsigned long long* times, uint32_t* sms, uint32_t n) {
+  n = n < kCandTimesCap ? n : kCandTimesCap;
+  return cudaMemcpyFromSymbol(times, g_cand_times, sizeof(unsigned long long) * 2 * n) !=
+             cudaSuccess ||
+         cudaMemcpyFromSymbol(sms, g_cand_sm, sizeof(uint32_t) * n) != cudaSuccess;
 }
 #endif
 
