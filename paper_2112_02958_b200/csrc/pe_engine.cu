@@ -140,6 +140,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+// resident rollout threads per SM (experiment knob; the product value is
+// the 64-register limit's 1024)
+#ifndef PE_SM_THREADS
+#define PE_SM_THREADS (kBlock * kMinBlocks)
+#endif
 #ifndef PE_FW_GROUP
 #define PE_FW_GROUP 1024
 #endif
@@ -269,7 +274,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
 #if PE_FW_GROUP < 1024
     // experiment: an SM-wide block's first wave as 1024 / PE_FW_GROUP runs of
     // PE_FW_GROUP consecutive positions, spread over the order
-    if (blockDim.x == kSmBlock && slots == gridDim.x * kSmBlock) {
+    if (blockDim.x == PE_SM_THREADS && slots == gridDim.x * PE_SM_THREADS) {
       uint32_t t = threadIdx.x;
       k = ((t / PE_FW_GROUP) * gridDim.x + blockIdx.x) * PE_FW_GROUP + t % PE_FW_GROUP;
     }
@@ -645,7 +650,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   // one resident thread per slot: kMinBlocks blocks of kBlock threads per SM;
   // arenas come in groups of kLanes interleaved candidates (one per warp)
   const uint64_t lanes = pe::kLanes;
-  uint64_t want = (uint64_t)e->sm_count * kBlock * kMinBlocks / kThreadsPerSlot;
+  uint64_t want = (uint64_t)e->sm_count * PE_SM_THREADS / kThreadsPerSlot;
   uint64_t big_groups = std::min<uint64_t>(
       (uint64_t)e->sm_count * 8 / lanes,
       std::max<uint64_t>(1, (budget / 8) / std::max<uint64_t>(e->big_layout.bytes, 1)));
@@ -1338,8 +1343,8 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
     return PE_ERR_CUDA;
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
   uint32_t threads = slots * kThreadsPerSlot;
-  uint32_t blk = threads % kSmBlock == 0 && threads >= (uint32_t)e->sm_count * kSmBlock
-                     ? kSmBlock : kBlock;
+  uint32_t blk = threads % PE_SM_THREADS == 0 && threads >= (uint32_t)e->sm_count * PE_SM_THREADS
+                     ? PE_SM_THREADS : kBlock;
   uint32_t grid = (threads + blk - 1) / blk;
   uint32_t bgrid = (bs * kThreadsPerSlot + kBlock - 1) / kBlock;
   // (the stuck-resurfacing instantiation only when the worklist uses it)
