@@ -48,6 +48,7 @@ struct pe_engine {
   uint64_t launches = 0;
   int64_t graph_bytes = 0;
   int sm_count = 148;
+  bool l2_persist = false;  // experiment: graph image in the persisting L2 carve-out
   // staging for host-pointer calls
   uint8_t* d_io = nullptr;
   size_t io_cap = 0;
@@ -593,6 +594,11 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
     return PE_ERR_CUDA;
   }
   e->graph_bytes = (int64_t)img.size();
+  if (const char* lp = std::getenv("PE_L2_PERSIST")) {
+    e->l2_persist = std::atoi(lp) != 0;
+    if (e->l2_persist)
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ((size_t)e->graph_bytes + (1 << 20)) & ~size_t((1 << 20) - 1));
+  }
   pe::GraphView v = g.host_view();
   uint8_t* b = e->d_graph;
   v.vshape = (const int32_t*)(b + o_vshape);
@@ -1349,9 +1355,23 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   uint32_t bgrid = (bs * kThreadsPerSlot + kBlock - 1) / kBlock;
   // (the stuck-resurfacing instantiation only when the worklist uses it)
   auto launch = [&](auto main_k, auto retry_k) {
-    main_k<<<grid, blk, 0, st>>>(e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
-                                    d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts, d_out,
-                                    d_legal, lw, e->d_ctr + 1, perm, sv, max_acts);
+    // (experiment PE_L2_PERSIST: the graph image as a persisting L2 window)
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = e->d_graph;
+    at[0].val.accessPolicyWindow.num_bytes = (size_t)e->graph_bytes;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(blk);
+    lc.stream = st;
+    lc.attrs = at;
+    lc.numAttrs = e->l2_persist ? 1 : 0;
+    cudaLaunchKernelEx(&lc, main_k, e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
+                       d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts, d_out, d_legal, lw,
+                       e->d_ctr + 1, perm, sv, max_acts);
     retry_k<<<bgrid, kBlock, 0, st>>>(e->dview, e->big_layout, e->d_big_arena, bs, d_prefix,
                                       d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
                                       d_nacts, d_out, d_legal, lw, nullptr, nullptr,
