@@ -137,6 +137,26 @@ def test_trie_scheduling_preserves_results(oracle_lib, monkeypatch, cfgno, reuse
         assert all(not H.compare_results(a, b) for a, b in zip(r1[:256], ref))
 
 
+def test_l2_persist_window_preserves_results(oracle_lib, monkeypatch):
+    # PE_L2_PERSIST=1 launches the main rollout kernel with the graph image
+    # as a persisting L2 window (a cache hint only): same actions and results
+    text = modelgen.config_program(2)
+    cfg = capi.default_search_config(group_scopes=1)
+    plain = _engine(text, cfg)
+    monkeypatch.setenv("PE_L2_PERSIST", "1")
+    hinted = _engine(text, cfg)
+    n = 8192
+    seeds = list(range(n))
+    r1, s1, _ = hinted.rollout_batch([[]] * n, seeds)
+    r2, s2, _ = plain.rollout_batch([[]] * n, seeds)
+    assert s1 == s2
+    assert all(not H.compare_results(a, b) for a, b in zip(r1, r2))
+    ref, rseqs, _ = H.rollout_batch("oracle", text, [[]] * 256, seeds[:256], cfg,
+                                    threads=os.cpu_count() or 1)
+    assert rseqs == s1[:256]
+    assert all(not H.compare_results(a, b) for a, b in zip(r1[:256], ref))
+
+
 def test_gpt2_medium_24_layer_rollouts(oracle_lib):
     # config 3: 24-layer GPT-2-medium graph on [batch=4, model=2]
     text = modelgen.config_program(3)
