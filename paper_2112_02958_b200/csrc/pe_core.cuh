@@ -1146,7 +1146,9 @@ struct Cand {
     if (tracing) a.em_opnd()[neo] = buf;
     ++neo;
     // ops are emitted in order, so the current op is always the latest use
+#ifndef PE_EXP_NO_LAST
     if (buf >= g.A) a.em_last()[buf - g.A] = j;
+#endif
   }
   // pending_sum.front(): the pending axis with the smallest name (table
   // over the 4-bit pending mask, GraphView::pend_front)
@@ -1551,7 +1553,9 @@ struct Cand {
       } else if (kind == kSliceByCoord) {
         r.sbc_cnt[ax]++;
       }
+#ifndef PE_EXP_NO_DELTA
       a.delta()[q.z + 1] -= lb;
+#endif
     }
     int64_t base = 0;
     for (int32_t x = 0; x < g.A; ++x) base += a.alb0()[x];
