@@ -138,7 +138,9 @@ def run_reference(args):
     from paper_2112_02958_b200 import modelgen
     text = modelgen.config_program(3)
     threads = os.cpu_count() or 1
-    per_step = 2 * threads  # ~1-3 s of CPU work per step on this path
+    # ~2 s of CPU work per step on this path; 8 rollouts per thread so one
+    # long rollout does not leave the other threads idle for most of the step
+    per_step = 8 * threads
     for w in range(args.warmup):
         cpu_reference(text, per_step, 10_000_000 + w * per_step, threads)
     total = 0.0
