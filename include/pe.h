@@ -8,7 +8,12 @@
  * either implementation through one set of types.
  *
  * Threading: graphs are immutable after creation and may be shared.  One
- * engine per device; an engine is not reentrant on one stream.
+ * engine per device.  An engine's calls must not run concurrently from
+ * several host threads (search is single-threaded); calls on
+ * different CUDA streams are accepted and are serialised on the device (each
+ * call's stream waits for the previous call's work: they share the engine's
+ * arenas, work counters and staging buffers).  Device-mode outputs of a call
+ * are complete when its stream reaches the call's last enqueued work.
  */
 #ifndef PE_H_
 #define PE_H_

@@ -49,6 +49,7 @@ struct pe_engine {
   int64_t graph_bytes = 0;
   int sm_count = 148;
   bool l2_persist = false;  // experiment: graph image in the persisting L2 carve-out
+  size_t l2_window = 0, l2_prev_limit = 0;
   // staging for host-pointer calls
   uint8_t* d_io = nullptr;
   size_t io_cap = 0;
@@ -82,6 +83,10 @@ struct pe_engine {
   uint64_t snap_stride = 0;
   int32_t snap_cap = 0, snap_used = 0;
   double snap_budget_gb = 0.0;  // prefix-state reuse: off unless enabled
+  // Calls share the engine's arenas, work counters and staging buffers, so
+  // calls on different streams are serialised on the device: each call's
+  // stream waits for the previous call's last enqueued work.
+  cudaEvent_t done = nullptr;
 };
 
 namespace {
@@ -324,7 +329,7 @@ pe_probe_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__
                 uint8_t* arena, uint32_t slots, const pe_action* prefix, const uint32_t* poff,
                 uint32_t n, int32_t acts_stride, pe_cost_params cp, int64_t baseline,
                 pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
-                int32_t legal_words, uint8_t* snap, uint64_t stride, const int32_t* snap_idx) {
+                int32_t legal_words, uint8_t* snap, uint64_t stride, int32_t* snap_idx) {
   uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
@@ -335,7 +340,13 @@ pe_probe_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__
                               acts_out + (uint64_t)k * acts_stride, n_out + k, r,
                               legal_out + (uint64_t)k * legal_words, legal_words);
     out[k] = r;
-    if (snap_idx[k] >= 0 && r.status == PE_CAND_OK) c.save(snap + stride * (uint64_t)snap_idx[k]);
+    // a probe that overflowed its tight arena saves nothing (the retry
+    // launch re-derives its legal set only): report that to the host, which
+    // attaches a snapshot to the trie node only when it was written
+    if (snap_idx[k] >= 0) {
+      if (r.status == PE_CAND_OK) c.save(snap + stride * (uint64_t)snap_idx[k]);
+      else snap_idx[k] = -1;
+    }
   }
 }
 
@@ -442,6 +453,14 @@ bool ensure_io(pe_engine* e, size_t bytes, pe_error* err) {
 }
 
 uint32_t launch_slots(const pe_engine* e, uint32_t n) { return std::min<uint32_t>(e->slots, n); }
+
+// order this call after the engine's previous call (any stream)
+bool call_begin(pe_engine* e, cudaStream_t st, pe_error* err) {
+  return cuda_ok(cudaStreamWaitEvent(st, e->done, 0), err, "stream wait");
+}
+bool call_end(pe_engine* e, cudaStream_t st, pe_error* err) {
+  return cuda_ok(cudaEventRecord(e->done, st), err, "event record");
+}
 
 }  // namespace
 
@@ -557,6 +576,10 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   pe_engine* e = new pe_engine();
   e->graph = graph;
   e->device = device;
+  if (!cuda_ok(cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming), err, "event")) {
+    delete e;
+    return PE_ERR_CUDA;
+  }
   pe_default_search_config(&e->cfg);
   pe_default_cost_params(&e->cp);
   if (cfg) e->cfg = *cfg;
@@ -595,9 +618,25 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   }
   e->graph_bytes = (int64_t)img.size();
   if (const char* lp = std::getenv("PE_L2_PERSIST")) {
-    e->l2_persist = std::atoi(lp) != 0;
-    if (e->l2_persist)
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ((size_t)e->graph_bytes + (1 << 20)) & ~size_t((1 << 20) - 1));
+    // experiment: the graph image as a persisting L2 window.  The carve-out
+    // and the window are clamped to the device limits; a failure only turns
+    // the hint off (and clears the pending error); destroy() gives the
+    // carve-out back.
+    if (std::atoi(lp) != 0) {
+      int max_persist = 0, max_window = 0;
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+      cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+      size_t want = ((size_t)e->graph_bytes + (1 << 20)) & ~size_t((1 << 20) - 1);
+      want = std::min<size_t>(want, (size_t)std::max(0, max_persist));
+      e->l2_window = std::min<size_t>((size_t)e->graph_bytes, (size_t)std::max(0, max_window));
+      if (want > 0 && e->l2_window > 0 &&
+          cudaDeviceGetLimit(&e->l2_prev_limit, cudaLimitPersistingL2CacheSize) == cudaSuccess &&
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+        e->l2_persist = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
   }
   pe::GraphView v = g.host_view();
   uint8_t* b = e->d_graph;
@@ -754,6 +793,12 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
 
 void pe_engine_destroy(pe_engine* e) {
   if (!e) return;
+  cudaSetDevice(e->device);
+  if (e->l2_persist) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, e->l2_prev_limit);
+    cudaGetLastError();
+  }
   if (e->d_graph) cudaFree(e->d_graph);
   if (e->d_arena) cudaFree(e->d_arena);
   if (e->d_big_arena) cudaFree(e->d_big_arena);
@@ -762,6 +807,7 @@ void pe_engine_destroy(pe_engine* e) {
                   (void*)e->d_perm, (void*)e->d_hist, (void*)e->d_tpath, (void*)e->d_snap})
     if (q) cudaFree(q);
   if (e->d_io) cudaFree(e->d_io);
+  if (e->done) cudaEventDestroy(e->done);
   delete e;
 }
 
@@ -940,6 +986,7 @@ pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* 
   if (n == 0) return PE_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+  if (!call_begin(e, st, err)) return PE_ERR_CUDA;
   const int32_t A = (int32_t)e->graph->g.args.size();
   const pe_action* d_acts = acts;
   const uint32_t* d_off = seq_off;
@@ -989,7 +1036,10 @@ pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* 
     if (trace && !cuda_ok(cudaMemcpyAsync(trace, d_trace, (size_t)n * trace_words * 4,
                                           cudaMemcpyDeviceToHost, st), err, "D2H trace"))
       return PE_ERR_CUDA;
+    if (!call_end(e, st, err)) return PE_ERR_CUDA;
     if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
+  } else if (!call_end(e, st, err)) {
+    return PE_ERR_CUDA;
   } else if (flags & PE_SYNC) {
     if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
   }
@@ -1006,8 +1056,10 @@ namespace {
 // without resurfacing) after each prefix: one rollout launch whose legal
 // output is taken right after the prefix.  Own buffers: the caller's inputs
 // may live in the staging buffer.
+// snap_idx: per prefix the snapshot slot to save into, or -1; on return -1
+// where no snapshot was written (the probe overflowed its tight arena).
 bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefixes,
-                 const std::vector<int32_t>& snap_idx, std::vector<std::vector<int32_t>>& legal,
+                 std::vector<int32_t>& snap_idx, std::vector<std::vector<int32_t>>& legal,
                  std::vector<int32_t>& status, cudaStream_t st, pe_error* err) {
   uint32_t n = (uint32_t)prefixes.size();
   std::vector<pe_action> acts;
@@ -1044,7 +1096,7 @@ bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefix
     pe_probe_kernel<<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
         e->dview, e->layout, e->d_arena, slots, (const pe_action*)buf[0], (const uint32_t*)buf[1],
         n, maxd, e->cp, e->baseline, (pe_action*)buf[3], (uint32_t*)buf[4], (pe_result*)buf[5],
-        (uint64_t*)buf[6], lw, e->d_snap, e->snap_stride, (const int32_t*)buf[7]);
+        (uint64_t*)buf[6], lw, e->d_snap, e->snap_stride, (int32_t*)buf[7]);
     // overflowed probes: legal sets from full-size arenas (no snapshot); the
     // uniform maxd only adds draws after the prefix, its legal set is final
     pe_rollout_kernel<true, false><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
@@ -1058,6 +1110,8 @@ bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefix
                  "D2H probe") &&
          cuda_ok(cudaMemcpyAsync(res.data(), buf[5], sizes[5], cudaMemcpyDeviceToHost, st), err,
                  "D2H probe") &&
+         cuda_ok(cudaMemcpyAsync(snap_idx.data(), buf[7], n * 4ull, cudaMemcpyDeviceToHost, st),
+                 err, "D2H probe") &&
          cuda_ok(cudaStreamSynchronize(st), err, "probe sync");
   }
   for (int k = 0; k < 8; ++k)
@@ -1185,8 +1239,8 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
   }
   if (e->t_nl.empty()) {
     std::vector<std::vector<int32_t>> lg;
-    std::vector<int32_t> stat;
-    if (!sched_probe(e, {{}}, {-1}, lg, stat, st, err)) return false;  // root: init() state
+    std::vector<int32_t> stat, none{-1};
+    if (!sched_probe(e, {{}}, none, lg, stat, st, err)) return false;  // root: init() state
     sched_add_node(e, -1, 0, lg[0]);
   }
   if (!ensure_dev(e->d_keys, e->sched_cap, n, err, "cudaMalloc(sched)") ||
@@ -1249,7 +1303,7 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
     if (!sched_probe(e, prefixes, sidx, lg, stat, st, err)) return false;
     for (size_t q = 0; q < want.size(); ++q) {
       int32_t id = sched_add_node(e, want[q].first, want[q].second, lg[q]);
-      e->t_snap[id] = stat[q] == PE_CAND_OK ? sidx[q] : -1;
+      e->t_snap[id] = sidx[q];  // -1 unless the probe wrote the snapshot
     }
   }
   pe_sched_scan_kernel<<<1, 1024, 0, st>>>(e->d_hist, m);
@@ -1286,6 +1340,7 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+  if (!call_begin(e, st, err)) return PE_ERR_CUDA;
   int32_t maxd = (int32_t)e->cfg.max_decisions;
   int32_t lw = (int32_t)pe_engine_legal_words(e);
   const pe_action* d_prefix = prefix;
@@ -1359,7 +1414,7 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeAccessPolicyWindow;
     at[0].val.accessPolicyWindow.base_ptr = e->d_graph;
-    at[0].val.accessPolicyWindow.num_bytes = (size_t)e->graph_bytes;
+    at[0].val.accessPolicyWindow.num_bytes = e->l2_window;
     at[0].val.accessPolicyWindow.hitRatio = 1.0f;
     at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
@@ -1369,20 +1424,24 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
     lc.stream = st;
     lc.attrs = at;
     lc.numAttrs = e->l2_persist ? 1 : 0;
-    cudaLaunchKernelEx(&lc, main_k, e->dview, e->layout, e->d_arena, slots, d_prefix, d_poff,
-                       d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts, d_out, d_legal, lw,
-                       e->d_ctr + 1, perm, sv, max_acts);
+    cudaError_t le = cudaLaunchKernelEx(&lc, main_k, e->dview, e->layout, e->d_arena, slots,
+                                        d_prefix, d_poff, d_seeds, n, maxd, e->cp, e->baseline,
+                                        d_acts, d_nacts, d_out, d_legal, lw, e->d_ctr + 1, perm,
+                                        sv, max_acts);
+    // the retry launch reads the statuses the main launch writes: never
+    // queue it behind a main launch that failed to start
+    if (le != cudaSuccess) return le;
     retry_k<<<bgrid, kBlock, 0, st>>>(e->dview, e->big_layout, e->d_big_arena, bs, d_prefix,
                                       d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
                                       d_nacts, d_out, d_legal, lw, nullptr, nullptr,
                                       SchedView(), max_acts);
+    return cudaGetLastError();
   };
-  if (e->wl.resurface)
-    launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>);
-  else
-    launch(pe_rollout_kernel<false, false>, pe_rollout_kernel<true, false>);
+  cudaError_t lerr = e->wl.resurface
+                         ? launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>)
+                         : launch(pe_rollout_kernel<false, false>, pe_rollout_kernel<true, false>);
   e->launches += 2;
-  if (!cuda_ok(cudaGetLastError(), err, "pe_rollout_kernel launch")) return PE_ERR_CUDA;
+  if (!cuda_ok(lerr, err, "pe_rollout_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {
     uint32_t kmax = 0;
     bool ok = cuda_ok(cudaMemcpyAsync(&kmax, max_acts, 4, cudaMemcpyDeviceToHost, st), err,
@@ -1401,8 +1460,10 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
     if (ok && legal_out)
       ok = cuda_ok(cudaMemcpyAsync(legal_out, d_legal, (size_t)n * lw * 8,
                                    cudaMemcpyDeviceToHost, st), err, "D2H legal");
-    if (!ok) return PE_ERR_CUDA;
+    if (!ok || !call_end(e, st, err)) return PE_ERR_CUDA;
     if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
+  } else if (!call_end(e, st, err)) {
+    return PE_ERR_CUDA;
   } else if (flags & PE_SYNC) {
     if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
   }

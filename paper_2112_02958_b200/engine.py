@@ -229,6 +229,30 @@ class Engine:
             lgl = [list(lg[i * self.legal_words:(i + 1) * self.legal_words]) for i in range(n)]
         return list(out), seqs, lgl
 
+    def rollout_roots_np(self, seeds):
+        """Root rollouts (every prefix empty) for a large batch, through the
+        host-buffer C-ABI, returned as numpy arrays: results (n, 192) uint8
+        (raw pe_result records), actions (n, max_decisions, 4) uint32 as
+        (value, dim, axis, kind) and n_acts (n,) uint32.  Action rows past
+        n_acts are unspecified (pe.h)."""
+        import numpy as np
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        n = int(seeds.shape[0])
+        maxd = self.cfg.max_decisions
+        poff = np.zeros(n + 1, dtype=np.uint32)
+        aout = np.zeros((n, maxd, 8), dtype=np.uint8)
+        nout = np.zeros(n, dtype=np.uint32)
+        out = np.zeros((n, C.sizeof(PeResult)), dtype=np.uint8)
+        err = PeError()
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        rc = self.lib.pe_rollout_batch(self.h, None, p(poff), p(seeds), n, p(aout), p(nout),
+                                       p(out), None, 0, None, C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        v = aout.view(np.uint32)[..., 0]
+        acts = np.stack([v, aout[..., 4], aout[..., 5], aout[..., 6]], axis=-1).astype(np.uint32)
+        return out, acts, nout
+
     def infer_rest(self, prefix):
         """infer_rest (REF propagate.cc:484-544) after `prefix`: returns
         prefix + [INFER_REST marker] + inferred TILE actions."""
