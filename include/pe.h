@@ -103,7 +103,8 @@ typedef struct pe_result {
   int32_t status;           /* PE_CAND_*                                    */
   int32_t fail_step;        /* index of the failing action, or -1           */
   int32_t feasible;         /* peak <= memory budget                        */
-  int32_t reserved;
+  int32_t reserved;         /* 0 */
+  int32_t reserved2;        /* 0 (explicit: no uninitialised padding bytes) */
   double runtime_s;         /* runtime_estimate                             */
   double reward;            /* reward in [0,1]                              */
 } pe_result;
@@ -182,6 +183,45 @@ typedef struct pe_graph pe_graph;
  * accepted as search roots. */
 pe_status pe_graph_create(const char* pir, size_t len, pe_graph** out,
                           pe_error* err);
+
+/* Structured construction: the same graph from arrays instead of text, for
+ * a reference-side binding that walks a `partir::Program` (REF ir.h:84-131)
+ * directly instead of printing it and re-parsing.  Values
+ * are indexed args first, then ops; an op may only use earlier values.  The
+ * graph is shape-checked exactly as pe_graph_create's. */
+typedef struct pe_arg_desc {
+  const char* id;     /* value name (NULL: "a<i>")                        */
+  const char* scope;  /* SPEC `scope` attribute, may be NULL              */
+  int32_t rank;
+  int64_t shape[PE_MAX_RANK];
+} pe_arg_desc;
+
+typedef struct pe_op_desc {
+  const char* id;           /* value name (NULL: "<i>")                    */
+  int32_t kind;             /* REF OpKind value (ir.h:31-62), base dialect */
+  int32_t rank;             /* declared result type                        */
+  int64_t shape[PE_MAX_RANK];
+  int32_t n_operands;
+  const int32_t* operands;  /* value indices                               */
+  /* dot (REF ir.h DotDims): n_batch / n_contract pairs                    */
+  int32_t n_batch, n_contract;
+  int32_t lhs_batch[PE_MAX_RANK], rhs_batch[PE_MAX_RANK];
+  int32_t lhs_contract[PE_MAX_RANK], rhs_contract[PE_MAX_RANK];
+  /* reduce dims / transpose perm / broadcast_in_dim map                   */
+  int32_t n_dims;
+  int32_t dims[PE_MAX_RANK];
+  int64_t start[PE_MAX_RANK], limit[PE_MAX_RANK]; /* slice (rank entries) */
+  int32_t dim;              /* concatenate                                 */
+  double value;             /* constant                                    */
+  const char* scope;        /* may be NULL                                 */
+} pe_op_desc;
+
+pe_status pe_graph_create_from_arrays(const char* name, int32_t n_axes,
+                                      const char* const* axis_names,
+                                      const int64_t* axis_sizes, int32_t n_args,
+                                      const pe_arg_desc* args, int32_t n_ops,
+                                      const pe_op_desc* ops, int32_t result,
+                                      pe_graph** out, pe_error* err);
 void pe_graph_destroy(pe_graph* g);
 int32_t pe_graph_num_args(const pe_graph* g);
 int32_t pe_graph_num_ops(const pe_graph* g);
@@ -191,6 +231,8 @@ int64_t pe_graph_axis_size(const pe_graph* g, int32_t axis);
 /* value index of `%name` (args first, then ops), -1 when absent */
 int32_t pe_graph_value_index(const pe_graph* g, const char* name);
 int32_t pe_graph_axis_index(const pe_graph* g, const char* name);
+/* mesh axis name into buf (declaration order); returns length or -1 */
+int32_t pe_graph_axis_name(const pe_graph* g, int32_t axis, char* buf, int32_t cap);
 /* value name into buf; returns length or -1 */
 int32_t pe_graph_value_name(const pe_graph* g, int32_t value, char* buf,
                             int32_t cap);

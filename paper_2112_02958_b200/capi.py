@@ -63,7 +63,7 @@ class PeResult(C.Structure):
         ("sbc_cnt", C.c_int32 * PE_MAX_AXES),
         ("n_spmd_ops", C.c_int32), ("n_stuck", C.c_int32), ("n_steps", C.c_int32),
         ("status", C.c_int32), ("fail_step", C.c_int32), ("feasible", C.c_int32),
-        ("reserved", C.c_int32),
+        ("reserved", C.c_int32), ("reserved2", C.c_int32),
         ("runtime_s", C.c_double), ("reward", C.c_double),
     ]
 
@@ -90,6 +90,23 @@ class PeSearchConfig(C.Structure):
         self.worklist_args = C.cast(arr, C.POINTER(C.c_uint32))
         self.n_worklist_args = len(args)
         return self
+
+
+class PeArgDesc(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("scope", C.c_char_p), ("rank", C.c_int32),
+                ("shape", C.c_int64 * PE_MAX_RANK)]
+
+
+class PeOpDesc(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("kind", C.c_int32), ("rank", C.c_int32),
+                ("shape", C.c_int64 * PE_MAX_RANK), ("n_operands", C.c_int32),
+                ("operands", C.POINTER(C.c_int32)), ("n_batch", C.c_int32),
+                ("n_contract", C.c_int32), ("lhs_batch", C.c_int32 * PE_MAX_RANK),
+                ("rhs_batch", C.c_int32 * PE_MAX_RANK), ("lhs_contract", C.c_int32 * PE_MAX_RANK),
+                ("rhs_contract", C.c_int32 * PE_MAX_RANK), ("n_dims", C.c_int32),
+                ("dims", C.c_int32 * PE_MAX_RANK), ("start", C.c_int64 * PE_MAX_RANK),
+                ("limit", C.c_int64 * PE_MAX_RANK), ("dim", C.c_int32), ("value", C.c_double),
+                ("scope", C.c_char_p)]
 
 
 PE_PLAN_MAX_ACTIONS = 64
@@ -133,7 +150,13 @@ SIGNATURES = {
     "pe_default_cost_params": (None, [C.POINTER(PeCostParams)]),
     "pe_default_search_config": (None, [C.POINTER(PeSearchConfig)]),
     "pe_graph_create": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(_P), C.POINTER(PeError)]),
+    "pe_graph_create_from_arrays": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_char_p),
+                                              C.POINTER(C.c_int64), C.c_int32,
+                                              C.POINTER(PeArgDesc), C.c_int32,
+                                              C.POINTER(PeOpDesc), C.c_int32, C.POINTER(_P),
+                                              C.POINTER(PeError)]),
     "pe_graph_destroy": (None, [_P]),
+    "pe_graph_axis_name": (C.c_int32, [_P, C.c_int32, C.c_char_p, C.c_int32]),
     "pe_graph_num_args": (C.c_int32, [_P]),
     "pe_graph_num_ops": (C.c_int32, [_P]),
     "pe_graph_num_axes": (C.c_int32, [_P]),

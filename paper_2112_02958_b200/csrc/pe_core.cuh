@@ -1673,6 +1673,7 @@ struct Cand {
     tick(0);
     r.fail_step = -1;
     r.reserved = 0;
+    r.reserved2 = 0;
     int32_t steps = 0;
     bool propagated = false;
     for (int32_t k = 0; k < n; ++k) {
@@ -1809,6 +1810,7 @@ struct Cand {
     tick(0);
     r.fail_step = -1;
     r.reserved = 0;
+    r.reserved2 = 0;
     if (legal_out)
       for (int32_t w = 0; w < legal_words; ++w) legal_out[w] = 0;
     // resurfacing runs at decision boundaries: before the next decision of

@@ -509,7 +509,102 @@ pe_status pe_graph_create(const char* pir, size_t len, pe_graph** out, pe_error*
   return PE_OK;
 }
 
+pe_status pe_graph_create_from_arrays(const char* name, int32_t n_axes,
+                                      const char* const* axis_names, const int64_t* axis_sizes,
+                                      int32_t n_args, const pe_arg_desc* args, int32_t n_ops,
+                                      const pe_op_desc* ops, int32_t result, pe_graph** out,
+                                      pe_error* err) {
+  if (!out || n_axes < 0 || n_args < 0 || n_ops < 0 || (n_axes && (!axis_names || !axis_sizes)) ||
+      (n_args && !args) || (n_ops && !ops)) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument or negative count");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  pe_graph* g = new (std::nothrow) pe_graph();
+  if (!g) {
+    set_err(err, PE_ERR_INTERNAL, "out of memory");
+    return PE_ERR_INTERNAL;
+  }
+  pe::HostGraph& h = g->g;
+  auto bad = [&](const std::string& m) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, m);
+    delete g;
+    return PE_ERR_INVALID_ARGUMENT;
+  };
+  h.name = name ? name : "";
+  for (int32_t a = 0; a < n_axes; ++a) {
+    h.axis_names.push_back(axis_names[a] ? axis_names[a] : "");
+    h.axis_sizes.push_back(axis_sizes[a]);
+  }
+  auto dims_of = [](int32_t rank, const int64_t* sh) {
+    return std::vector<int64_t>(sh, sh + std::max(0, std::min(rank, (int32_t)PE_MAX_RANK)));
+  };
+  for (int32_t a = 0; a < n_args; ++a) {
+    const pe_arg_desc& d = args[a];
+    if (d.rank < 0 || d.rank > PE_MAX_RANK) return bad("argument rank out of range");
+    pe::HostArg x;
+    x.id = d.id ? d.id : "a" + std::to_string(a);
+    x.scope = d.scope ? d.scope : "";
+    x.shape = dims_of(d.rank, d.shape);
+    h.args.push_back(std::move(x));
+  }
+  for (int32_t o = 0; o < n_ops; ++o) {
+    const pe_op_desc& d = ops[o];
+    if (d.kind < 0 || d.kind >= pe::kNumBaseKinds) return bad("op kind outside the base dialect");
+    if (d.rank < 0 || d.rank > PE_MAX_RANK || d.n_operands < 0 || (d.n_operands && !d.operands) ||
+        d.n_batch < 0 || d.n_batch > PE_MAX_RANK || d.n_contract < 0 ||
+        d.n_contract > PE_MAX_RANK || d.n_dims < 0 || d.n_dims > PE_MAX_RANK)
+      return bad("op descriptor field out of range");
+    pe::HostOp x;
+    x.id = d.id ? d.id : std::to_string(o);
+    x.kind = (pe::Kind)d.kind;
+    x.shape = dims_of(d.rank, d.shape);
+    for (int32_t k = 0; k < d.n_operands; ++k) {
+      if (d.operands[k] < 0 || d.operands[k] >= n_args + o)
+        return bad("op " + x.id + ": operand is not an earlier value");
+      x.operands.push_back(d.operands[k]);
+    }
+    x.lhs_batch.assign(d.lhs_batch, d.lhs_batch + d.n_batch);
+    x.rhs_batch.assign(d.rhs_batch, d.rhs_batch + d.n_batch);
+    x.lhs_contract.assign(d.lhs_contract, d.lhs_contract + d.n_contract);
+    x.rhs_contract.assign(d.rhs_contract, d.rhs_contract + d.n_contract);
+    x.dims.assign(d.dims, d.dims + d.n_dims);
+    if (x.kind == pe::kSlice && !x.operands.empty()) {
+      int32_t r = (int32_t)h.value_shape(x.operands[0]).size();
+      x.start.assign(d.start, d.start + r);
+      x.limit.assign(d.limit, d.limit + r);
+    }
+    x.dim = d.dim;
+    x.value = d.value;
+    x.scope = d.scope ? d.scope : "";
+    h.ops.push_back(std::move(x));
+  }
+  if (result < 0 || result >= n_args + n_ops) return bad("result is not a value index");
+  h.result = result;
+  std::vector<std::string> seen;
+  for (int32_t v = 0; v < h.num_values(); ++v) {
+    const std::string& id = v < n_args ? h.args[v].id : h.ops[v - n_args].id;
+    seen.push_back(id);
+  }
+  std::sort(seen.begin(), seen.end());
+  if (std::adjacent_find(seen.begin(), seen.end()) != seen.end()) return bad("duplicate value name");
+  pe::LoadError le;
+  if (!pe::finish_graph(h, le)) {
+    set_err(err, le.code, le.message);
+    delete g;
+    return (pe_status)le.code;
+  }
+  *out = g;
+  if (err) err->code = PE_OK;
+  return PE_OK;
+}
+
 void pe_graph_destroy(pe_graph* g) { delete g; }
+int32_t pe_graph_axis_name(const pe_graph* g, int32_t axis, char* buf, int32_t cap) {
+  if (!g || axis < 0 || axis >= (int32_t)g->g.axis_names.size()) return -1;
+  const std::string& s = g->g.axis_names[axis];
+  if (buf && cap > 0) std::snprintf(buf, cap, "%s", s.c_str());
+  return (int32_t)s.size();
+}
 int32_t pe_graph_num_args(const pe_graph* g) { return (int32_t)g->g.args.size(); }
 int32_t pe_graph_num_ops(const pe_graph* g) { return (int32_t)g->g.ops.size(); }
 int32_t pe_graph_num_axes(const pe_graph* g) { return (int32_t)g->g.axis_names.size(); }

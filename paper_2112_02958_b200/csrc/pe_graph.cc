@@ -1,9 +1,10 @@
-// pe_graph.cc — `.pir` loader and graph compiler (host C++).
+// pe_graph.cc — graph checking and compilation (host C++).
 //
-// Replaces REF parse_program (parser.cc:461-467) + validate
-// (validate.cc:371-389) for the untiled programs the search starts from, and
+// A HostGraph arrives from the `.pir` reader (pe_pir.cc) or from structured
+// arrays (pe_graph_create_from_arrays).  This file checks its shapes (the
+// rules REF validate enforces for the base dialect, validate.cc:161-225) and
 // precompiles the per-op propagation rules of REF registry.cc:123-206 into
-// flat tables.  The grammar follows SPEC tensor_ir "External Interfaces".
+// the flat tables of pe::GraphView.
 #include "pe_graph.h"
 
 #include <algorithm>
@@ -19,527 +20,214 @@
 namespace pe {
 namespace {
 
-// ---------------------------------------------------------------- lexer
-enum class Tok { kIdent, kValue, kAt, kString, kNumber, kLParen, kRParen, kLBrace,
-                 kRBrace, kLBracket, kRBracket, kComma, kColon, kEquals, kArrow, kEnd };
-
-struct Token {
-  Tok tok = Tok::kEnd;
-  std::string text;
-  int line = 1, column = 1;
-};
-
-struct Fail {
+// ---------------------------------------------------------------- checking
+// Shape checking of the base dialect: every op's declared result type must
+// equal the type its kind infers from its operands (the shape rules of
+// SPEC tensor_ir; the reference enforces them in validate, REF
+// validate.cc:161-225).  On top of those, the engine's own limits: rank <= 4,
+// <= 4 mesh axes, dims and axis sizes that fit int32 (its value records).
+struct Bad {
   LoadError e;
 };
-
-[[noreturn]] void parse_fail(const Token& t, const std::string& msg) {
-  Fail f;
-  f.e.code = PE_ERR_PARSE;
-  f.e.line = t.line;
-  f.e.column = t.column;
-  f.e.message = "parse error at " + std::to_string(t.line) + ":" + std::to_string(t.column) +
-                ": " + msg;
-  throw f;
+[[noreturn]] void reject(const std::string& msg, int code = PE_ERR_VALIDATION) {
+  Bad b;
+  b.e.code = code;
+  b.e.message = msg;
+  throw b;
 }
 
-[[noreturn]] void invalid(const std::string& msg, int code = PE_ERR_VALIDATION) {
-  Fail f;
-  f.e.code = code;
-  f.e.message = msg;
-  throw f;
+std::string type_text(const std::vector<int64_t>& dims) {
+  std::string t = "f32[";
+  for (size_t i = 0; i < dims.size(); ++i) {
+    if (i) t += ',';
+    t += std::to_string(dims[i]);
+  }
+  return t + "]";
 }
 
-class Lexer {
- public:
-  Lexer(const char* s, size_t n) : s_(s), n_(n) {}
-  Token next() {
-    skip();
-    Token t;
-    t.line = line_;
-    t.column = col_;
-    if (p_ >= n_) return t;
-    char c = s_[p_];
-    auto single = [&](Tok k) {
-      t.tok = k;
-      adv();
-      return t;
-    };
-    switch (c) {
-      case '(': return single(Tok::kLParen);
-      case ')': return single(Tok::kRParen);
-      case '{': return single(Tok::kLBrace);
-      case '}': return single(Tok::kRBrace);
-      case '[': return single(Tok::kLBracket);
-      case ']': return single(Tok::kRBracket);
-      case ',': return single(Tok::kComma);
-      case ':': return single(Tok::kColon);
-      case '=': return single(Tok::kEquals);
-      case '@': return single(Tok::kAt);
-      default: break;
-    }
-    if (c == '%') {
-      adv();
-      t.tok = Tok::kValue;
-      t.text = ident();
-      if (t.text.empty()) parse_fail(t, "expected value name after '%'");
-      return t;
-    }
-    if (c == '"') {
-      adv();
-      t.tok = Tok::kString;
-      while (p_ < n_ && s_[p_] != '"') {
-        t.text += s_[p_];
-        adv();
-      }
-      if (p_ >= n_) parse_fail(t, "unterminated string");
-      adv();
-      return t;
-    }
-    if (c == '-' && p_ + 1 < n_ && s_[p_ + 1] == '>') {
-      adv();
-      adv();
-      t.tok = Tok::kArrow;
-      return t;
-    }
-    if (std::isdigit((unsigned char)c) || c == '-' || c == '+') {
-      t.tok = Tok::kNumber;
-      size_t b = p_;
-      adv();
-      while (p_ < n_ && (std::isdigit((unsigned char)s_[p_]) || s_[p_] == '.' || s_[p_] == 'e' ||
-                         s_[p_] == 'E' ||
-                         ((s_[p_] == '-' || s_[p_] == '+') && (s_[p_ - 1] == 'e' || s_[p_ - 1] == 'E'))))
-        adv();
-      t.text.assign(s_ + b, p_ - b);
-      return t;
-    }
-    if (std::isalpha((unsigned char)c) || c == '_') {
-      t.tok = Tok::kIdent;
-      t.text = ident();
-      return t;
-    }
-    parse_fail(t, std::string("unexpected character '") + c + "'");
-  }
+using Shape = std::vector<int64_t>;
+// Inference per kind: fills `out` or returns why the op is malformed.
+using Infer = std::string (*)(const HostOp& op, const std::vector<Shape>& in, Shape& out);
 
- private:
-  void skip() {
-    while (p_ < n_) {
-      char c = s_[p_];
-      if (c == '/' && p_ + 1 < n_ && s_[p_ + 1] == '/') {
-        while (p_ < n_ && s_[p_] != '\n') adv();
-      } else if (std::isspace((unsigned char)c)) {
-        adv();
-      } else {
-        break;
-      }
-    }
-  }
-  std::string ident() {
-    std::string o;
-    while (p_ < n_ && (std::isalnum((unsigned char)s_[p_]) || s_[p_] == '_' || s_[p_] == '.' ||
-                       s_[p_] == '/')) {
-      o += s_[p_];
-      adv();
-    }
-    return o;
-  }
-  void adv() {
-    if (s_[p_] == '\n') {
-      ++line_;
-      col_ = 1;
-    } else {
-      ++col_;
-    }
-    ++p_;
-  }
-  const char* s_;
-  size_t n_, p_ = 0;
-  int line_ = 1, col_ = 1;
-};
+std::string want_arity(const std::vector<Shape>& in, size_t n) {
+  if (in.size() == n) return "";
+  return "takes " + std::to_string(n) + " operand" + (n == 1 ? "" : "s") + ", has " +
+         std::to_string(in.size());
+}
+bool dim_ok(int d, size_t rank) { return d >= 0 && (size_t)d < rank; }
 
-const std::map<std::string, Kind>& kind_names() {
-  static const std::map<std::string, Kind> m = {
-      {"constant", kConstant}, {"add", kAdd}, {"sub", kSub}, {"mul", kMul},
-      {"div", kDiv}, {"neg", kNeg}, {"exp", kExp}, {"tanh", kTanh},
-      {"rsqrt", kRsqrt}, {"maximum", kMaximum}, {"dot", kDot},
-      {"reduce_sum", kReduceSum}, {"reduce_max", kReduceMax},
-      {"transpose", kTranspose}, {"reshape", kReshape},
-      {"broadcast_in_dim", kBroadcastInDim}, {"slice", kSlice},
-      {"concatenate", kConcatenate}};
-  return m;
+std::string infer_nullary(const HostOp& op, const std::vector<Shape>& in, Shape& out) {
+  out = op.shape;
+  return want_arity(in, 0);
+}
+std::string infer_unary(const HostOp&, const std::vector<Shape>& in, Shape& out) {
+  std::string w = want_arity(in, 1);
+  if (w.empty()) out = in[0];
+  return w;
+}
+std::string infer_binary(const HostOp&, const std::vector<Shape>& in, Shape& out) {
+  std::string w = want_arity(in, 2);
+  if (!w.empty()) return w;
+  if (in[0] != in[1]) return "pointwise operands " + type_text(in[0]) + " and " + type_text(in[1]) + " disagree";
+  out = in[0];
+  return "";
+}
+std::string infer_dot(const HostOp& op, const std::vector<Shape>& in, Shape& out) {
+  std::string w = want_arity(in, 2);
+  if (!w.empty()) return w;
+  const Shape &l = in[0], &r = in[1];
+  if (op.lhs_batch.size() != op.rhs_batch.size() || op.lhs_contract.size() != op.rhs_contract.size())
+    return "lhs and rhs dimension lists have different lengths";
+  std::vector<char> lused(l.size(), 0), rused(r.size(), 0);
+  auto pair_up = [&](const std::vector<int>& a, const std::vector<int>& b, const char* what) {
+    for (size_t i = 0; i < a.size(); ++i) {
+      if (!dim_ok(a[i], l.size()) || !dim_ok(b[i], r.size()))
+        return std::string(what) + " dim pair " + std::to_string(i) + " is out of range";
+      if (l[a[i]] != r[b[i]]) return std::string(what) + " dims of different sizes";
+      if (lused[a[i]]++ || rused[b[i]]++) return std::string(what) + " dim listed twice";
+    }
+    return std::string();
+  };
+  std::string e = pair_up(op.lhs_batch, op.rhs_batch, "batch");
+  if (e.empty()) e = pair_up(op.lhs_contract, op.rhs_contract, "contracting");
+  if (!e.empty()) return e;
+  out.clear();  // batch dims, then lhs free dims, then rhs free dims
+  for (int b : op.lhs_batch) out.push_back(l[b]);
+  for (size_t i = 0; i < l.size(); ++i)
+    if (!lused[i]) out.push_back(l[i]);
+  for (size_t i = 0; i < r.size(); ++i)
+    if (!rused[i]) out.push_back(r[i]);
+  return "";
+}
+std::string infer_reduce(const HostOp& op, const std::vector<Shape>& in, Shape& out) {
+  std::string w = want_arity(in, 1);
+  if (!w.empty()) return w;
+  std::vector<char> gone(in[0].size(), 0);
+  for (int d : op.dims) {
+    if (!dim_ok(d, in[0].size())) return "reduced dim " + std::to_string(d) + " is out of range";
+    if (gone[d]++) return "reduced dim " + std::to_string(d) + " listed twice";
+  }
+  out.clear();
+  for (size_t i = 0; i < in[0].size(); ++i)
+    if (!gone[i]) out.push_back(in[0][i]);
+  return "";
+}
+std::string infer_transpose(const HostOp& op, const std::vector<Shape>& in, Shape& out) {
+  std::string w = want_arity(in, 1);
+  if (!w.empty()) return w;
+  std::vector<char> hit(in[0].size(), 0);
+  if (op.dims.size() != in[0].size()) return "permutation length differs from the operand rank";
+  out.clear();
+  for (int d : op.dims) {
+    if (!dim_ok(d, in[0].size()) || hit[d]++) return "perm is not a permutation of the operand dims";
+    out.push_back(in[0][d]);
+  }
+  return "";
+}
+std::string infer_reshape(const HostOp& op, const std::vector<Shape>& in, Shape& out) {
+  std::string w = want_arity(in, 1);
+  if (!w.empty()) return w;
+  int64_t from = 1, to = 1;
+  for (int64_t d : in[0]) from *= d;
+  for (int64_t d : op.shape) to *= d;
+  if (from != to) return "reshape from " + type_text(in[0]) + " must keep the element count";
+  out = op.shape;
+  return "";
+}
+std::string infer_broadcast(const HostOp& op, const std::vector<Shape>& in, Shape& out) {
+  std::string w = want_arity(in, 1);
+  if (!w.empty()) return w;
+  if (op.dims.size() != in[0].size()) return "map needs one entry per operand dim";
+  for (size_t i = 0; i < op.dims.size(); ++i) {
+    int m = op.dims[i];
+    if (!dim_ok(m, op.shape.size())) return "map entry " + std::to_string(m) + " is out of range";
+    if (i > 0 && m <= op.dims[i - 1]) return "map entries must increase";
+    if (op.shape[m] != in[0][i]) return "operand dim " + std::to_string(i) + " does not fit result dim " + std::to_string(m);
+  }
+  out = op.shape;
+  return "";
+}
+std::string infer_slice(const HostOp& op, const std::vector<Shape>& in, Shape& out) {
+  std::string w = want_arity(in, 1);
+  if (!w.empty()) return w;
+  size_t r = in[0].size();
+  if (op.start.size() != r || op.limit.size() != r) return "start and limit need one entry per dim";
+  out.clear();
+  for (size_t i = 0; i < r; ++i) {
+    if (!(0 <= op.start[i] && op.start[i] < op.limit[i] && op.limit[i] <= in[0][i]))
+      return "bounds of dim " + std::to_string(i) + " are not 0 <= start < limit <= size";
+    out.push_back(op.limit[i] - op.start[i]);
+  }
+  return "";
+}
+std::string infer_concat(const HostOp& op, const std::vector<Shape>& in, Shape& out) {
+  if (in.size() < 2) return "concatenates at least two operands";
+  if (!dim_ok(op.dim, in[0].size())) return "concatenation dim is out of range";
+  out = in[0];
+  for (size_t k = 1; k < in.size(); ++k) {
+    if (in[k].size() != in[0].size()) return "operands of different ranks";
+    for (size_t d = 0; d < in[0].size(); ++d)
+      if ((int)d != op.dim && in[k][d] != in[0][d])
+        return "operand " + std::to_string(k) + " differs outside the concatenation dim";
+    out[op.dim] += in[k][op.dim];
+  }
+  return "";
 }
 
-// ---------------------------------------------------------------- parser
-class Parser {
- public:
-  Parser(const char* s, size_t n, HostGraph& g) : lx_(s, n), g_(g) { adv(); }
-
-  void parse() {
-    if (cur_.tok == Tok::kIdent && cur_.text == "mesh") {
-      adv();
-      expect(Tok::kLBrace, "'{'");
-      while (cur_.tok != Tok::kRBrace) {
-        g_.axis_names.push_back(expect(Tok::kString, "axis name string").text);
-        expect(Tok::kEquals, "'='");
-        g_.axis_sizes.push_back(expect_int("axis size"));
-        if (cur_.tok == Tok::kComma) adv();
-        else break;
-      }
-      expect(Tok::kRBrace, "'}'");
-    }
-    expect_ident("func");
-    expect(Tok::kAt, "'@'");
-    g_.name = expect(Tok::kIdent, "function name").text;
-    expect(Tok::kLParen, "'('");
-    while (cur_.tok != Tok::kRParen) {
-      HostArg a;
-      a.id = expect(Tok::kValue, "argument name").text;
-      expect(Tok::kColon, "':'");
-      a.shape = parse_type();
-      if (cur_.tok == Tok::kLBrace) {
-        adv();
-        expect_ident("scope");
-        expect(Tok::kEquals, "'='");
-        a.scope = expect(Tok::kString, "scope string").text;
-        expect(Tok::kRBrace, "'}'");
-      }
-      define(a.id);
-      g_.args.push_back(std::move(a));
-      if (cur_.tok == Tok::kComma) adv();
-      else break;
-    }
-    expect(Tok::kRParen, "')'");
-    expect(Tok::kArrow, "'->'");
-    parse_type();
-    expect(Tok::kLBrace, "'{'");
-    for (;;) {
-      if (cur_.tok == Tok::kIdent && cur_.text == "return") {
-        adv();
-        Token r = expect(Tok::kValue, "terminator value");
-        auto it = ids_.find(r.text);
-        if (it == ids_.end())
-          invalid("returned value %" + r.text + " is not defined at top level");
-        g_.result = it->second;
-        expect(Tok::kRBrace, "'}'");
-        break;
-      }
-      if (cur_.tok != Tok::kValue) parse_fail(cur_, "expected op definition or 'return'");
-      HostOp op;
-      op.id = cur_.text;
-      adv();
-      expect(Tok::kEquals, "'='");
-      parse_op(op);
-      define(op.id);
-      g_.ops.push_back(std::move(op));
-    }
-    if (cur_.tok != Tok::kEnd) parse_fail(cur_, "trailing input after function body");
+Infer infer_for(Kind k) {
+  switch (k) {
+    case kConstant: return infer_nullary;
+    case kNeg: case kExp: case kTanh: case kRsqrt: return infer_unary;
+    case kAdd: case kSub: case kMul: case kDiv: case kMaximum: return infer_binary;
+    case kDot: return infer_dot;
+    case kReduceSum: case kReduceMax: return infer_reduce;
+    case kTranspose: return infer_transpose;
+    case kReshape: return infer_reshape;
+    case kBroadcastInDim: return infer_broadcast;
+    case kSlice: return infer_slice;
+    case kConcatenate: return infer_concat;
+    default: return nullptr;
   }
-
- private:
-  void define(const std::string& id) {
-    int32_t idx = (int32_t)(g_.args.size() + g_.ops.size());
-    if (id.empty() || !ids_.emplace(id, idx).second) invalid("redefinition of %" + id);
-  }
-
-  void parse_op(HostOp& op) {
-    Token kt = expect(Tok::kIdent, "op kind");
-    if (kt.text == "tile" || kt.text == "sum" || kt.text == "atomic" || kt.text == "slice_axis")
-      invalid("op %" + op.id + ": tiled-dialect programs are not accepted as search roots; "
-              "the engine starts from the untiled graph",
-              PE_ERR_INVALID_ARGUMENT);
-    if (kt.text == "all_reduce" || kt.text == "all_gather" || kt.text == "slice_by_coord")
-      parse_fail(kt, "SPMD ops cannot appear in the textual input form");
-    auto it = kind_names().find(kt.text);
-    if (it == kind_names().end()) parse_fail(kt, "unknown op '" + kt.text + "'");
-    op.kind = it->second;
-    expect(Tok::kLParen, "'('");
-    while (cur_.tok != Tok::kRParen) {
-      Token v = expect(Tok::kValue, "operand");
-      auto f = ids_.find(v.text);
-      if (f == ids_.end())
-        invalid("op %" + op.id + ": unknown or not-yet-defined value %" + v.text);
-      op.operands.push_back(f->second);
-      if (cur_.tok == Tok::kComma) adv();
-      else break;
-    }
-    expect(Tok::kRParen, "')'");
-    if (cur_.tok == Tok::kLBrace) parse_attrs(op);
-    expect(Tok::kColon, "':'");
-    op.shape = parse_type();
-  }
-
-  void parse_attrs(HostOp& op) {
-    expect(Tok::kLBrace, "'{'");
-    while (cur_.tok != Tok::kRBrace) {
-      Token key = expect(Tok::kIdent, "attribute name");
-      expect(Tok::kEquals, "'='");
-      if (key.text == "contract") {
-        int_pair(op.lhs_contract, op.rhs_contract);
-      } else if (key.text == "batch") {
-        int_pair(op.lhs_batch, op.rhs_batch);
-      } else if (key.text == "dims" || key.text == "perm" || key.text == "map") {
-        int_list(op.dims);
-      } else if (key.text == "start") {
-        i64_list(op.start);
-      } else if (key.text == "limit") {
-        i64_list(op.limit);
-      } else if (key.text == "dim") {
-        op.dim = (int)expect_int("dim");
-      } else if (key.text == "value") {
-        Token v = expect(Tok::kNumber, "number");
-        char* end = nullptr;
-        op.value = std::strtod(v.text.c_str(), &end);
-        if (end != v.text.c_str() + v.text.size()) parse_fail(v, "malformed number");
-      } else if (key.text == "scope") {
-        op.scope = expect(Tok::kString, "scope string").text;
-      } else {
-        parse_fail(key, "unknown attribute '" + key.text + "'");
-      }
-      if (cur_.tok == Tok::kComma) adv();
-      else break;
-    }
-    expect(Tok::kRBrace, "'}'");
-  }
-
-  std::vector<int64_t> parse_type() {
-    Token t = expect(Tok::kIdent, "type");
-    if (t.text != "f32") parse_fail(t, "unknown element type '" + t.text + "'");
-    expect(Tok::kLBracket, "'['");
-    std::vector<int64_t> s;
-    while (cur_.tok != Tok::kRBracket) {
-      s.push_back(expect_int("dimension"));
-      if (cur_.tok == Tok::kComma) adv();
-      else break;
-    }
-    expect(Tok::kRBracket, "']'");
-    return s;
-  }
-  void int_list(std::vector<int>& o) {
-    std::vector<int64_t> t;
-    i64_list(t);
-    for (int64_t v : t) o.push_back((int)v);
-  }
-  void i64_list(std::vector<int64_t>& o) {
-    expect(Tok::kLBracket, "'['");
-    while (cur_.tok != Tok::kRBracket) {
-      o.push_back(expect_int("integer"));
-      if (cur_.tok == Tok::kComma) adv();
-      else break;
-    }
-    expect(Tok::kRBracket, "']'");
-  }
-  void int_pair(std::vector<int>& a, std::vector<int>& b) {
-    expect(Tok::kLBracket, "'['");
-    int_list(a);
-    expect(Tok::kComma, "','");
-    int_list(b);
-    expect(Tok::kRBracket, "']'");
-  }
-  int64_t expect_int(const char* what) {
-    Token t = expect(Tok::kNumber, what);
-    const char* s = t.text.c_str();
-    char* end = nullptr;
-    long long v = std::strtoll(s, &end, 10);
-    if (end != s + t.text.size() || t.text.empty() || t.text[0] == '+')
-      parse_fail(t, std::string("expected integer ") + what);
-    return v;
-  }
-  Token expect(Tok k, const char* what) {
-    if (cur_.tok != k) parse_fail(cur_, std::string("expected ") + what);
-    Token t = cur_;
-    adv();
-    return t;
-  }
-  void expect_ident(const char* name) {
-    if (cur_.tok != Tok::kIdent || cur_.text != name)
-      parse_fail(cur_, std::string("expected '") + name + "'");
-    adv();
-  }
-  void adv() { cur_ = lx_.next(); }
-
-  Lexer lx_;
-  HostGraph& g_;
-  Token cur_;
-  std::map<std::string, int32_t> ids_;
-};
-
-// ---------------------------------------------------------------- validate
-// Shape inference of the base dialect (REF validate.cc:161-225).
-std::string shape_str(const std::vector<int64_t>& s) {
-  std::string o = "f32[";
-  for (size_t i = 0; i < s.size(); ++i) o += (i ? "," : "") + std::to_string(s[i]);
-  return o + "]";
 }
 
-void validate(const HostGraph& g) {
-  std::set<std::string> names;
+void check_dims(const std::string& who, const Shape& s) {
+  if ((int)s.size() > kMaxRank) reject(who + ": rank " + std::to_string(s.size()) + " > 4");
+  for (int64_t d : s) {
+    if (d < 1) reject(who + ": every dimension must be >= 1");
+    if (d > kMaxDim) reject(who + ": dimension " + std::to_string(d) + " exceeds 2^31-1", PE_ERR_INVALID_ARGUMENT);
+  }
+}
+
+void check_graph(const HostGraph& g) {
+  if ((int)g.axis_names.size() > kMaxAxes) reject("the engine supports at most 4 mesh axes", PE_ERR_INVALID_ARGUMENT);
   for (size_t a = 0; a < g.axis_names.size(); ++a) {
-    if (g.axis_names[a].empty()) invalid("mesh axis with empty name");
-    if (g.axis_sizes[a] < 1) invalid("mesh axis \"" + g.axis_names[a] + "\" has size < 1");
-    if (g.axis_sizes[a] > kMaxDim)
-      invalid("mesh axis \"" + g.axis_names[a] + "\" size exceeds 2^31-1",
-              PE_ERR_INVALID_ARGUMENT);
-    if (!names.insert(g.axis_names[a]).second)
-      invalid("duplicate mesh axis \"" + g.axis_names[a] + "\"");
+    const std::string who = "mesh axis \"" + g.axis_names[a] + "\"";
+    if (g.axis_names[a].empty()) reject("mesh axes need non-empty names");
+    if (g.axis_sizes[a] < 1) reject(who + ": size must be >= 1");
+    if (g.axis_sizes[a] > kMaxDim) reject(who + ": size exceeds 2^31-1", PE_ERR_INVALID_ARGUMENT);
+    for (size_t b = 0; b < a; ++b)
+      if (g.axis_names[b] == g.axis_names[a]) reject(who + " is declared twice");
   }
-  if ((int)g.axis_names.size() > kMaxAxes)
-    invalid("more than 4 mesh axes", PE_ERR_INVALID_ARGUMENT);
-  if (g.name.empty()) invalid("program without a name");
-  for (const HostArg& a : g.args) {
-    if ((int)a.shape.size() > kMaxRank) invalid("argument %" + a.id + " rank exceeds 4");
-    for (int64_t d : a.shape) {
-      if (d < 1) invalid("argument %" + a.id + " dimension < 1");
-      if (d > kMaxDim)
-        invalid("argument %" + a.id + " dimension exceeds 2^31-1", PE_ERR_INVALID_ARGUMENT);
-    }
-  }
-  auto fail = [](const HostOp& op, const std::string& m, int code = PE_ERR_VALIDATION) {
-    invalid("op %" + op.id + ": " + m, code);
-  };
-  auto in_rank = [&](const HostOp& op, int d, int r, const char* what) {
-    if (d < 0 || d >= r) fail(op, std::string(what) + " " + std::to_string(d) + " out of range");
-  };
+  if (g.name.empty()) reject("the function has no name");
+  for (const HostArg& a : g.args) check_dims("parameter %" + a.id, a.shape);
+  std::vector<Shape> in;
+  Shape got;
   for (const HostOp& op : g.ops) {
-    if ((int)op.shape.size() > kMaxRank) fail(op, "rank exceeds 4");
-    for (int64_t d : op.shape) {
-      if (d < 1) fail(op, "result dimension < 1");
-      if (d > kMaxDim) fail(op, "result dimension exceeds 2^31-1", PE_ERR_INVALID_ARGUMENT);
-    }
-    std::vector<std::vector<int64_t>> in;
+    const std::string who = "%" + op.id;
+    check_dims(who, op.shape);
+    if (op.operands.size() > 8191) reject(who + ": more than 8191 operands", PE_ERR_INVALID_ARGUMENT);
+    Infer f = infer_for(op.kind);
+    if (!f) reject(who + ": kind is outside the base dialect");
+    in.clear();
     for (int32_t v : op.operands) in.push_back(g.value_shape(v));
-    auto arity = [&](size_t n) {
-      if (in.size() != n)
-        fail(op, "expects " + std::to_string(n) + " operand(s), got " + std::to_string(in.size()));
-    };
-    std::vector<int64_t> want;
-    switch (op.kind) {
-      case kConstant:
-        arity(0);
-        want = op.shape;
-        break;
-      case kAdd: case kSub: case kMul: case kDiv: case kMaximum:
-        arity(2);
-        if (in[0] != in[1]) fail(op, "operand shapes differ: " + shape_str(in[0]) + " vs " + shape_str(in[1]));
-        want = in[0];
-        break;
-      case kNeg: case kExp: case kTanh: case kRsqrt:
-        arity(1);
-        want = in[0];
-        break;
-      case kDot: {
-        arity(2);
-        const auto& l = in[0];
-        const auto& r = in[1];
-        if (op.lhs_batch.size() != op.rhs_batch.size()) fail(op, "batch dimension lists differ in length");
-        if (op.lhs_contract.size() != op.rhs_contract.size())
-          fail(op, "contracting dimension lists differ in length");
-        std::set<int> lu, ru;
-        for (size_t i = 0; i < op.lhs_batch.size(); ++i) {
-          in_rank(op, op.lhs_batch[i], (int)l.size(), "lhs batch dim");
-          in_rank(op, op.rhs_batch[i], (int)r.size(), "rhs batch dim");
-          if (l[op.lhs_batch[i]] != r[op.rhs_batch[i]]) fail(op, "batch dimension size mismatch");
-          if (!lu.insert(op.lhs_batch[i]).second || !ru.insert(op.rhs_batch[i]).second)
-            fail(op, "repeated batch dimension");
-        }
-        for (size_t i = 0; i < op.lhs_contract.size(); ++i) {
-          in_rank(op, op.lhs_contract[i], (int)l.size(), "lhs contracting dim");
-          in_rank(op, op.rhs_contract[i], (int)r.size(), "rhs contracting dim");
-          if (l[op.lhs_contract[i]] != r[op.rhs_contract[i]])
-            fail(op, "contracting dimension size mismatch");
-          if (!lu.insert(op.lhs_contract[i]).second || !ru.insert(op.rhs_contract[i]).second)
-            fail(op, "dimension both batch and contracting");
-        }
-        for (int b : op.lhs_batch) want.push_back(l[b]);
-        for (int i = 0; i < (int)l.size(); ++i)
-          if (!lu.count(i)) want.push_back(l[i]);
-        for (int i = 0; i < (int)r.size(); ++i)
-          if (!ru.count(i)) want.push_back(r[i]);
-        if ((int)want.size() > kMaxRank) fail(op, "dot result rank exceeds 4");
-        break;
-      }
-      case kReduceSum: case kReduceMax: {
-        arity(1);
-        std::set<int> red(op.dims.begin(), op.dims.end());
-        if (red.size() != op.dims.size()) fail(op, "repeated reduce dim");
-        for (int d : op.dims) in_rank(op, d, (int)in[0].size(), "reduce dim");
-        for (int i = 0; i < (int)in[0].size(); ++i)
-          if (!red.count(i)) want.push_back(in[0][i]);
-        break;
-      }
-      case kTranspose: {
-        arity(1);
-        int r = (int)in[0].size();
-        if ((int)op.dims.size() != r) fail(op, "permutation length does not match rank");
-        std::set<int> seen(op.dims.begin(), op.dims.end());
-        if ((int)seen.size() != r || (!seen.empty() && (*seen.begin() < 0 || *seen.rbegin() >= r)))
-          fail(op, "permutation is not a bijection on dims");
-        for (int d : op.dims) want.push_back(in[0][d]);
-        break;
-      }
-      case kReshape: {
-        arity(1);
-        int64_t a = 1, b = 1;
-        for (int64_t d : in[0]) a *= d;
-        for (int64_t d : op.shape) b *= d;
-        if (a != b) fail(op, "reshape changes element count");
-        want = op.shape;
-        break;
-      }
-      case kBroadcastInDim: {
-        arity(1);
-        if ((int)op.dims.size() != (int)in[0].size())
-          fail(op, "broadcast dim map length does not match operand rank");
-        int prev = -1;
-        for (size_t i = 0; i < op.dims.size(); ++i) {
-          int m = op.dims[i];
-          in_rank(op, m, (int)op.shape.size(), "broadcast map entry");
-          if (m <= prev) fail(op, "broadcast dim map must be strictly increasing");
-          prev = m;
-          if (in[0][i] != op.shape[m]) fail(op, "broadcast operand dim size mismatch");
-        }
-        want = op.shape;
-        break;
-      }
-      case kSlice: {
-        arity(1);
-        int r = (int)in[0].size();
-        if ((int)op.start.size() != r || (int)op.limit.size() != r)
-          fail(op, "slice start/limit length does not match rank");
-        for (int i = 0; i < r; ++i) {
-          if (op.start[i] < 0 || op.limit[i] > in[0][i] || op.start[i] >= op.limit[i])
-            fail(op, "slice bounds invalid for dim " + std::to_string(i));
-          want.push_back(op.limit[i] - op.start[i]);
-        }
-        break;
-      }
-      case kConcatenate: {
-        if (in.size() < 2) fail(op, "concatenate expects at least 2 operands");
-        in_rank(op, op.dim, (int)in[0].size(), "concatenate dim");
-        want = in[0];
-        for (size_t i = 1; i < in.size(); ++i) {
-          if (in[i].size() != in[0].size()) fail(op, "operand rank mismatch");
-          for (int d = 0; d < (int)in[0].size(); ++d)
-            if (d != op.dim && in[i][d] != in[0][d])
-              fail(op, "non-concat dimension " + std::to_string(d) + " mismatch");
-          want[op.dim] += in[i][op.dim];
-        }
-        if (in.size() > 8191) fail(op, "too many operands", PE_ERR_INVALID_ARGUMENT);
-        break;
-      }
-      default:
-        fail(op, "not a base-dialect op");
-    }
-    if (want != op.shape)
-      fail(op, "declared type " + shape_str(op.shape) + " does not match inferred " + shape_str(want));
-    for (int64_t d : op.shape)
-      if (d > 0x7fffffff) fail(op, "dimension exceeds int32", PE_ERR_INVALID_ARGUMENT);
+    std::string why = f(op, in, got);
+    if (!why.empty()) reject(who + ": " + why);
+    if ((int)got.size() > kMaxRank) reject(who + ": inferred rank exceeds 4");
+    if (got != op.shape)
+      reject(who + ": declared " + type_text(op.shape) + " but the operands give " + type_text(got));
   }
-  for (const HostArg& a : g.args)
-    for (int64_t d : a.shape)
-      if (d > 0x7fffffff) invalid("argument dimension exceeds int32", PE_ERR_INVALID_ARGUMENT);
-  if (g.result < 0) invalid("program has no return");
+  if (g.result < 0) reject("the function returns nothing");
 }
-
 // ---------------------------------------------------------------- rules
 // Per-op propagation rule with GLOBAL operand shapes (REF registry.cc).
 // Class order and member order follow the reference exactly: they fix the
@@ -890,17 +578,19 @@ void attach_worklist(GraphView& v, const Worklist& w) {
   v.ord_mem = w.ord_mem.data();
 }
 
-bool load_graph(const char* text, size_t len, HostGraph& g, LoadError& err) {
+bool finish_graph(HostGraph& g, LoadError& err) {
   try {
-    Parser p(text, len, g);
-    p.parse();
-    validate(g);
+    check_graph(g);
     compile(g);
-  } catch (const Fail& f) {
-    err = f.e;
+  } catch (const Bad& b) {
+    err = b.e;
     return false;
   }
   return true;
+}
+
+bool load_graph(const char* text, size_t len, HostGraph& g, LoadError& err) {
+  return read_pir(text, len, g, err) && finish_graph(g, err);
 }
 
 }  // namespace pe

@@ -1,9 +1,11 @@
-// pe_graph.h — host graph loader + compiler (the boundary's `parse_program`).
+// pe_graph.h — host graph model, loader and compiler (the boundary's
+// `parse_program`, REF parser.h:28).
 //
-// Parses the reference's `.pir` text format (SPEC tensor_ir "External
-// Interfaces"; REF parser.cc), validates it with the reference's shape
-// rules (REF validate.cc:161-225), and compiles it into the SoA tables of
-// pe::GraphView.  Host-only C++; no exceptions cross the C-ABI.
+// A program enters as `.pir` text (SPEC tensor_ir "External Interfaces";
+// reader in pe_pir.cc) or as structured arrays (pe_graph_create_from_arrays),
+// is shape-checked (the base-dialect rules REF validate.cc:161-225 enforces)
+// and compiled into the SoA tables of pe::GraphView.  Host-only C++; no
+// exceptions cross the C-ABI.
 #pragma once
 #include <stdint.h>
 
@@ -110,7 +112,12 @@ struct LoadError {
   std::string message;
 };
 
-// Parse + validate + compile.  Returns false and fills `err` on failure.
+// `.pir` text -> HostGraph (pe_pir.cc): syntax only (names resolved,
+// nothing shape-checked yet).
+bool read_pir(const char* text, size_t len, HostGraph& g, LoadError& err);
+// Shape-check + compile a HostGraph however it was built (pe_graph.cc).
+bool finish_graph(HostGraph& g, LoadError& err);
+// read_pir + finish_graph.  Returns false and fills `err` on failure.
 bool load_graph(const char* text, size_t len, HostGraph& g, LoadError& err);
 
 // SPEC:568 scope normalisation used for grouping.

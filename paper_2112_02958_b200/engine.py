@@ -70,15 +70,18 @@ def _raise(rc: int, err: PeError):
 class Graph:
     """A parsed, validated and compiled program (parse_program)."""
 
-    def __init__(self, text: str):
+    def __init__(self, text: str | None, _handle=None):
         self.lib = capi.load()
         self.text = text
-        b = text.encode()
-        h = C.c_void_p()
-        err = PeError()
-        rc = self.lib.pe_graph_create(b, len(b), C.byref(h), C.byref(err))
-        if rc != capi.PE_OK:
-            _raise(rc, err)
+        if _handle is None:
+            b = text.encode()
+            h = C.c_void_p()
+            err = PeError()
+            rc = self.lib.pe_graph_create(b, len(b), C.byref(h), C.byref(err))
+            if rc != capi.PE_OK:
+                _raise(rc, err)
+        else:
+            h = _handle
         self.h = h
         L = self.lib
         self.n_args = L.pe_graph_num_args(h)
@@ -98,12 +101,68 @@ class Graph:
         for a in range(self.n_args):
             L.pe_graph_arg_scope(h, a, buf, 1024)
             self.scopes.append(buf.value.decode())
-        import re
-        m = re.search(r"mesh\s*\{([^}]*)\}", text)
-        self.axis_names = re.findall(r'"([^"]+)"\s*=', m.group(1)) if m else []
+        self.axis_names = []
+        for a in range(self.n_axes):
+            L.pe_graph_axis_name(h, a, buf, 1024)
+            self.axis_names.append(buf.value.decode())
         self.groups = [[L.pe_graph_group_member(h, g, i) for i in range(L.pe_graph_group_size(h, g))]
                        for g in range(L.pe_graph_num_groups(h))]
         self._index = {n: i for i, n in enumerate(self.names)}
+
+    @classmethod
+    def from_arrays(cls, name, axes, args, ops, result):
+        """Structured construction (pe_graph_create_from_arrays): `axes` =
+        [(name, size)], `args` = [(id, shape, scope)], `ops` = [dict(id, kind,
+        shape, operands, batch=([],[]), contract=([],[]), dims=[], start=[],
+        limit=[], dim=-1, value=0.0, scope="")], `result` = value index."""
+        lib = capi.load()
+        keep = []
+        names = (C.c_char_p * max(1, len(axes)))(*[a[0].encode() for a in axes])
+        sizes = (C.c_int64 * max(1, len(axes)))(*[a[1] for a in axes])
+        ad = (capi.PeArgDesc * max(1, len(args)))()
+        for i, (aid, shape, scope) in enumerate(args):
+            ad[i].id = aid.encode()
+            ad[i].scope = scope.encode() if scope else None
+            ad[i].rank = len(shape)
+            for d, x in enumerate(shape):
+                ad[i].shape[d] = x
+        od = (capi.PeOpDesc * max(1, len(ops)))()
+        for i, o in enumerate(ops):
+            d = od[i]
+            d.id = o["id"].encode()
+            d.kind = o["kind"]
+            d.rank = len(o["shape"])
+            for k, x in enumerate(o["shape"]):
+                d.shape[k] = x
+            opn = (C.c_int32 * max(1, len(o["operands"])))(*o["operands"])
+            keep.append(opn)
+            d.n_operands = len(o["operands"])
+            d.operands = C.cast(opn, C.POINTER(C.c_int32))
+            lb, rb = o.get("batch", ([], []))
+            lc, rc_ = o.get("contract", ([], []))
+            d.n_batch, d.n_contract = len(lb), len(lc)
+            for k in range(len(lb)):
+                d.lhs_batch[k], d.rhs_batch[k] = lb[k], rb[k]
+            for k in range(len(lc)):
+                d.lhs_contract[k], d.rhs_contract[k] = lc[k], rc_[k]
+            dims = o.get("dims", [])
+            d.n_dims = len(dims)
+            for k, x in enumerate(dims):
+                d.dims[k] = x
+            for k, x in enumerate(o.get("start", [])):
+                d.start[k] = x
+            for k, x in enumerate(o.get("limit", [])):
+                d.limit[k] = x
+            d.dim = o.get("dim", -1)
+            d.value = o.get("value", 0.0)
+            d.scope = o["scope"].encode() if o.get("scope") else None
+        h = C.c_void_p()
+        err = PeError()
+        rc = lib.pe_graph_create_from_arrays(name.encode(), len(axes), names, sizes, len(args),
+                                             ad, len(ops), od, result, C.byref(h), C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        return cls(None, _handle=h)
 
     def __del__(self):
         h = getattr(self, "h", None)

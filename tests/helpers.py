@@ -22,7 +22,8 @@ _P = C.c_void_p
 
 def build_harness() -> str:
     src = [os.path.join(ROOT, "tests", "native", "pe_host_harness.cc"),
-           os.path.join(ROOT, "paper_2112_02958_b200", "csrc", "pe_graph.cc")]
+           os.path.join(ROOT, "paper_2112_02958_b200", "csrc", "pe_graph.cc"),
+           os.path.join(ROOT, "paper_2112_02958_b200", "csrc", "pe_pir.cc")]
     hdrs = [os.path.join(ROOT, "paper_2112_02958_b200", "csrc", h)
             for h in ("pe_core.cuh", "pe_graph.h", "pe_graph_view.h", "pe_rules.h")]
     hdrs.append(os.path.join(ROOT, "include", "pe.h"))
