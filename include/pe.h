@@ -84,7 +84,9 @@ enum {
                            before it is scored, fail_step names the action  */
   PE_CAND_INTERNAL = 2, /* InternalError / ValidationError inside propagate or
                            lowering; no score                               */
-  PE_CAND_CAPACITY = 3  /* engine arena bound exceeded (engine only)        */
+  PE_CAND_CAPACITY = 3, /* engine arena bound exceeded (engine only)        */
+  PE_CAND_PAUSED = 4    /* internal: an InferRest decision awaiting the
+                           host's batched expansion; never returned         */
 };
 
 typedef struct pe_result {
@@ -153,6 +155,16 @@ typedef struct pe_search_config {
                               (a TILE_GROUP action still tiles every member).
                               Read once at engine / oracle setup. */
   uint32_t n_worklist_args;
+  uint32_t infer_rest_action; /* 1 = InferRest is a legal action (SPEC
+                              legal_actions: "plus InferRest (if any argument
+                              untiled)"): legal when some
+                              argument is neither sliced nor atomic-wrapped;
+                              its ordinal follows every TileValue ordinal
+                              (Stop stays last); rollouts draw uniformly over
+                              TileValue + InferRest, Stop weight 1 before the
+                              first decision and 2 after.  Applying it runs
+                              infer_rest (REF propagate.cc:484-544) over the
+                              auto axes.  0 (default) = TileValue + Stop. */
 } pe_search_config;
 
 void pe_default_cost_params(pe_cost_params* out);

@@ -430,9 +430,22 @@ void resurface(const Setup& s, const std::vector<StuckNode>& stuck, Resurfaced& 
   }
 }
 
-uint32_t num_ordinals(const Setup& s) {
+// TileValue ordinals (worklist entries x dims x auto axes)
+uint32_t tile_ordinals(const Setup& s) {
   size_t entries = s.entries.size() + (s.cfg.resurface_stuck ? s.root.ops.size() : 0);
   return (uint32_t)(entries * PE_MAX_RANK * s.auto_axes.size());
+}
+// every action ordinal but Stop: TileValue, then InferRest when it is an
+// action (pe.h infer_rest_action; SPEC legal_actions order)
+uint32_t num_ordinals(const Setup& s) {
+  return tile_ordinals(s) + (s.cfg.infer_rest_action ? 1 : 0);
+}
+// SPEC legal_actions: InferRest "if any argument untiled"
+bool infer_rest_legal(const Setup& s, const Program& p) {
+  if (!s.cfg.infer_rest_action) return false;
+  for (const Argument& a : s.root.args)
+    if (!carries_tiling(p, a.id)) return true;
+  return false;
 }
 
 // TileValue(op result, d, axis) is legal when apply_tile_action would
@@ -482,6 +495,10 @@ std::vector<uint32_t> legal_ordinals(const Setup& s, const Program& p,
 pe_action ordinal_action(const Setup& s, uint32_t ord) {
   uint32_t na = (uint32_t)s.auto_axes.size();
   pe_action a{};
+  if (s.cfg.infer_rest_action && ord == tile_ordinals(s)) {
+    a.kind = PE_ACT_INFER_REST;
+    return a;
+  }
   uint32_t ai = ord % na;
   uint32_t d = (ord / na) % PE_MAX_RANK;
   uint32_t e = ord / na / PE_MAX_RANK;
@@ -510,11 +527,15 @@ void rollout_one(const Setup& s, const pe_action* prefix, uint32_t n_prefix, uin
   if (legal_out) std::fill(legal_out, legal_out + nwords, 0ull);
   try {
     bool terminal = false;
+    const pe_action ir_marker{0, 0, 0, PE_ACT_INFER_REST, 0};
     for (uint32_t k = 0; k < n_prefix; ++k) {
       if (prefix[k].kind == PE_ACT_STOP) {
         terminal = true;
         break;
       }
+      // tiles an engine inferred for an InferRest decision are re-derived
+      // here by the reference's infer_rest on the decision itself
+      if (prefix[k].pad & PE_ACT_FLAG_INFERRED) continue;
       if (!apply_action(s, p, stuck, prefix[k])) {
         r.status = PE_CAND_ILLEGAL;
         r.fail_step = (int32_t)k;
@@ -522,22 +543,28 @@ void rollout_one(const Setup& s, const pe_action* prefix, uint32_t n_prefix, uin
         break;
       }
       resurface(s, stuck, R);
-      if (nacts < maxd) acts_out[nacts] = prefix[k];
+      // decisions are recorded; InferRest as its (unexpanded) decision
+      if (nacts < maxd) acts_out[nacts] = prefix[k].kind == PE_ACT_INFER_REST ? ir_marker : prefix[k];
       ++nacts;
       r.n_steps++;
     }
     if (r.status == PE_CAND_OK) {
       std::vector<uint32_t> legal = legal_ordinals(s, p, R);
-      if (legal_out)
+      bool ir = infer_rest_legal(s, p);
+      if (legal_out) {
         for (uint32_t o : legal) legal_out[o / 64] |= 1ull << (o % 64);
+        if (ir) legal_out[tile_ordinals(s) / 64] |= 1ull << (tile_ordinals(s) % 64);
+      }
       uint64_t st = seed;
       while (!terminal) {
-        if ((uint32_t)r.n_steps >= maxd || legal.empty()) break;
+        // uniform over TileValue + InferRest, then Stop (weight 1 before the
+        // first decision, 2 after)
+        if ((uint32_t)r.n_steps >= maxd || legal.size() + (ir ? 1 : 0) == 0) break;
         uint64_t ws = r.n_steps >= 1 ? 2 : 1;
-        uint64_t total = legal.size() + ws;
+        uint64_t total = legal.size() + (ir ? 1 : 0) + ws;
         uint64_t pick = splitmix_next(st) % total;
-        if (pick >= legal.size()) break;
-        pe_action a = ordinal_action(s, legal[pick]);
+        if (pick >= legal.size() + (ir ? 1 : 0)) break;
+        pe_action a = pick == legal.size() ? ir_marker : ordinal_action(s, legal[pick]);
         if (!apply_action(s, p, stuck, a)) {
           r.status = PE_CAND_ILLEGAL;  // cannot happen: legal by construction
           r.fail_step = (int32_t)nacts;
@@ -548,6 +575,7 @@ void rollout_one(const Setup& s, const pe_action* prefix, uint32_t n_prefix, uin
         ++nacts;
         r.n_steps++;
         legal = legal_ordinals(s, p, R);
+        ir = infer_rest_legal(s, p);
       }
     }
     *n_out = std::min(nacts, maxd);
@@ -708,6 +736,7 @@ int oracle_legal(const char* pir, size_t len, const pe_search_config* cfg, const
     return 70;
   }
   std::vector<uint32_t> l = legal_ordinals(s, p, R);
+  if (infer_rest_legal(s, p)) l.push_back(tile_ordinals(s));
   *n_out = (uint32_t)l.size();
   for (uint32_t i = 0; i < l.size() && i < cap; ++i) ords_out[i] = l[i];
   return 0;

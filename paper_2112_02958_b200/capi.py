@@ -32,6 +32,7 @@ PE_CAND_OK = 0
 PE_CAND_ILLEGAL = 1
 PE_CAND_INTERNAL = 2
 PE_CAND_CAPACITY = 3
+PE_CAND_PAUSED = 4
 
 PE_MEM_DEVICE = 1
 PE_SYNC = 2
@@ -80,7 +81,8 @@ class PeSearchConfig(C.Structure):
                 ("seed", C.c_uint64), ("uct_c", C.c_double),
                 ("leaf_batch", C.c_uint32), ("scoped_only", C.c_uint32),
                 ("resurface_stuck", C.c_uint32),
-                ("worklist_args", C.POINTER(C.c_uint32)), ("n_worklist_args", C.c_uint32)]
+                ("worklist_args", C.POINTER(C.c_uint32)), ("n_worklist_args", C.c_uint32),
+                ("infer_rest_action", C.c_uint32)]
 
     def restrict_worklist(self, args) -> "PeSearchConfig":
         """Restrict the static worklist to these argument indices (ranker
@@ -138,7 +140,7 @@ def default_cost_params() -> PeCostParams:
 
 
 def default_search_config(**kw) -> PeSearchConfig:
-    c = PeSearchConfig(0xFFFFFFFF, 32, 1, 500, 0, 1.414, 256, 0, 0, None, 0)
+    c = PeSearchConfig(0xFFFFFFFF, 32, 1, 500, 0, 1.414, 256, 0, 0, None, 0, 0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c

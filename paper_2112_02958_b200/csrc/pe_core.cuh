@@ -1754,6 +1754,29 @@ struct Cand {
     }
     return n;
   }
+  // InferRest is legal when some argument neither carries a slice nor is
+  // atomic-wrapped (SPEC legal_actions "if any argument untiled"; the carry
+  // bits are exactly REF rewrite.cc:42-51 carries_tiling for arguments)
+  PE_HD bool infer_rest_legal() const {
+    for (int32_t w = 0; w <= (g.A >> 5); ++w) {
+      int32_t bits = g.A - (w << 5);
+      uint32_t all = bits >= 32 ? 0xFFFFFFFFu : ((1u << bits) - 1u);
+      if ((a.carry()[w] & all) != all) return true;
+    }
+    return false;
+  }
+  // stop here for the host's batched InferRest expansion (pe_engine.cu
+  // ir_resolve): record the (unexpanded) decision, report the position
+  // (prefix index, or -1 for a drawn decision) and the draws consumed
+  PE_HD void pause(pe_result& r, pe_action* acts_out, int32_t& nacts, int32_t maxd,
+                   int32_t steps, int32_t at, int32_t draws) {
+    if (nacts < maxd) acts_out[nacts] = pe_action{0, 0, 0, PE_ACT_INFER_REST, 0};
+    ++nacts;
+    r.status = PE_CAND_PAUSED;
+    r.fail_step = at;
+    r.reserved = draws;
+    r.n_steps = steps;
+  }
   PE_HD pe_action ordinal_action(int32_t ord) const {
     pe_action x;
     int32_t na = g.n_auto;
@@ -1830,13 +1853,20 @@ struct Cand {
       }
       if (prefix[k].kind == PE_ACT_INFER_REST) {  // expanded by the host
         if (!(prefix[k].pad & PE_ACT_FLAG_EXPANDED)) {
+          if (g.ir_pause) {
+            pause(r, acts_out, nacts, maxd, steps, k, 0);
+            *n_out = (uint32_t)(nacts < maxd ? nacts : maxd);
+            return;
+          }
           status = PE_CAND_ILLEGAL;
           r.fail_step = k;
           terminal = true;
           break;
         }
+        // recorded as the decision (unexpanded); its inferred tiles follow
+        // in the prefix and are not recorded
         propagated = true;
-        if (nacts < maxd) acts_out[nacts] = prefix[k];
+        if (nacts < maxd) acts_out[nacts] = pe_action{0, 0, 0, PE_ACT_INFER_REST, 0};
         ++nacts;
         ++steps;
         continue;
@@ -1853,26 +1883,39 @@ struct Cand {
       propagated = true;
       if (bad()) break;
       rs_due = RS;
-      if (nacts < maxd) acts_out[nacts] = prefix[k];
-      ++nacts;
-      if (!(prefix[k].pad & PE_ACT_FLAG_INFERRED)) ++steps;
+      if (!(prefix[k].pad & PE_ACT_FLAG_INFERRED)) {  // decisions only
+        if (nacts < maxd) acts_out[nacts] = prefix[k];
+        ++nacts;
+        ++steps;
+      }
     }
     if (RS && rs_due && !bad() && status == PE_CAND_OK) resurface_update();
     if (!bad() && status == PE_CAND_OK) {
       if (legal_out) {
         int32_t nl = build_legal<RS>();
         for (int32_t i = 0; i < nl; ++i) legal_out[a.lg()[i] >> 6] |= 1ull << (a.lg()[i] & 63);
+        if (g.ir_ord >= 0 && infer_rest_legal())
+          legal_out[g.ir_ord >> 6] |= 1ull << (g.ir_ord & 63);
       }
       // (each decision draws once: splitmix adds the golden gamma per draw)
       uint64_t st = seed + (uint64_t)snap_d * 0x9E3779B97F4A7C15ull;
+      int32_t draws = snap_d;
       while (!terminal) {
         if (steps >= maxd) break;
         tick(4);
         int32_t nl = build_legal<RS>();
-        if (nl == 0) break;
+        // InferRest follows the TileValue actions (SPEC legal_actions order)
+        int32_t ir = g.ir_ord >= 0 && infer_rest_legal() ? 1 : 0;
+        if (nl + ir == 0) break;
         uint64_t ws = steps >= 1 ? 2 : 1;
-        uint64_t pick = splitmix(st) % ((uint64_t)nl + ws);
-        if (pick >= (uint64_t)nl) break;
+        uint64_t pick = splitmix(st) % ((uint64_t)(nl + ir) + ws);
+        ++draws;
+        if (pick >= (uint64_t)(nl + ir)) break;
+        if (pick == (uint64_t)nl) {
+          pause(r, acts_out, nacts, maxd, steps, -1, draws);
+          *n_out = (uint32_t)(nacts < maxd ? nacts : maxd);
+          return;
+        }
         pe_action x = ordinal_action(a.lg()[pick]);
         tick(5);
         bool ok = apply_action(x);

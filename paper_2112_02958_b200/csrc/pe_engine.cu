@@ -19,6 +19,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "pe.h"
@@ -454,6 +455,9 @@ bool ensure_io(pe_engine* e, size_t bytes, pe_error* err) {
 
 uint32_t launch_slots(const pe_engine* e, uint32_t n) { return std::min<uint32_t>(e->slots, n); }
 
+bool ir_expand_batch(pe_engine* e, std::vector<std::vector<pe_action>*>& seqs, cudaStream_t st,
+                     pe_error* err);
+
 // order this call after the engine's previous call (any stream)
 bool call_begin(pe_engine* e, cudaStream_t st, pe_error* err) {
   return cuda_ok(cudaStreamWaitEvent(st, e->done, 0), err, "stream wait");
@@ -687,8 +691,9 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
                              e->cfg.scoped_only != 0, e->cfg.resurface_stuck != 0,
                              pe::worklist_filter(g, e->cfg));
   e->cfg.worklist_args = nullptr;  // read once; the caller's array may go away
+  e->wl.infer_rest = e->cfg.infer_rest_action != 0;
   const pe::Worklist& w = e->wl;
-  e->n_ordinals = (uint32_t)w.n_ordinals();
+  e->n_ordinals = (uint32_t)w.n_action_ordinals();
 
   // device image of the graph tables
   std::vector<uint8_t> img;
@@ -927,6 +932,10 @@ int64_t pe_engine_graph_bytes(const pe_engine* e) { return e->graph_bytes; }
 pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* out) {
   if (!out || ord >= e->n_ordinals) return PE_ERR_INVALID_ARGUMENT;
   const pe::Worklist& w = e->wl;
+  if (w.infer_rest && (int32_t)ord == w.n_ordinals()) {  // InferRest follows the TileValues
+    *out = pe_action{0, 0, 0, PE_ACT_INFER_REST, 0};
+    return PE_OK;
+  }
   uint32_t na = (uint32_t)w.auto_axes.size();
   uint32_t ai = ord % na, d = (ord / na) % pe::kMaxRank, ent = ord / na / pe::kMaxRank;
   out->axis = (uint8_t)w.auto_axes[ai];
@@ -942,81 +951,6 @@ pe_status pe_engine_ordinal_action(const pe_engine* e, uint32_t ord, pe_action* 
   return PE_OK;
 }
 
-// Host-orchestrated infer_rest (REF propagate.cc:484-544): every round
-// evaluates, in ONE batch on the GPU, the sequence so far extended by each
-// (untiled, non-atomic argument) x dim x auto axis trial, and accepts the
-// first argument (argument order) with exactly one trial that adds no
-// all_gather bytes; rounds repeat until no argument is uniquely determined.
-// The result is `prefix + [INFER_REST(expanded)] + inferred TILE actions`,
-// whose evaluation equals the reference's infer_rest on the same state.
-static pe_status infer_rest_expand(pe_engine* e, std::vector<pe_action>& cur, pe_error* err) {
-  const pe::HostGraph& g = e->graph->g;
-  const int32_t A = (int32_t)g.args.size();
-  pe_action marker{0, 0, 0, PE_ACT_INFER_REST, PE_ACT_FLAG_EXPANDED};
-  cur.push_back(marker);
-  std::vector<pe_result> res(1);
-  std::vector<uint8_t> flags(A);
-  auto eval = [&](const std::vector<pe_action>& acts, const std::vector<uint32_t>& off,
-                  uint32_t n, pe_result* out, uint8_t* fl) {
-    return pe_eval_batch_ex(e, acts.data(), off.data(), n, out, nullptr, 0, fl, 0, nullptr, err);
-  };
-  std::vector<uint32_t> off1{0, (uint32_t)cur.size()};
-  pe_status st = eval(cur, off1, 1, res.data(), flags.data());
-  if (st != PE_OK) return st;
-  if (res[0].status != PE_CAND_OK) return PE_OK;  // the candidate reports its own status
-  bool any_tiled = false;
-  for (int32_t a = 0; a < A; ++a) any_tiled |= (flags[a] & 1) != 0;
-  if (!any_tiled) return PE_OK;
-  for (;;) {
-    int64_t baseline = 0;
-    for (int x = 0; x < PE_MAX_AXES; ++x) baseline += res[0].ag_bytes[x];
-    std::vector<pe_action> trial_acts;
-    std::vector<uint32_t> toff{0};
-    std::vector<std::pair<int32_t, pe_action>> trials;  // (arg, action)
-    for (int32_t a = 0; a < A; ++a) {
-      if (flags[a] & 3) continue;  // arg_is_tiled / arg_is_atomic
-      const auto& s = g.args[a].shape;
-      for (int32_t d = 0; d < (int32_t)s.size(); ++d)
-        for (int32_t ax : e->wl.auto_axes) {
-          if (s[d] % g.axis_sizes[ax] != 0) continue;
-          pe_action t{(uint32_t)a, (uint8_t)d, (uint8_t)ax, PE_ACT_TILE, PE_ACT_FLAG_INFERRED};
-          trials.push_back({a, t});
-          trial_acts.insert(trial_acts.end(), cur.begin(), cur.end());
-          trial_acts.push_back(t);
-          toff.push_back((uint32_t)trial_acts.size());
-        }
-    }
-    if (trials.empty()) return PE_OK;
-    std::vector<pe_result> tr(trials.size());
-    st = eval(trial_acts, toff, (uint32_t)trials.size(), tr.data(), nullptr);
-    if (st != PE_OK) return st;
-    int32_t chosen = -1;
-    for (size_t i = 0; i < trials.size();) {
-      int32_t a = trials[i].first;
-      size_t j = i, hit = 0, n_consistent = 0;
-      for (; j < trials.size() && trials[j].first == a; ++j) {
-        int64_t ag = 0;
-        for (int x = 0; x < PE_MAX_AXES; ++x) ag += tr[j].ag_bytes[x];
-        if (tr[j].status == PE_CAND_OK && ag <= baseline) {
-          if (n_consistent == 0) hit = j;
-          ++n_consistent;
-        }
-      }
-      if (n_consistent == 1) {
-        chosen = (int32_t)hit;
-        break;
-      }
-      i = j;
-    }
-    if (chosen < 0) return PE_OK;
-    cur.push_back(trials[chosen].second);
-    off1[1] = (uint32_t)cur.size();
-    st = eval(cur, off1, 1, res.data(), flags.data());
-    if (st != PE_OK) return st;
-    if (res[0].status != PE_CAND_OK) return PE_OK;
-  }
-}
-
 pe_status pe_infer_rest(pe_engine* e, const pe_action* prefix, uint32_t n_prefix, pe_action* out,
                         uint32_t cap, uint32_t* n_out, pe_error* err) {
   if (!e || (!prefix && n_prefix) || !out || !n_out) {
@@ -1024,8 +958,10 @@ pe_status pe_infer_rest(pe_engine* e, const pe_action* prefix, uint32_t n_prefix
     return PE_ERR_INVALID_ARGUMENT;
   }
   std::vector<pe_action> cur(prefix, prefix + n_prefix);
-  pe_status st = infer_rest_expand(e, cur, err);
-  if (st != PE_OK) return st;
+  std::vector<std::vector<pe_action>*> one{&cur};
+  if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice") ||
+      !ir_expand_batch(e, one, nullptr, err))
+    return PE_ERR_CUDA;
   *n_out = (uint32_t)cur.size();
   if (cur.size() > cap) {
     set_err(err, PE_ERR_CAPACITY, "output buffer too small");
@@ -1043,28 +979,53 @@ pe_status pe_eval_batch(pe_engine* e, const pe_action* acts, const uint32_t* seq
     return PE_ERR_INVALID_ARGUMENT;
   }
   if (!(flags & PE_MEM_DEVICE) && n > 0) {
-    // expand unexpanded INFER_REST decisions on the host (nested GPU batches)
+    // Unexpanded INFER_REST decisions: expanded left to right, every
+    // candidate's next one in the same batched expansion (ir_expand_batch).
     bool any = false;
     for (uint32_t k = 0; k < seq_off[n] && !any; ++k)
       any = acts[k].kind == PE_ACT_INFER_REST && !(acts[k].pad & PE_ACT_FLAG_EXPANDED);
     if (any) {
+      if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+      std::vector<std::vector<pe_action>> cur(n);
+      std::vector<std::vector<int32_t>> orig(n);  // expanded index -> caller's index
+      std::vector<uint32_t> pos(n);
+      for (uint32_t c = 0; c < n; ++c) pos[c] = seq_off[c];
+      for (;;) {
+        std::vector<std::vector<pe_action>*> jobs;
+        std::vector<uint32_t> who;
+        for (uint32_t c = 0; c < n; ++c) {
+          while (pos[c] < seq_off[c + 1]) {
+            const pe_action& a = acts[pos[c]++];
+            if (a.kind == PE_ACT_INFER_REST && !(a.pad & PE_ACT_FLAG_EXPANDED)) {
+              jobs.push_back(&cur[c]);
+              who.push_back(c);
+              break;
+            }
+            cur[c].push_back(a);
+            orig[c].push_back((int32_t)(pos[c] - 1 - seq_off[c]));
+          }
+        }
+        if (jobs.empty()) break;
+        std::vector<size_t> before(jobs.size());
+        for (size_t j = 0; j < jobs.size(); ++j) before[j] = jobs[j]->size();
+        if (!ir_expand_batch(e, jobs, (cudaStream_t)stream, err)) return PE_ERR_CUDA;
+        for (size_t j = 0; j < jobs.size(); ++j)
+          orig[who[j]].resize(jobs[j]->size(), (int32_t)(pos[who[j]] - 1 - seq_off[who[j]]));
+      }
       std::vector<pe_action> flat;
       std::vector<uint32_t> off{0};
       for (uint32_t c = 0; c < n; ++c) {
-        std::vector<pe_action> cur;
-        for (uint32_t k = seq_off[c]; k < seq_off[c + 1]; ++k) {
-          if (acts[k].kind == PE_ACT_INFER_REST && !(acts[k].pad & PE_ACT_FLAG_EXPANDED)) {
-            pe_status st = infer_rest_expand(e, cur, err);
-            if (st != PE_OK) return st;
-          } else {
-            cur.push_back(acts[k]);
-          }
-        }
-        flat.insert(flat.end(), cur.begin(), cur.end());
+        flat.insert(flat.end(), cur[c].begin(), cur[c].end());
         off.push_back((uint32_t)flat.size());
       }
-      return pe_eval_batch_ex(e, flat.data(), off.data(), n, out, trace, trace_words, nullptr,
-                              flags, stream, err);
+      pe_status st = pe_eval_batch_ex(e, flat.data(), off.data(), n, out, trace, trace_words,
+                                      nullptr, flags, stream, err);
+      // an illegal action is named by its index in the caller's sequence
+      for (uint32_t c = 0; st == PE_OK && c < n; ++c)
+        if (out[c].status == PE_CAND_ILLEGAL && out[c].fail_step >= 0 &&
+            out[c].fail_step < (int32_t)orig[c].size())
+          out[c].fail_step = orig[c][out[c].fail_step];
+      return st;
     }
   }
   return pe_eval_batch_ex(e, acts, seq_off, n, out, trace, trace_words, nullptr, flags, stream,
@@ -1416,6 +1377,430 @@ bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
   return true;
 }
 
+// Main + retry rollout launches over one batch (the caller has set up the
+// schedule).  `gv` is the engine's graph view, possibly with ir_pause set.
+cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_action* d_prefix,
+                             const uint32_t* d_poff, const uint64_t* d_seeds, uint32_t n,
+                             pe_action* d_acts, uint32_t* d_nacts, pe_result* d_out,
+                             uint64_t* d_legal, const uint32_t* perm, const SchedView& sv,
+                             uint32_t* max_acts, cudaStream_t st) {
+  int32_t maxd = (int32_t)e->cfg.max_decisions;
+  int32_t lw = (int32_t)pe_engine_legal_words(e);
+  uint32_t slots = launch_slots(e, n);
+  cudaError_t ce = cudaMemsetAsync(e->d_ctr + 1, 0, sizeof(uint32_t), st);
+  if (ce != cudaSuccess) return ce;
+  uint32_t bs = std::min<uint32_t>(e->big_slots, n);
+  uint32_t threads = slots * kThreadsPerSlot;
+  uint32_t blk = threads % PE_SM_THREADS == 0 && threads >= (uint32_t)e->sm_count * PE_SM_THREADS
+                     ? PE_SM_THREADS : kBlock;
+  uint32_t grid = (threads + blk - 1) / blk;
+  uint32_t bgrid = (bs * kThreadsPerSlot + kBlock - 1) / kBlock;
+  // (the stuck-resurfacing instantiation only when the worklist uses it)
+  auto launch = [&](auto main_k, auto retry_k) {
+    // (experiment PE_L2_PERSIST: the graph image as a persisting L2 window)
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = e->d_graph;
+    at[0].val.accessPolicyWindow.num_bytes = e->l2_window;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(blk);
+    lc.stream = st;
+    lc.attrs = at;
+    lc.numAttrs = e->l2_persist ? 1 : 0;
+    cudaError_t le = cudaLaunchKernelEx(&lc, main_k, gv, e->layout, e->d_arena, slots, d_prefix,
+                                        d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
+                                        d_nacts, d_out, d_legal, lw, e->d_ctr + 1, perm, sv,
+                                        max_acts);
+    // the retry launch reads the statuses the main launch writes: never
+    // queue it behind a main launch that failed to start
+    if (le != cudaSuccess) return le;
+    retry_k<<<bgrid, kBlock, 0, st>>>(gv, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff,
+                                      d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts,
+                                      d_out, d_legal, lw, nullptr, nullptr, SchedView(),
+                                      max_acts);
+    return cudaGetLastError();
+  };
+  cudaError_t lerr = e->wl.resurface
+                         ? launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>)
+                         : launch(pe_rollout_kernel<false, false>, pe_rollout_kernel<true, false>);
+  e->launches += 2;
+  return lerr;
+}
+
+// ---- InferRest as a batched composite action (pe.h infer_rest_action) ----
+// REF infer_rest (propagate.cc:484-544) from a state given as an action
+// sequence: for every untiled (not sliced), non-atomic argument in order,
+// each (dim x auto axis) that divides is a trial = the sequence + that tile,
+// propagated and lowered; a trial is consistent when it evaluates and adds
+// no all_gather bytes over the current state.  The first argument with
+// exactly one consistent trial takes it, and the rounds repeat until none
+// does.  Here ALL trials of ALL sequences being expanded run as one batched
+// evaluation per round (chunked by size), so a batch of paused rollouts
+// costs one launch per inference round, not one per candidate.
+
+// Host sequences evaluated on the device through the engine's own eval
+// kernels (private buffers: the caller's staging buffer may be in use).
+bool eval_seqs(pe_engine* e, const std::vector<pe_action>& acts, const std::vector<uint32_t>& off,
+               std::vector<pe_result>& res, std::vector<uint8_t>* argflags, cudaStream_t st,
+               pe_error* err) {
+  uint32_t n = (uint32_t)off.size() - 1;
+  res.resize(n);
+  if (n == 0) return true;
+  const size_t A = e->graph->g.args.size();
+  size_t b_acts = std::max<size_t>(1, acts.size()) * sizeof(pe_action);
+  size_t b_fl = argflags ? (size_t)n * A : 0;
+  void *d_acts = nullptr, *d_off = nullptr, *d_out = nullptr, *d_fl = nullptr;
+  bool ok = cuda_ok(cudaMalloc(&d_acts, b_acts), err, "cudaMalloc(ir)") &&
+            cuda_ok(cudaMalloc(&d_off, off.size() * 4), err, "cudaMalloc(ir)") &&
+            cuda_ok(cudaMalloc(&d_out, (size_t)n * sizeof(pe_result)), err, "cudaMalloc(ir)") &&
+            (!argflags || cuda_ok(cudaMalloc(&d_fl, std::max<size_t>(1, b_fl)), err, "cudaMalloc(ir)"));
+  ok = ok && (acts.empty() || cuda_ok(cudaMemcpyAsync(d_acts, acts.data(), acts.size() * sizeof(pe_action),
+                                                      cudaMemcpyHostToDevice, st), err, "H2D ir")) &&
+       cuda_ok(cudaMemcpyAsync(d_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice, st), err,
+               "H2D ir");
+  ok = ok && pe_eval_batch_ex(e, (const pe_action*)d_acts, (const uint32_t*)d_off, n,
+                              (pe_result*)d_out, nullptr, 0, (uint8_t*)d_fl, PE_MEM_DEVICE, st,
+                              err) == PE_OK;
+  ok = ok && cuda_ok(cudaMemcpyAsync(res.data(), d_out, (size_t)n * sizeof(pe_result),
+                                     cudaMemcpyDeviceToHost, st), err, "D2H ir");
+  if (ok && argflags) {
+    argflags->resize(b_fl);
+    ok = cuda_ok(cudaMemcpyAsync(argflags->data(), d_fl, b_fl, cudaMemcpyDeviceToHost, st), err,
+                 "D2H ir");
+  }
+  ok = ok && cuda_ok(cudaStreamSynchronize(st), err, "ir sync");
+  for (void* q : {d_acts, d_off, d_out, d_fl})
+    if (q) cudaFree(q);
+  return ok;
+}
+
+int64_t ag_total(const pe_result& r) {
+  int64_t s = 0;
+  for (int x = 0; x < PE_MAX_AXES; ++x) s += r.ag_bytes[x];
+  return s;
+}
+
+// Appends [INFER_REST marker (expanded)] + the inferred tiles to every
+// sequence of `seqs` (each = the state InferRest is applied to).
+bool ir_expand_batch(pe_engine* e, std::vector<std::vector<pe_action>*>& seqs, cudaStream_t st,
+                     pe_error* err) {
+  const pe::HostGraph& g = e->graph->g;
+  const int32_t A = (int32_t)g.args.size();
+  const pe_action marker{0, 0, 0, PE_ACT_INFER_REST, PE_ACT_FLAG_EXPANDED};
+  struct Job {
+    std::vector<pe_action>* seq;
+    int64_t base_ag;
+    std::vector<uint8_t> flags;  // bit 0 sliced, bit 1 atomic (arg_is_tiled / arg_is_atomic)
+  };
+  std::vector<Job> live;
+  {
+    std::vector<pe_action> flat;
+    std::vector<uint32_t> off{0};
+    for (auto* s : seqs) {
+      s->push_back(marker);
+      flat.insert(flat.end(), s->begin(), s->end());
+      off.push_back((uint32_t)flat.size());
+    }
+    std::vector<pe_result> res;
+    std::vector<uint8_t> fl;
+    if (!eval_seqs(e, flat, off, res, &fl, st, err)) return false;
+    for (size_t j = 0; j < seqs.size(); ++j) {
+      if (res[j].status != PE_CAND_OK) continue;  // the candidate reports its own status
+      Job jb{seqs[j], ag_total(res[j]), std::vector<uint8_t>(fl.begin() + j * A, fl.begin() + (j + 1) * A)};
+      bool any_tiled = false;
+      for (int32_t a = 0; a < A; ++a) any_tiled |= (jb.flags[a] & 1) != 0;
+      if (any_tiled) live.push_back(std::move(jb));  // nothing tiled: a no-op
+    }
+  }
+  const size_t kMaxTrialActs = (size_t)1 << 23;  // actions per trial launch
+  while (!live.empty()) {
+    // every trial of every live job, in (job, argument, dim, axis) order
+    struct Trial {
+      uint32_t job;
+      int32_t arg;
+      pe_action tile;
+    };
+    std::vector<Trial> trials;
+    for (uint32_t j = 0; j < live.size(); ++j)
+      for (int32_t a = 0; a < A; ++a) {
+        if (live[j].flags[a] & 3) continue;
+        const auto& sh = g.args[a].shape;
+        for (int32_t d = 0; d < (int32_t)sh.size(); ++d)
+          for (int32_t ax : e->wl.auto_axes)
+            if (sh[d] % g.axis_sizes[ax] == 0)
+              trials.push_back({j, a, pe_action{(uint32_t)a, (uint8_t)d, (uint8_t)ax, PE_ACT_TILE,
+                                                PE_ACT_FLAG_INFERRED}});
+      }
+    std::vector<pe_result> tres(trials.size());
+    for (size_t t0 = 0; t0 < trials.size();) {
+      std::vector<pe_action> flat;
+      std::vector<uint32_t> off{0};
+      size_t t1 = t0;
+      while (t1 < trials.size() && (t1 == t0 || flat.size() < kMaxTrialActs)) {
+        const auto& s = *live[trials[t1].job].seq;
+        flat.insert(flat.end(), s.begin(), s.end());
+        flat.push_back(trials[t1].tile);
+        off.push_back((uint32_t)flat.size());
+        ++t1;
+      }
+      std::vector<pe_result> r;
+      if (!eval_seqs(e, flat, off, r, nullptr, st, err)) return false;
+      std::copy(r.begin(), r.end(), tres.begin() + t0);
+      t0 = t1;
+    }
+    // per job: the first argument with exactly one consistent trial
+    std::vector<int32_t> pick(live.size(), -1);
+    for (size_t t = 0; t < trials.size();) {
+      size_t u = t;
+      int32_t hits = 0, hit = -1;
+      for (; u < trials.size() && trials[u].job == trials[t].job && trials[u].arg == trials[t].arg; ++u)
+        if (tres[u].status == PE_CAND_OK && ag_total(tres[u]) <= live[trials[t].job].base_ag) {
+          if (hits++ == 0) hit = (int32_t)u;
+        }
+      if (hits == 1 && pick[trials[t].job] < 0) pick[trials[t].job] = hit;
+      t = u;
+    }
+    std::vector<Job> next;
+    std::vector<pe_action> flat;
+    std::vector<uint32_t> off{0};
+    for (uint32_t j = 0; j < live.size(); ++j) {
+      if (pick[j] < 0) continue;  // no argument determined: this expansion is complete
+      live[j].seq->push_back(trials[pick[j]].tile);
+      flat.insert(flat.end(), live[j].seq->begin(), live[j].seq->end());
+      off.push_back((uint32_t)flat.size());
+      next.push_back(std::move(live[j]));
+    }
+    if (next.empty()) break;
+    std::vector<pe_result> res;
+    std::vector<uint8_t> fl;
+    if (!eval_seqs(e, flat, off, res, &fl, st, err)) return false;
+    live.clear();
+    for (size_t j = 0; j < next.size(); ++j) {
+      if (res[j].status != PE_CAND_OK) continue;
+      next[j].base_ag = ag_total(res[j]);
+      next[j].flags.assign(fl.begin() + j * A, fl.begin() + (j + 1) * A);
+      live.push_back(std::move(next[j]));
+    }
+  }
+  return true;
+}
+
+__global__ void pe_paused_kernel(const pe_result* out, uint32_t n, uint32_t* list, uint32_t* count) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && out[i].status == PE_CAND_PAUSED) list[atomicAdd(count, 1u)] = i;
+}
+
+// per paused candidate: pause position, draws consumed, recorded actions
+__global__ void pe_ir_gather_kernel(const uint32_t* list, uint32_t m, const pe_result* out,
+                                    const pe_action* acts, const uint32_t* nacts, int32_t maxd,
+                                    int32_t* info, pe_action* acts_g) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  uint32_t i = list[j];
+  info[3 * j] = out[i].fail_step;
+  info[3 * j + 1] = out[i].reserved;
+  info[3 * j + 2] = (int32_t)nacts[i];
+  for (int32_t k = 0; k < maxd; ++k) acts_g[(uint64_t)j * maxd + k] = acts[(uint64_t)i * maxd + k];
+}
+
+// resumed results back into the caller's slots; legal rows only for
+// candidates whose legal set is taken after the caller's prefix in this run
+__global__ void pe_ir_scatter_kernel(const uint32_t* list, uint32_t m, const pe_result* out2,
+                                     const pe_action* acts2, const uint32_t* nacts2,
+                                     const uint64_t* legal2, const uint8_t* take_legal,
+                                     int32_t maxd, int32_t lw, pe_result* out, pe_action* acts,
+                                     uint32_t* nacts, uint64_t* legal) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  uint32_t i = list[j];
+  out[i] = out2[j];
+  nacts[i] = nacts2[j];
+  for (int32_t k = 0; k < maxd; ++k) acts[(uint64_t)i * maxd + k] = acts2[(uint64_t)j * maxd + k];
+  if (legal && take_legal[j])
+    for (int32_t w = 0; w < lw; ++w) legal[(uint64_t)i * lw + w] = legal2[(uint64_t)j * lw + w];
+}
+
+struct RolloutIo {
+  pe::GraphView gv;
+  const pe_action* d_prefix;
+  const uint32_t* d_poff;
+  const uint64_t* d_seeds;
+  uint32_t n;
+  pe_action* d_acts;
+  uint32_t* d_nacts;
+  pe_result* d_out;
+  uint64_t* d_legal;
+  uint32_t* max_acts;
+  const pe_action* h_prefix;  // host copies (host mode), else NULL
+  const uint32_t* h_poff;
+  const uint64_t* h_seeds;
+};
+
+// Resolves every paused candidate of a rollout batch: expand its InferRest
+// decision (batched with all other paused candidates), then resume it from
+// the expanded sequence with its RNG stream advanced past the draws it
+// consumed (splitmix64 state = seed + draws * gamma); a resumed rollout may
+// pause again.  The caller's outputs end up exactly as an uninterrupted
+// rollout would have written them.
+pe_status ir_resolve(pe_engine* e, const RolloutIo& io, cudaStream_t st, pe_error* err) {
+  const int32_t maxd = (int32_t)e->cfg.max_decisions;
+  const int32_t lw = (int32_t)pe_engine_legal_words(e);
+  const uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+  // host view of the caller's prefixes and seeds (device mode: fetched once)
+  std::vector<pe_action> hp;
+  std::vector<uint32_t> hpoff;
+  std::vector<uint64_t> hseeds;
+  bool have_host = io.h_poff != nullptr;
+  struct Cur {
+    std::vector<pe_action> prefix;
+    uint64_t seed;
+  };
+  std::unordered_map<uint32_t, Cur> cur;  // candidates resumed at least once
+  std::vector<void*> bufs;
+  auto fail = [&](pe_status s) {
+    cudaStreamSynchronize(st);
+    for (void* q : bufs) cudaFree(q);
+    return s;
+  };
+  auto dalloc = [&](size_t bytes) -> void* {
+    void* q = nullptr;
+    if (!cuda_ok(cudaMalloc(&q, std::max<size_t>(bytes, 16)), err, "cudaMalloc(ir)")) return nullptr;
+    bufs.push_back(q);
+    return q;
+  };
+  uint32_t* d_list = (uint32_t*)dalloc((size_t)io.n * 4 + 4);
+  uint32_t* d_cnt = (uint32_t*)dalloc(4);
+  if (!d_list || !d_cnt) return fail(PE_ERR_CUDA);
+  for (int round = 0;; ++round) {
+    uint32_t m = 0;
+    if (!cuda_ok(cudaMemsetAsync(d_cnt, 0, 4, st), err, "ir count")) return fail(PE_ERR_CUDA);
+    pe_paused_kernel<<<(io.n + 255) / 256, 256, 0, st>>>(io.d_out, io.n, d_list, d_cnt);
+    e->launches += 1;
+    if (!cuda_ok(cudaGetLastError(), err, "ir launch") ||
+        !cuda_ok(cudaMemcpyAsync(&m, d_cnt, 4, cudaMemcpyDeviceToHost, st), err, "D2H ir") ||
+        !cuda_ok(cudaStreamSynchronize(st), err, "ir sync"))
+      return fail(PE_ERR_CUDA);
+    if (m == 0) break;
+    std::vector<uint32_t> list(m);
+    if (!cuda_ok(cudaMemcpy(list.data(), d_list, (size_t)m * 4, cudaMemcpyDeviceToHost), err, "D2H ir"))
+      return fail(PE_ERR_CUDA);
+    std::sort(list.begin(), list.end());
+    if (!cuda_ok(cudaMemcpy(d_list, list.data(), (size_t)m * 4, cudaMemcpyHostToDevice), err, "H2D ir"))
+      return fail(PE_ERR_CUDA);
+    if (!have_host) {
+      hpoff.assign(io.n + 1, 0);
+      hseeds.assign(io.n, 0);
+      bool ok = io.d_poff == nullptr ||
+                cuda_ok(cudaMemcpy(hpoff.data(), io.d_poff, (size_t)(io.n + 1) * 4, cudaMemcpyDeviceToHost),
+                        err, "D2H ir");
+      ok = ok && cuda_ok(cudaMemcpy(hseeds.data(), io.d_seeds, (size_t)io.n * 8, cudaMemcpyDeviceToHost),
+                         err, "D2H ir");
+      if (ok && io.d_prefix && hpoff[io.n]) {
+        hp.resize(hpoff[io.n]);
+        ok = cuda_ok(cudaMemcpy(hp.data(), io.d_prefix, hp.size() * sizeof(pe_action),
+                                cudaMemcpyDeviceToHost), err, "D2H ir");
+      }
+      if (!io.d_prefix) std::fill(hpoff.begin(), hpoff.end(), 0u);
+      if (!ok) return fail(PE_ERR_CUDA);
+      have_host = true;
+    }
+    const pe_action* P = io.h_prefix ? io.h_prefix : hp.data();
+    const uint32_t* PO = io.h_poff ? io.h_poff : hpoff.data();
+    const uint64_t* SD = io.h_seeds ? io.h_seeds : hseeds.data();
+    // pause position, draws and recorded actions of the paused candidates
+    int32_t* d_info = (int32_t*)dalloc((size_t)m * 12);
+    pe_action* d_ag = (pe_action*)dalloc((size_t)m * maxd * sizeof(pe_action));
+    if (!d_info || !d_ag) return fail(PE_ERR_CUDA);
+    pe_ir_gather_kernel<<<(m + 255) / 256, 256, 0, st>>>(d_list, m, io.d_out, io.d_acts, io.d_nacts,
+                                                          maxd, d_info, d_ag);
+    e->launches += 1;
+    std::vector<int32_t> info((size_t)m * 3);
+    std::vector<pe_action> ag((size_t)m * maxd);
+    if (!cuda_ok(cudaGetLastError(), err, "ir launch") ||
+        !cuda_ok(cudaMemcpyAsync(info.data(), d_info, info.size() * 4, cudaMemcpyDeviceToHost, st), err, "D2H ir") ||
+        !cuda_ok(cudaMemcpyAsync(ag.data(), d_ag, ag.size() * sizeof(pe_action), cudaMemcpyDeviceToHost, st), err, "D2H ir") ||
+        !cuda_ok(cudaStreamSynchronize(st), err, "ir sync"))
+      return fail(PE_ERR_CUDA);
+    // the state each InferRest applies to, and what follows it
+    std::vector<std::vector<pe_action>> state(m), rest(m);
+    std::vector<uint64_t> seed2(m);
+    std::vector<uint8_t> take_legal(m, 0);
+    for (uint32_t j = 0; j < m; ++j) {
+      uint32_t i = list[j];
+      auto it = cur.find(i);
+      const pe_action* pb = it != cur.end() ? it->second.prefix.data() : P + PO[i];
+      uint32_t pn = it != cur.end() ? (uint32_t)it->second.prefix.size() : PO[i + 1] - PO[i];
+      uint64_t sd = it != cur.end() ? it->second.seed : SD[i];
+      int32_t at = info[3 * j], draws = info[3 * j + 1], nrec = info[3 * j + 2];
+      if (at >= 0) {  // an unexpanded marker in the prefix
+        state[j].assign(pb, pb + at);
+        rest[j].assign(pb + at + 1, pb + pn);
+        // the legal set is taken after the caller's whole prefix, which
+        // the resumed run reaches for the first time
+        take_legal[j] = 1;
+      } else {  // a drawn decision: the prefix, then the drawn tiles
+        state[j].assign(pb, pb + pn);
+        uint32_t rec = 0;
+        for (uint32_t k = 0; k < pn; ++k) rec += (pb[k].pad & PE_ACT_FLAG_INFERRED) ? 0 : 1;
+        if (nrec > maxd) return fail(PE_ERR_INTERNAL);
+        for (int32_t k = (int32_t)rec; k < nrec - 1; ++k) state[j].push_back(ag[(size_t)j * maxd + k]);
+      }
+      seed2[j] = sd + (uint64_t)draws * kGamma;
+    }
+    std::vector<std::vector<pe_action>*> ptrs(m);
+    for (uint32_t j = 0; j < m; ++j) ptrs[j] = &state[j];
+    if (!ir_expand_batch(e, ptrs, st, err)) return fail(PE_ERR_CUDA);
+    // resume: expanded state + the rest of the prefix, advanced seed
+    std::vector<pe_action> flat;
+    std::vector<uint32_t> off{0};
+    for (uint32_t j = 0; j < m; ++j) {
+      Cur c;
+      c.prefix = std::move(state[j]);
+      c.prefix.insert(c.prefix.end(), rest[j].begin(), rest[j].end());
+      c.seed = seed2[j];
+      flat.insert(flat.end(), c.prefix.begin(), c.prefix.end());
+      off.push_back((uint32_t)flat.size());
+      cur[list[j]] = std::move(c);
+    }
+    pe_action* d_p2 = (pe_action*)dalloc(std::max<size_t>(1, flat.size()) * sizeof(pe_action));
+    uint32_t* d_o2 = (uint32_t*)dalloc(off.size() * 4);
+    uint64_t* d_s2 = (uint64_t*)dalloc((size_t)m * 8);
+    pe_action* d_a2 = (pe_action*)dalloc((size_t)m * maxd * sizeof(pe_action));
+    uint32_t* d_n2 = (uint32_t*)dalloc((size_t)m * 4);
+    pe_result* d_r2 = (pe_result*)dalloc((size_t)m * sizeof(pe_result));
+    uint64_t* d_l2 = io.d_legal ? (uint64_t*)dalloc((size_t)m * lw * 8) : nullptr;
+    uint8_t* d_tl = (uint8_t*)dalloc(m);
+    if (!d_p2 || !d_o2 || !d_s2 || !d_a2 || !d_n2 || !d_r2 || (io.d_legal && !d_l2) || !d_tl)
+      return fail(PE_ERR_CUDA);
+    std::vector<uint64_t> s2h(seed2.begin(), seed2.end());
+    bool ok = (flat.empty() || cuda_ok(cudaMemcpyAsync(d_p2, flat.data(), flat.size() * sizeof(pe_action),
+                                                       cudaMemcpyHostToDevice, st), err, "H2D ir")) &&
+              cuda_ok(cudaMemcpyAsync(d_o2, off.data(), off.size() * 4, cudaMemcpyHostToDevice, st), err, "H2D ir") &&
+              cuda_ok(cudaMemcpyAsync(d_s2, s2h.data(), (size_t)m * 8, cudaMemcpyHostToDevice, st), err, "H2D ir") &&
+              cuda_ok(cudaMemcpyAsync(d_tl, take_legal.data(), m, cudaMemcpyHostToDevice, st), err, "H2D ir");
+    ok = ok && cuda_ok(enqueue_rollouts(e, io.gv, d_p2, d_o2, d_s2, m, d_a2, d_n2, d_r2, d_l2,
+                                        nullptr, SchedView(), io.max_acts, st),
+                       err, "pe_rollout_kernel launch (resume)");
+    if (ok) {
+      pe_ir_scatter_kernel<<<(m + 255) / 256, 256, 0, st>>>(d_list, m, d_r2, d_a2, d_n2, d_l2, d_tl,
+                                                            maxd, lw, io.d_out, io.d_acts,
+                                                            io.d_nacts, io.d_legal);
+      e->launches += 1;
+      ok = cuda_ok(cudaGetLastError(), err, "ir launch") &&
+           cuda_ok(cudaStreamSynchronize(st), err, "ir sync");
+    }
+    // (flat / off / seeds are read by the async copies before this point)
+    if (!ok) return fail(PE_ERR_CUDA);
+    for (size_t k = 2; k < bufs.size(); ++k) cudaFree(bufs[k]);
+    bufs.resize(2);
+  }
+  return fail(PE_OK);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1482,61 +1867,38 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   const uint32_t* perm = nullptr;
   SchedView sv;
   bool roots = (flags & PE_MEM_DEVICE) ? prefix == nullptr : prefix_off[n] == 0;
-  if (roots && e->sched_depth > 0 && !e->wl.resurface && n >= e->sched_min_batch &&
+  if (roots && e->sched_depth > 0 && !e->wl.resurface && !e->wl.infer_rest &&
+      n >= e->sched_min_batch &&
       !sched_perm(e, n, d_seeds, maxd, st, &perm, &sv, err))
     return PE_ERR_CUDA;
   // candidates start from their node's saved state unless legal sets after
   // the (empty) prefix are requested
   if (d_legal || !sv.snap) sv.keys = nullptr;
-  uint32_t slots = launch_slots(e, n);
-  if (!cuda_ok(cudaMemsetAsync(e->d_ctr + 1, 0, sizeof(uint32_t), st), err,
-               "reset work counter"))
-    return PE_ERR_CUDA;
   // host mode: the kernels record the longest action list so only that many
   // columns of acts_out travel back
   uint32_t* max_acts = (flags & PE_MEM_DEVICE) ? nullptr : e->d_ctr + 4;
   if (max_acts && !cuda_ok(cudaMemsetAsync(max_acts, 0, 4, st), err, "reset max acts"))
     return PE_ERR_CUDA;
-  uint32_t bs = std::min<uint32_t>(e->big_slots, n);
-  uint32_t threads = slots * kThreadsPerSlot;
-  uint32_t blk = threads % PE_SM_THREADS == 0 && threads >= (uint32_t)e->sm_count * PE_SM_THREADS
-                     ? PE_SM_THREADS : kBlock;
-  uint32_t grid = (threads + blk - 1) / blk;
-  uint32_t bgrid = (bs * kThreadsPerSlot + kBlock - 1) / kBlock;
-  // (the stuck-resurfacing instantiation only when the worklist uses it)
-  auto launch = [&](auto main_k, auto retry_k) {
-    // (experiment PE_L2_PERSIST: the graph image as a persisting L2 window)
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow.base_ptr = e->d_graph;
-    at[0].val.accessPolicyWindow.num_bytes = e->l2_window;
-    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(blk);
-    lc.stream = st;
-    lc.attrs = at;
-    lc.numAttrs = e->l2_persist ? 1 : 0;
-    cudaError_t le = cudaLaunchKernelEx(&lc, main_k, e->dview, e->layout, e->d_arena, slots,
-                                        d_prefix, d_poff, d_seeds, n, maxd, e->cp, e->baseline,
-                                        d_acts, d_nacts, d_out, d_legal, lw, e->d_ctr + 1, perm,
-                                        sv, max_acts);
-    // the retry launch reads the statuses the main launch writes: never
-    // queue it behind a main launch that failed to start
-    if (le != cudaSuccess) return le;
-    retry_k<<<bgrid, kBlock, 0, st>>>(e->dview, e->big_layout, e->d_big_arena, bs, d_prefix,
-                                      d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
-                                      d_nacts, d_out, d_legal, lw, nullptr, nullptr,
-                                      SchedView(), max_acts);
-    return cudaGetLastError();
-  };
-  cudaError_t lerr = e->wl.resurface
-                         ? launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>)
-                         : launch(pe_rollout_kernel<false, false>, pe_rollout_kernel<true, false>);
-  e->launches += 2;
-  if (!cuda_ok(lerr, err, "pe_rollout_kernel launch")) return PE_ERR_CUDA;
+  // InferRest decisions (pe.h infer_rest_action, or unexpanded markers in a
+  // host prefix) pause their candidates for the batched expansion below
+  bool ir = e->wl.infer_rest;
+  if (!(flags & PE_MEM_DEVICE))
+    for (uint32_t k = 0; k < prefix_off[n] && !ir; ++k)
+      ir = prefix[k].kind == PE_ACT_INFER_REST && !(prefix[k].pad & PE_ACT_FLAG_EXPANDED);
+  pe::GraphView gv = e->dview;
+  gv.ir_pause = ir ? 1 : 0;
+  if (!cuda_ok(enqueue_rollouts(e, gv, d_prefix, d_poff, d_seeds, n, d_acts, d_nacts, d_out,
+                                d_legal, perm, sv, max_acts, st),
+               err, "pe_rollout_kernel launch"))
+    return PE_ERR_CUDA;
+  if (ir) {
+    RolloutIo io{gv, d_prefix, d_poff, d_seeds, n, d_acts, d_nacts, d_out, d_legal, max_acts,
+                 (flags & PE_MEM_DEVICE) ? nullptr : prefix,
+                 (flags & PE_MEM_DEVICE) ? nullptr : prefix_off,
+                 (flags & PE_MEM_DEVICE) ? nullptr : seeds};
+    pe_status rs = ir_resolve(e, io, st, err);
+    if (rs != PE_OK) return rs;
+  }
   if (!(flags & PE_MEM_DEVICE)) {
     uint32_t kmax = 0;
     bool ok = cuda_ok(cudaMemcpyAsync(&kmax, max_acts, 4, cudaMemcpyDeviceToHost, st), err,

@@ -574,6 +574,8 @@ void attach_worklist(GraphView& v, const Worklist& w) {
   v.grp_mem = w.grp_mem.data();
   v.n_ord = w.n_static_ordinals();
   v.resurface = w.resurface ? 1 : 0;
+  v.ir_ord = w.infer_rest ? w.n_ordinals() : -1;
+  v.ir_pause = 0;
   v.ord_off = w.ord_off.data();
   v.ord_mem = w.ord_mem.data();
 }

@@ -85,17 +85,20 @@ struct Worklist {
   std::vector<int32_t> ent_val;  // action value per entry: group index or argument
   bool groups = true;
   bool resurface = false;  // stuck resurfacing (pe.h resurface_stuck)
+  bool infer_rest = false;  // InferRest is an action (pe.h infer_rest_action)
   int32_t n_ops = 0;
   int32_t n_entries() const { return (int32_t)ent_off.size() - 1; }
   // ordinals of the static entries (arguments / groups)
   int32_t n_static_ordinals() const {
     return n_entries() * kMaxRank * (int32_t)auto_axes.size();
   }
-  // all ordinals: static entries, then one block per op when stuck nodes
-  // can resurface
+  // TileValue ordinals: static entries, then one block per op when stuck
+  // nodes can resurface
   int32_t n_ordinals() const {
     return (n_entries() + (resurface ? n_ops : 0)) * kMaxRank * (int32_t)auto_axes.size();
   }
+  // every action ordinal but Stop: the TileValue ones, then InferRest
+  int32_t n_action_ordinals() const { return n_ordinals() + (infer_rest ? 1 : 0); }
 };
 // keep = per-argument filter (empty = all arguments; ranker top-k)
 Worklist build_worklist(const HostGraph& g, uint32_t auto_axes_mask, bool group_scopes,

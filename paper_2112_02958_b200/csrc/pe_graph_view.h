@@ -113,6 +113,12 @@ struct GraphView {
   int32_t resurface;
   // TileValue ordinals of the static entries: statically legal members
   int32_t n_ord;
+  // InferRest as a rollout action (pe.h infer_rest_action): ir_ord = its
+  // ordinal (after every TileValue ordinal), -1 when off.  A drawn InferRest
+  // -- and, when ir_pause, an unexpanded InferRest in a prefix -- pauses the
+  // candidate (PE_CAND_PAUSED) for the host's batched expansion.
+  int32_t ir_ord;
+  int32_t ir_pause;
   const int32_t* ord_off;    // [n_ord+1]
   const int32_t* ord_mem;
 

@@ -146,6 +146,9 @@ def ordinal_actions(graph, cfg) -> list:
             for d in range(capi.PE_MAX_RANK):
                 for ax in auto:
                     out.append(PeAction(graph.n_args + o, d, ax, capi.PE_ACT_TILE, 0))
+    if getattr(cfg, "infer_rest_action", 0):
+        # InferRest follows every TileValue ordinal (pe.h infer_rest_action)
+        out.append(PeAction(0, 0, 0, capi.PE_ACT_INFER_REST, 0))
     out.append(PeAction(0, 0, 0, capi.PE_ACT_STOP, 0))
     return out
 

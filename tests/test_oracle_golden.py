@@ -84,6 +84,21 @@ def test_legal_actions_linear(oracle_lib):
     assert len(H.oracle_legal(modelgen.linear(), [(1, 1, 0, 0)], cfg)) == 0
 
 
+def test_legal_actions_with_infer_rest(oracle_lib):
+    # SPEC legal_actions: "... plus InferRest (if any argument untiled) and
+    # Stop": `linear` on {shard=2} offers 6 TileValue + InferRest; an axis of
+    # size 3 leaves "only Stop and InferRest"; once every argument carries
+    # tiling (w sliced, b sliced, x atomic) InferRest is gone too
+    cfg = capi.default_search_config(group_scopes=0, infer_rest_action=1)
+    ir = H.oracle_info(modelgen.linear(), cfg)["n_ordinals"] - 1
+    legal = H.oracle_legal(modelgen.linear(), [], cfg)
+    assert len(legal) == 7 and legal[-1] == ir
+    assert H.oracle_legal(modelgen.linear(mesh=(("shard", 3),)), [], cfg) == [ir]
+    assert H.oracle_legal(modelgen.linear(), [(1, 1, 0, 0)], cfg) == []
+    # applying InferRest first (nothing tiled) is a legal no-op decision
+    assert len(H.oracle_legal(modelgen.linear(), [(0, 0, 0, 2)], cfg)) == 7
+
+
 def test_batch_first_blocks_model_actions(oracle_lib):
     # SURVEY.md §0 hazard (v): tiling the batch input before the model-axis
     # decisions wraps every weight atomic; every later weight action is illegal.
