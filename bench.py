@@ -374,6 +374,128 @@ def run_engine(args):
     return 0
 
 
+# ------------------------------------------------------------- config 4 sweep
+def cpu_capped(text, cfg, cap_s, threads, seed0):
+    """Reference CPU rollouts on `threads` host threads, each thread taking
+    candidates until `cap_s` seconds have passed (a candidate that starts
+    before the cap runs to completion).  Returns (completed, seconds)."""
+    import concurrent.futures as cf
+
+    import helpers as H
+    t0 = time.perf_counter()
+    done = [0] * threads
+
+    def worker(k):
+        i = 0
+        while time.perf_counter() - t0 < cap_s:
+            H.rollout_batch("oracle", text, [[]], [seed0 + k * 1_000_000 + i], cfg, threads=1)
+            done[k] += 1
+            i += 1
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(worker, range(threads)))
+    return sum(done), time.perf_counter() - t0
+
+
+def run_sweep(args):
+    """BASELINE.json configs[3] / SURVEY.md §8(d) config 4: batched
+    candidate evaluation at 1K..1M candidates per launch on the 48-layer
+    training-step graph (52,154 ops, 1,156 arguments), mesh [batch=4,
+    model=2], grouped worklist.  One JSON line; `value` is the largest size's
+    device-timed rate, `sweep` has every size."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2112_02958_b200 import capi, engine, modelgen
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    text = modelgen.config_program(4)
+    cfg = capi.default_search_config(group_scopes=1)
+    g = engine.Graph(text)
+    eng = engine.Engine(g, device=0, cfg=cfg)
+    maxd = cfg.max_decisions
+    st = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(st.cuda_stream)
+    b_cand = eng.graph_bytes() + 2 * 8 * (g.n_args + g.n_ops) + C.sizeof(capi.PeResult) + 8 * maxd + 16
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    sizes = [int(x) for x in args.sizes.split(",")]
+    rows = []
+    base = 40_000_000
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    with ClockSampler(0) as clk:
+        for B in sizes:
+            seeds = torch.arange(B, dtype=torch.int64, device=dev)
+            poff = torch.zeros(B + 1, dtype=torch.int32, device=dev)
+            acts = torch.empty(B * maxd * 8, dtype=torch.uint8, device=dev)
+            na = torch.empty(B, dtype=torch.int32, device=dev)
+            res = torch.empty(B * C.sizeof(capi.PeResult), dtype=torch.uint8, device=dev)
+            ms = []
+            for rep in range(args.warmup + args.steps):
+                seeds.add_(base)  # fresh candidates every call
+                base += B
+                flush.zero_()
+                torch.cuda.synchronize(dev)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                eng.rollout_batch_device(None, poff.data_ptr(), seeds.data_ptr(), B, acts.data_ptr(),
+                                         na.data_ptr(), res.data_ptr(), stream=sp)
+                e1.record(st)
+                torch.cuda.synchronize(dev)
+                if rep >= args.warmup:
+                    ms.append(e0.elapsed_time(e1))
+            t = sum(ms) / len(ms)
+            cps = B / t * 1e3
+            import numpy as np
+            host = res.view(B, C.sizeof(capi.PeResult)).cpu().numpy().view(np.int32)
+            f = lambda name: host[:, getattr(capi.PeResult, name).offset // 4]  # noqa: E731
+            rows.append({"candidates": B, "ms_per_launch": t, "cand_per_s": cps,
+                         "roofline_frac": cps * b_cand / 1e9 / peak,
+                         "failed": int((f("status") != 0).sum()),
+                         "mean_decisions": float(f("n_steps").mean()),
+                         "mean_spmd_ops": float(f("n_spmd_ops").mean())})
+            print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
+    top = rows[-1]
+    # e2e: host buffers through the C-ABI at the largest size (copies timed)
+    B = sizes[-1]
+    t0 = time.perf_counter()
+    eng.rollout_roots_np(__import__("numpy").arange(B, dtype="uint64") + base)
+    e2e = B / (time.perf_counter() - t0)
+    cpu = None
+    if not args.no_cpu_baseline:
+        import helpers as H
+        if os.path.exists(H.ORACLE_SO):
+            threads = os.cpu_count() or 1
+            done, dt = cpu_capped(text, cfg, args.cpu_cap_s, threads, 90_000_000)
+            cpu = {"value": done / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"root rollouts, {threads} threads, each capped at {args.cpu_cap_s:.0f} s "
+                             f"(a started candidate finishes): {done} completed in {dt:.0f} s",
+                   "completed": done, "note": "see profiles/r2_cfg4_cpu_baseline.json for the "
+                   "30-min-per-thread capped run and its extrapolation"}
+    line = {"metric": METRIC, "value": top["cand_per_s"], "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": top["ms_per_launch"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic",
+            "config": {"workload": "config 4: 48-layer training step (52,154 ops, 1,156 args), "
+                                   "mesh [batch=4, model=2], grouped worklist, root rollouts",
+                       "graph_ops": g.n_ops, "graph_args": g.n_args, "sizes": sizes,
+                       "arena_bytes": eng.arena_bytes(), "slots": eng.slots(),
+                       "l2": "256 MB flush before every launch"},
+            "sweep": rows,
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * 8 + (B + 1) * 4,
+                    "d2h_bytes_per_step": B * (maxd * 8 + 4 + C.sizeof(capi.PeResult))},
+            "roofline": {"bound": "hbm", "achieved": top["cand_per_s"] * b_cand / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": top["roofline_frac"], "traffic": None,
+                         "algorithmic_bytes_per_candidate": b_cand, "kernel": "pe_rollout_kernel"},
+            "cpu_baseline": cpu, "clocks": clk.summary()}
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -385,7 +507,19 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity-sample", action="store_true")
     ap.add_argument("--parity-n", type=int, default=128)
+    ap.add_argument("--config", type=int, default=3,
+                    help="3: the headline (GPT-2-medium 24L rollouts); 4: the 1K..1M sweep")
+    ap.add_argument("--sizes", default="1024,4096,16384,65536",
+                    help="config 4 sweep sizes (candidates per launch)")
+    ap.add_argument("--cpu-cap-s", type=float, default=60.0,
+                    help="config 4: per-thread cap of the reference CPU sample")
     args = ap.parse_args()
+    if args.config == 4:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config 4 reference timing is the "
+                              "capped run in profiles/r2_cfg4_cpu_baseline.json"}))
+            return 0
+        return run_sweep(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_engine(args)

@@ -354,6 +354,49 @@ int64_t pe_engine_sched_nodes(const pe_engine* e);
  * (also env PE_SCHED_SNAP_GB at engine creation). */
 pe_status pe_engine_set_state_reuse(pe_engine* e, double budget_gb);
 
+/* Prefix-state cache (incremental leaf evaluation): with a
+ * budget > 0 (GiB of HBM), host-mode pe_rollout_batch calls save the
+ * propagated state after each candidate's (non-empty, TILE / TILE_GROUP
+ * only) prefix, and a later candidate whose prefix extends a cached one
+ * starts from that state instead of replaying it -- an MCTS leaf is its
+ * parent's state plus one action.  Least-recently-used slots are reused.
+ * Results are identical with or without it.  Not used with stuck
+ * resurfacing or InferRest actions.  pe_search turns it on (4 GiB) when
+ * unset.  Set before the first call that would use it. */
+pe_status pe_engine_set_prefix_cache(pe_engine* e, double budget_gb);
+/* lookups that started from a cached state, states saved, live entries */
+void pe_engine_prefix_cache_stats(const pe_engine* e, uint64_t* hits, uint64_t* saved,
+                                  int64_t* entries);
+
+/* ---- state handles (§8(b) pe_state): a propagated partitioning state ----
+ * pe_state_create evaluates `acts` (TILE / TILE_GROUP decisions from the
+ * untiled graph: apply_tile_action + propagate each, REF rewrite.cc:61,
+ * propagate.cc:459) and keeps the propagated state on the device.
+ * PE_ERR_ILLEGAL / PE_ERR_INTERNAL when the sequence does not evaluate. */
+typedef struct pe_state pe_state;
+pe_status pe_state_create(pe_engine* e, const pe_action* acts, uint32_t n, pe_state** out,
+                          pe_error* err);
+void pe_state_destroy(pe_state* s);
+uint32_t pe_state_num_decisions(const pe_state* s);
+/* the state's own evaluation (lower_to_spmd + collective_stats + cost) */
+pe_status pe_state_result(const pe_state* s, pe_result* out);
+/* Per-argument ShardingSpec of the lowered program's arguments and of the
+ * returned value as spec words (trace layout above; REF spmd.cc:370-391,
+ * mesh.h ShardingSpec), and the stuck list of the last propagate as
+ * (op index, reason) pairs (REF propagate.h:28-38).  arg_specs: A words;
+ * stuck: 2 * stuck_cap words; any may be NULL. */
+pe_status pe_state_specs(const pe_state* s, uint32_t* arg_specs, uint32_t* result_spec,
+                         int32_t* stuck, uint32_t stuck_cap, uint32_t* n_stuck, pe_error* err);
+/* Incremental evaluation (host buffers): candidate c = parents[c] (NULL =
+ * the untiled graph) + acts[seq_off[c] .. seq_off[c+1]) (TILE / TILE_GROUP),
+ * each action applied + propagated from the parent's saved state, then
+ * lowered and scored: the same result as pe_eval_batch of the parent's
+ * decisions followed by the candidate's actions (fail_step indexes that
+ * concatenation). */
+pe_status pe_eval_from_states(pe_engine* e, const pe_state* const* parents, const pe_action* acts,
+                              const uint32_t* seq_off, uint32_t n, pe_result* out, void* stream,
+                              pe_error* err);
+
 /* ---- search (SPEC search module: mcts_search / emit_plan) ---- */
 #define PE_PLAN_MAX_ACTIONS 64
 

@@ -193,6 +193,17 @@ SIGNATURES = {
     "pe_engine_sched_nodes": (C.c_int64, [_P]),
     "pe_engine_set_state_reuse": (C.c_int, [_P, C.c_double]),
     "pe_engine_graph_bytes": (C.c_int64, [_P]),
+    "pe_engine_set_prefix_cache": (C.c_int, [_P, C.c_double]),
+    "pe_engine_prefix_cache_stats": (None, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                            C.POINTER(C.c_int64)]),
+    "pe_state_create": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(_P), C.POINTER(PeError)]),
+    "pe_state_destroy": (None, [_P]),
+    "pe_state_num_decisions": (C.c_uint32, [_P]),
+    "pe_state_result": (C.c_int, [_P, C.POINTER(PeResult)]),
+    "pe_state_specs": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                 C.POINTER(C.c_int32), C.c_uint32, C.POINTER(C.c_uint32),
+                                 C.POINTER(PeError)]),
+    "pe_eval_from_states": (C.c_int, [_P, _P, _P, _P, C.c_uint32, _P, _P, C.POINTER(PeError)]),
     "pe_mcts_run": (C.c_int, [C.POINTER(PeMctsParams), ROLLOUT_FN, _P, MERGE_FN, _P, _P,
                               C.POINTER(PePlan), C.POINTER(PeError)]),
     "pe_search": (C.c_int, [_P, C.POINTER(PeSearchConfig), C.c_uint32, C.c_uint32, MERGE_FN,

@@ -307,6 +307,23 @@ struct Pull {
   int32_t drive;  // value slot of the driving loop
 };
 
+// Where a rollout starts: from init(), or from a saved
+// propagated state (Cand::save) covering the first `done` decisions --
+// `path`, recorded into the action output -- with the prefix applied from
+// entry k0 on and `draws` RNG draws already consumed; the state after the
+// whole prefix may be saved for later candidates (prefix-state cache,
+// pe_state handles).
+struct Resume {
+  const uint8_t* snap = nullptr;
+  int32_t done = 0;
+  const pe_action* path = nullptr;
+  int32_t k0 = 0;
+  int32_t draws = 0;
+  bool stop = false;       // (scheduling trie) its next draw is Stop
+  uint8_t* save = nullptr;  // save the post-prefix state here ...
+  uint8_t* saved = nullptr; // ... and set *saved = 1 once written
+};
+
 struct Cand {
   const GraphView& g;
   const Caps caps;
@@ -538,10 +555,17 @@ struct Cand {
     for (int32_t i = 0; i < nfs; ++i) *q++ = a.fs()[i];
     for (int32_t w = 0; w <= (g.A >> 5); ++w) *q++ = (int32_t)a.carry()[w];
   }
-  // init() for a candidate that starts from a saved prefix state
+  // init() for a candidate that starts from a saved prefix state; a state
+  // saved from a full-size arena may not fit a tight one (CAPACITY: the
+  // retry kernel loads it into a full-size arena)
   PE_HD void load(const uint8_t* src) {
     const V4* p = reinterpret_cast<const V4*>(src);
     V4 h = *p++;
+    status = PE_CAND_OK;
+    if (h.x > caps.V || h.y > caps.L || h.z > caps.FS) {
+      fail(PE_CAND_CAPACITY);
+      return;
+    }
     nslots = h.x;
     nloops = h.y;
     nfs = h.z;
@@ -1807,26 +1831,25 @@ struct Cand {
   // kernel: instruction-cache stalls).
   template <bool RS>
   //
-  // snap (prefix-state reuse): start from the saved state
-  // after the candidate's first snap_d decisions -- `snap_path`, which its
-  // own seed draws (the scheduler matched them; snap_stop: its next draw is
-  // Stop) -- instead of init() and replaying them.  Only for root rollouts
-  // (np == 0) without legal output.
+  // rs: start from a saved state instead of init() and
+  // replaying the decisions it covers -- the scheduling trie's states of
+  // root rollouts (their own seed draws the path; rs.stop: the next draw is
+  // Stop) and the prefix-state cache / pe_state parents (the path is the
+  // prefix's first rs.done entries).
   PE_HD void rollout(const pe_action* prefix, int32_t np, uint64_t seed, int32_t maxd,
                      const pe_cost_params& cp, int64_t baseline, pe_action* acts_out,
                      uint32_t* n_out, pe_result& r, uint64_t* legal_out, int32_t legal_words,
-                     const uint8_t* snap = nullptr, int32_t snap_d = 0,
-                     const pe_action* snap_path = nullptr, bool snap_stop = false) {
+                     const Resume& rs = Resume()) {
     tracing = false;
     tick_start();
     int32_t steps = 0, nacts = 0;
     bool propagated = false, terminal = false;
-    if (snap) {
-      load(snap);
-      for (int32_t k = 0; k < snap_d && k < maxd; ++k) acts_out[k] = snap_path[k];
-      steps = nacts = snap_d;
-      propagated = snap_d > 0;
-      terminal = snap_stop;
+    if (rs.snap) {
+      load(rs.snap);
+      for (int32_t k = 0; k < rs.done && k < maxd; ++k) acts_out[k] = rs.path[k];
+      steps = nacts = rs.done;
+      propagated = rs.done > 0;
+      terminal = rs.stop;
     } else {
       init();
     }
@@ -1841,7 +1864,7 @@ struct Cand {
     // before enumerating legal actions -- i.e. after every whole decision,
     // as the oracle does after each apply_action
     bool rs_due = false;
-    for (int32_t k = 0; k < np; ++k) {
+    for (int32_t k = bad() ? np : rs.k0; k < np; ++k) {
       if (RS && rs_due && !(prefix[k].pad & PE_ACT_FLAG_INFERRED)) {
         resurface_update();
         rs_due = false;
@@ -1890,6 +1913,10 @@ struct Cand {
       }
     }
     if (RS && rs_due && !bad() && status == PE_CAND_OK) resurface_update();
+    if (rs.save && !bad() && status == PE_CAND_OK) {
+      save(rs.save);
+      if (rs.saved) *rs.saved = 1;
+    }
     if (!bad() && status == PE_CAND_OK) {
       if (legal_out) {
         int32_t nl = build_legal<RS>();
@@ -1898,8 +1925,8 @@ struct Cand {
           legal_out[g.ir_ord >> 6] |= 1ull << (g.ir_ord & 63);
       }
       // (each decision draws once: splitmix adds the golden gamma per draw)
-      uint64_t st = seed + (uint64_t)snap_d * 0x9E3779B97F4A7C15ull;
-      int32_t draws = snap_d;
+      uint64_t st = seed + (uint64_t)rs.draws * 0x9E3779B97F4A7C15ull;
+      int32_t draws = rs.draws;
       while (!terminal) {
         if (steps >= maxd) break;
         tick(4);

@@ -88,6 +88,29 @@ struct pe_engine {
   // calls on different streams are serialised on the device: each call's
   // stream waits for the previous call's last enqueued work.
   cudaEvent_t done = nullptr;
+  // Prefix-state cache (pe_engine_set_prefix_cache): the post-prefix states
+  // of host-mode rollout prefixes (MCTS leaves: the tree path), keyed by the
+  // prefix's bytes.  A candidate starts from its longest cached prefix and
+  // saves its own; slots are reused least-recently-used (clock hand).
+  double pc_budget_gb = 0.0;
+  uint8_t* d_pc = nullptr;
+  uint64_t pc_stride = 0;
+  int32_t pc_cap = 0, pc_hand = 0;
+  std::unordered_map<std::string, int32_t> pc_map;
+  std::vector<std::string> pc_key;
+  std::vector<uint64_t> pc_used;
+  uint64_t pc_clock = 0, pc_hits = 0, pc_saved = 0;
+  std::vector<std::string> pc_pending;  // per candidate of the current call
+  uint64_t* d_cv = nullptr;  // from | save addresses, from_len, saved flags
+  size_t cv_cap = 0;
+};
+
+struct pe_state {
+  pe_engine* e = nullptr;
+  uint8_t* d_snap = nullptr;         // Cand::save image of the propagated state
+  std::vector<pe_action> path;       // the decisions it covers
+  pe_result result{};                // its evaluation (lowered + scored)
+  std::vector<int32_t> trace;        // its parity trace (pe_state_specs)
 };
 
 namespace {
@@ -205,6 +228,17 @@ struct SchedView {
   uint32_t kstride = 1;  // keys are node * kstride + slot
 };
 
+// Per-candidate saved states (prefix-state cache, pe_state handles): start
+// from the state at device address from[i] (0: none) covering the first
+// from_len[i] prefix entries; save the post-prefix state to save[i] (0:
+// none) and set saved[i] = 1 once written.
+struct CacheView {
+  const uint64_t* from = nullptr;
+  const int32_t* from_len = nullptr;
+  const uint64_t* save = nullptr;
+  uint8_t* saved = nullptr;
+};
+
 template <bool RETRY, bool RS>
 __global__ void __launch_bounds__(kSmBlock, 1)
 pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
@@ -213,7 +247,8 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                   uint32_t n, int32_t maxd, pe_cost_params cp, int64_t baseline,
                   pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
                   int32_t legal_words, uint32_t* ctr, const uint32_t* perm,
-                  const __grid_constant__ SchedView sv, uint32_t* max_acts) {
+                  const __grid_constant__ SchedView sv, const __grid_constant__ CacheView cv,
+                  uint32_t* max_acts) {
 #if PE_SOLO
   // experiment: one active lane per warp (no SIMT divergence across candidates)
   if (threadIdx.x % 32) return;
@@ -229,19 +264,28 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
   auto run = [&](uint32_t k) {
     uint32_t i = perm ? perm[k] : k;
     if (RETRY && out[i].status != PE_CAND_CAPACITY) return;
-    // start from the saved state of the candidate's trie node when there is one
-    const uint8_t* snap = nullptr;
-    const pe_action* spath = nullptr;
-    int32_t sd = 0;
-    bool sstop = false;
+    // start from a saved state: the candidate's trie node's, or its longest
+    // cached prefix's
+    pe::Resume rs;
     if (sv.keys) {
       uint32_t key = sv.keys[i], node = key / sv.kstride;
       int4 nd = sv.tnode[node];
       if (nd.w >= 0) {
-        snap = sv.snap + sv.stride * (uint64_t)nd.w;
-        sd = nd.z;
-        spath = sv.tpath + (uint64_t)node * sv.path_cap;
-        sstop = key % sv.kstride == 0;  // its next draw is Stop
+        rs.snap = sv.snap + sv.stride * (uint64_t)nd.w;
+        rs.done = rs.draws = nd.z;
+        rs.path = sv.tpath + (uint64_t)node * sv.path_cap;
+        rs.stop = key % sv.kstride == 0;  // its next draw is Stop
+      }
+    }
+    if (cv.from) {
+      if (cv.from[i]) {
+        rs.snap = reinterpret_cast<const uint8_t*>(cv.from[i]);
+        rs.done = rs.k0 = cv.from_len[i];
+        rs.path = prefix + poff[i];
+      }
+      if (cv.save[i]) {
+        rs.save = reinterpret_cast<uint8_t*>(cv.save[i]);
+        rs.saved = cv.saved + i;
       }
     }
 #if defined(PE_CAND_TIMES) && defined(__CUDA_ARCH__)
@@ -251,7 +295,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
     c.template rollout<RS>(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd,
                            cp, baseline, acts_out + (uint64_t)i * maxd, n_out + i, r,
                            legal_out ? legal_out + (uint64_t)i * legal_words : nullptr,
-                           legal_words, snap, sd, spath, sstop);
+                           legal_words, rs);
     out[i] = r;
 #if defined(PE_CAND_TIMES) && defined(__CUDA_ARCH__)
     if (!RETRY && k < kCandTimesCap) {
@@ -907,6 +951,8 @@ void pe_engine_destroy(pe_engine* e) {
                   (void*)e->d_perm, (void*)e->d_hist, (void*)e->d_tpath, (void*)e->d_snap})
     if (q) cudaFree(q);
   if (e->d_io) cudaFree(e->d_io);
+  if (e->d_pc) cudaFree(e->d_pc);
+  if (e->d_cv) cudaFree(e->d_cv);
   if (e->done) cudaEventDestroy(e->done);
   delete e;
 }
@@ -1159,7 +1205,7 @@ bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefix
         e->dview, e->big_layout, e->d_big_arena, bs, (const pe_action*)buf[0],
         (const uint32_t*)buf[1], (const uint64_t*)buf[2], n, maxd, e->cp, e->baseline,
         (pe_action*)buf[3], (uint32_t*)buf[4], (pe_result*)buf[5], (uint64_t*)buf[6], lw,
-        nullptr, nullptr, SchedView(), nullptr);
+        nullptr, nullptr, SchedView(), CacheView(), nullptr);
     e->launches += 2;
     ok = cuda_ok(cudaGetLastError(), err, "probe launch") &&
          cuda_ok(cudaMemcpyAsync(lg.data(), buf[6], sizes[6], cudaMemcpyDeviceToHost, st), err,
@@ -1383,7 +1429,7 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
                              const uint32_t* d_poff, const uint64_t* d_seeds, uint32_t n,
                              pe_action* d_acts, uint32_t* d_nacts, pe_result* d_out,
                              uint64_t* d_legal, const uint32_t* perm, const SchedView& sv,
-                             uint32_t* max_acts, cudaStream_t st) {
+                             const CacheView& cv, uint32_t* max_acts, cudaStream_t st) {
   int32_t maxd = (int32_t)e->cfg.max_decisions;
   int32_t lw = (int32_t)pe_engine_legal_words(e);
   uint32_t slots = launch_slots(e, n);
@@ -1414,14 +1460,14 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
     cudaError_t le = cudaLaunchKernelEx(&lc, main_k, gv, e->layout, e->d_arena, slots, d_prefix,
                                         d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
                                         d_nacts, d_out, d_legal, lw, e->d_ctr + 1, perm, sv,
-                                        max_acts);
+                                        cv, max_acts);
     // the retry launch reads the statuses the main launch writes: never
     // queue it behind a main launch that failed to start
     if (le != cudaSuccess) return le;
     retry_k<<<bgrid, kBlock, 0, st>>>(gv, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff,
                                       d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts,
                                       d_out, d_legal, lw, nullptr, nullptr, SchedView(),
-                                      max_acts);
+                                      CacheView(), max_acts);
     return cudaGetLastError();
   };
   cudaError_t lerr = e->wl.resurface
@@ -1783,7 +1829,7 @@ pe_status ir_resolve(pe_engine* e, const RolloutIo& io, cudaStream_t st, pe_erro
               cuda_ok(cudaMemcpyAsync(d_s2, s2h.data(), (size_t)m * 8, cudaMemcpyHostToDevice, st), err, "H2D ir") &&
               cuda_ok(cudaMemcpyAsync(d_tl, take_legal.data(), m, cudaMemcpyHostToDevice, st), err, "H2D ir");
     ok = ok && cuda_ok(enqueue_rollouts(e, io.gv, d_p2, d_o2, d_s2, m, d_a2, d_n2, d_r2, d_l2,
-                                        nullptr, SchedView(), io.max_acts, st),
+                                        nullptr, SchedView(), CacheView(), io.max_acts, st),
                        err, "pe_rollout_kernel launch (resume)");
     if (ok) {
       pe_ir_scatter_kernel<<<(m + 255) / 256, 256, 0, st>>>(d_list, m, d_r2, d_a2, d_n2, d_l2, d_tl,
@@ -1799,6 +1845,170 @@ pe_status ir_resolve(pe_engine* e, const RolloutIo& io, cudaStream_t st, pe_erro
     bufs.resize(2);
   }
   return fail(PE_OK);
+}
+
+
+uint64_t snapshot_stride(const pe_engine* e) {
+  return (pe::Cand::snap_bytes(e->dview, e->big_layout.caps) + 255) & ~uint64_t(255);
+}
+
+// Per candidate: its longest cached prefix (start there) and, when its whole
+// prefix is not cached yet, a slot to save the post-prefix state into.
+bool pc_plan(pe_engine* e, const pe_action* prefix, const uint32_t* poff, uint32_t n,
+             cudaStream_t st, CacheView* cv, std::vector<int32_t>& save_slot, pe_error* err) {
+  if (!e->d_pc) {
+    e->pc_stride = snapshot_stride(e);
+    uint64_t cap = (uint64_t)(e->pc_budget_gb * (double)(1ull << 30)) / e->pc_stride;
+    e->pc_cap = (int32_t)std::min<uint64_t>(cap, 1u << 20);
+    if (e->pc_cap <= 0) return true;
+    if (!cuda_ok(cudaMalloc(&e->d_pc, (size_t)e->pc_cap * e->pc_stride), err,
+                 "cudaMalloc(prefix cache)"))
+      return false;
+    e->pc_key.assign(e->pc_cap, std::string());
+    e->pc_used.assign(e->pc_cap, 0);
+  }
+  ++e->pc_clock;
+  std::vector<uint64_t> from(n, 0), save(n, 0);
+  std::vector<int32_t> from_len(n, 0);
+  save_slot.assign(n, -1);
+  std::unordered_map<std::string, int32_t> planned;  // full prefixes saved by this batch
+  e->pc_pending.assign(n, std::string());
+  for (uint32_t i = 0; i < n; ++i) {
+    const char* b = reinterpret_cast<const char*>(prefix + poff[i]);
+    uint32_t np = poff[i + 1] - poff[i];
+    bool decisions = true;  // cache only plain decision prefixes
+    for (uint32_t k = 0; k < np && decisions; ++k)
+      decisions = prefix[poff[i] + k].kind <= PE_ACT_TILE_GROUP && prefix[poff[i] + k].pad == 0;
+    if (!decisions || np == 0) continue;
+    for (uint32_t k = np; k >= 1; --k) {
+      auto it = e->pc_map.find(std::string(b, (size_t)k * sizeof(pe_action)));
+      if (it == e->pc_map.end()) continue;
+      from[i] = (uint64_t)(e->d_pc + e->pc_stride * (uint64_t)it->second);
+      from_len[i] = (int32_t)k;
+      e->pc_used[it->second] = e->pc_clock;
+      ++e->pc_hits;
+      break;
+    }
+    if (from_len[i] == (int32_t)np) continue;
+    std::string key(b, (size_t)np * sizeof(pe_action));
+    if (planned.count(key)) continue;
+    // a slot not read by this batch: the clock hand's next
+    int32_t slot = -1;
+    for (int32_t tries = 0; tries < e->pc_cap && slot < 0; ++tries) {
+      int32_t h = e->pc_hand;
+      e->pc_hand = (e->pc_hand + 1) % e->pc_cap;
+      if (e->pc_used[h] != e->pc_clock) slot = h;
+    }
+    if (slot < 0) continue;
+    if (!e->pc_key[slot].empty()) e->pc_map.erase(e->pc_key[slot]);
+    e->pc_key[slot].clear();
+    e->pc_used[slot] = e->pc_clock;
+    save[i] = (uint64_t)(e->d_pc + e->pc_stride * (uint64_t)slot);
+    save_slot[i] = slot;
+    e->pc_pending[i] = key;
+    planned.emplace(std::move(key), slot);
+  }
+  // device arrays: from, save (u64), from_len (i32), saved flags (u8)
+  size_t words = 2 * (size_t)n + ((size_t)n + 1) / 2 + ((size_t)n + 7) / 8 + 4;
+  if (!ensure_dev(e->d_cv, e->cv_cap, words, err, "cudaMalloc(cache view)")) return false;
+  uint64_t* d_from = e->d_cv;
+  uint64_t* d_save = d_from + n;
+  int32_t* d_len = reinterpret_cast<int32_t*>(d_save + n);
+  uint8_t* d_saved = reinterpret_cast<uint8_t*>(d_len + ((n + 1) & ~1u));
+  if (!cuda_ok(cudaMemcpyAsync(d_from, from.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st), err, "H2D cache") ||
+      !cuda_ok(cudaMemcpyAsync(d_save, save.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st), err, "H2D cache") ||
+      !cuda_ok(cudaMemcpyAsync(d_len, from_len.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st), err, "H2D cache") ||
+      !cuda_ok(cudaMemsetAsync(d_saved, 0, n, st), err, "cache flags") ||
+      !cuda_ok(cudaStreamSynchronize(st), err, "cache sync"))  // (host vectors go away)
+    return false;
+  cv->from = d_from;
+  cv->from_len = d_len;
+  cv->save = d_save;
+  cv->saved = d_saved;
+  return true;
+}
+
+// After the launch: a slot becomes a cache entry only if its state was
+// written (a candidate that overflowed its tight arena saves nothing).
+bool pc_commit(pe_engine* e, uint32_t n, const std::vector<int32_t>& save_slot, cudaStream_t st,
+               pe_error* err) {
+  uint64_t* d_save = e->d_cv + n;
+  uint8_t* d_saved = reinterpret_cast<uint8_t*>(reinterpret_cast<int32_t*>(d_save + n) +
+                                                ((n + 1) & ~1u));
+  std::vector<uint8_t> saved(n);
+  if (!cuda_ok(cudaMemcpyAsync(saved.data(), d_saved, n, cudaMemcpyDeviceToHost, st), err, "D2H cache") ||
+      !cuda_ok(cudaStreamSynchronize(st), err, "cache sync"))
+    return false;
+  for (uint32_t i = 0; i < n; ++i) {
+    int32_t slot = save_slot[i];
+    if (slot < 0 || !saved[i]) continue;
+    e->pc_key[slot] = std::move(e->pc_pending[i]);
+    e->pc_map[e->pc_key[slot]] = slot;
+    ++e->pc_saved;
+  }
+  e->pc_pending.clear();
+  return true;
+}
+
+// Candidates = prefix (host) from optional saved states, no draws (each
+// prefix ends in Stop): the evaluation of prefix[c], optionally saving the
+// post-prefix state (pe_state handles).
+bool run_states(pe_engine* e, const std::vector<pe_action>& flat, const std::vector<uint32_t>& off,
+                const std::vector<uint64_t>& from, const std::vector<int32_t>& from_len,
+                const std::vector<uint64_t>& save, std::vector<uint8_t>& saved,
+                std::vector<pe_result>& res, cudaStream_t st, pe_error* err) {
+  uint32_t n = (uint32_t)off.size() - 1;
+  const int32_t maxd = (int32_t)e->cfg.max_decisions;
+  res.resize(n);
+  saved.assign(n, 0);
+  if (n == 0) return true;
+  std::vector<void*> bufs;
+  auto dal = [&](size_t b) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, std::max<size_t>(b, 16)) != cudaSuccess) return (void*)nullptr;
+    bufs.push_back(q);
+    return q;
+  };
+  pe_action* d_p = (pe_action*)dal(std::max<size_t>(1, flat.size()) * sizeof(pe_action));
+  uint32_t* d_o = (uint32_t*)dal(off.size() * 4);
+  uint64_t* d_s = (uint64_t*)dal((size_t)n * 8);
+  pe_action* d_a = (pe_action*)dal((size_t)n * maxd * sizeof(pe_action));
+  uint32_t* d_n = (uint32_t*)dal((size_t)n * 4);
+  pe_result* d_r = (pe_result*)dal((size_t)n * sizeof(pe_result));
+  uint64_t* d_f = (uint64_t*)dal((size_t)n * 8);
+  uint64_t* d_v = (uint64_t*)dal((size_t)n * 8);
+  int32_t* d_l = (int32_t*)dal((size_t)n * 4);
+  uint8_t* d_ok = (uint8_t*)dal(n);
+  bool ok = bufs.size() == 10;
+  if (!ok) set_err(err, PE_ERR_CUDA, "cudaMalloc(states)");
+  ok = ok && (flat.empty() || cuda_ok(cudaMemcpyAsync(d_p, flat.data(), flat.size() * sizeof(pe_action),
+                                                      cudaMemcpyHostToDevice, st), err, "H2D states")) &&
+       cuda_ok(cudaMemcpyAsync(d_o, off.data(), off.size() * 4, cudaMemcpyHostToDevice, st), err, "H2D states") &&
+       cuda_ok(cudaMemsetAsync(d_s, 0, (size_t)n * 8, st), err, "states") &&
+       cuda_ok(cudaMemcpyAsync(d_f, from.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st), err, "H2D states") &&
+       cuda_ok(cudaMemcpyAsync(d_v, save.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st), err, "H2D states") &&
+       cuda_ok(cudaMemcpyAsync(d_l, from_len.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st), err, "H2D states") &&
+       cuda_ok(cudaMemsetAsync(d_ok, 0, n, st), err, "states");
+  CacheView cv;
+  cv.from = d_f;
+  cv.from_len = d_l;
+  cv.save = d_v;
+  cv.saved = d_ok;
+  ok = ok && cuda_ok(enqueue_rollouts(e, e->dview, d_p, d_o, d_s, n, d_a, d_n, d_r, nullptr,
+                                      nullptr, SchedView(), cv, nullptr, st),
+                     err, "pe_rollout_kernel launch (states)") &&
+       cuda_ok(cudaMemcpyAsync(res.data(), d_r, (size_t)n * sizeof(pe_result), cudaMemcpyDeviceToHost, st),
+               err, "D2H states") &&
+       cuda_ok(cudaMemcpyAsync(saved.data(), d_ok, n, cudaMemcpyDeviceToHost, st), err, "D2H states") &&
+       cuda_ok(cudaStreamSynchronize(st), err, "states sync");
+  for (void* q : bufs) cudaFree(q);
+  return ok;
+}
+
+bool plain_decisions(const pe_action* a, uint32_t n) {
+  for (uint32_t k = 0; k < n; ++k)
+    if (a[k].kind > PE_ACT_TILE_GROUP || a[k].pad != 0) return false;
+  return true;
 }
 
 }  // namespace
@@ -1887,10 +2097,17 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
       ir = prefix[k].kind == PE_ACT_INFER_REST && !(prefix[k].pad & PE_ACT_FLAG_EXPANDED);
   pe::GraphView gv = e->dview;
   gv.ir_pause = ir ? 1 : 0;
+  // prefix-state cache (host mode, non-root prefixes)
+  CacheView cv;
+  std::vector<int32_t> pc_save;
+  if (!(flags & PE_MEM_DEVICE) && e->pc_budget_gb > 0 && !roots && !ir && !e->wl.resurface &&
+      !pc_plan(e, prefix, prefix_off, n, st, &cv, pc_save, err))
+    return PE_ERR_CUDA;
   if (!cuda_ok(enqueue_rollouts(e, gv, d_prefix, d_poff, d_seeds, n, d_acts, d_nacts, d_out,
-                                d_legal, perm, sv, max_acts, st),
+                                d_legal, perm, sv, cv, max_acts, st),
                err, "pe_rollout_kernel launch"))
     return PE_ERR_CUDA;
+  if (cv.save && !pc_commit(e, n, pc_save, st, err)) return PE_ERR_CUDA;
   if (ir) {
     RolloutIo io{gv, d_prefix, d_poff, d_seeds, n, d_acts, d_nacts, d_out, d_legal, max_acts,
                  (flags & PE_MEM_DEVICE) ? nullptr : prefix,
@@ -1924,6 +2141,153 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
   } else if (flags & PE_SYNC) {
     if (!cuda_ok(cudaStreamSynchronize(st), err, "sync")) return PE_ERR_CUDA;
   }
+  return PE_OK;
+}
+
+pe_status pe_engine_set_prefix_cache(pe_engine* e, double budget_gb) {
+  if (!e || budget_gb < 0) return PE_ERR_INVALID_ARGUMENT;
+  if (e->d_pc) return e->pc_budget_gb == budget_gb ? PE_OK : PE_ERR_INVALID_ARGUMENT;
+  e->pc_budget_gb = budget_gb;
+  return PE_OK;
+}
+
+void pe_engine_prefix_cache_stats(const pe_engine* e, uint64_t* hits, uint64_t* saved,
+                                  int64_t* entries) {
+  if (hits) *hits = e->pc_hits;
+  if (saved) *saved = e->pc_saved;
+  if (entries) *entries = (int64_t)e->pc_map.size();
+}
+
+pe_status pe_state_create(pe_engine* e, const pe_action* acts, uint32_t n, pe_state** out,
+                          pe_error* err) {
+  if (!e || !out || (n && !acts)) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  if (!plain_decisions(acts, n)) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "pe_state: TILE / TILE_GROUP decisions only");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+  pe_state* s = new pe_state();
+  s->e = e;
+  s->path.assign(acts, acts + n);
+  // its evaluation and parity trace (arg / result specs, stuck list)
+  const uint32_t tw = 8 + 2 * (uint32_t)e->graph->g.args.size() + 2 * (uint32_t)e->graph->g.ops.size();
+  s->trace.assign(tw, 0);
+  uint32_t off[2] = {0, n};
+  pe_status ps = pe_eval_batch(e, n ? acts : nullptr, off, 1, &s->result, s->trace.data(), tw, 0,
+                               nullptr, err);
+  if (ps != PE_OK) {
+    delete s;
+    return ps;
+  }
+  if (s->result.status != PE_CAND_OK) {
+    set_err(err, s->result.status == PE_CAND_ILLEGAL ? PE_ERR_ILLEGAL : PE_ERR_INTERNAL,
+            "pe_state: the sequence does not evaluate (status " +
+                std::to_string(s->result.status) + ")");
+    pe_status code = s->result.status == PE_CAND_ILLEGAL ? PE_ERR_ILLEGAL : PE_ERR_INTERNAL;
+    delete s;
+    return code;
+  }
+  if (!cuda_ok(cudaMalloc(&s->d_snap, snapshot_stride(e)), err, "cudaMalloc(state)")) {
+    delete s;
+    return PE_ERR_CUDA;
+  }
+  std::vector<pe_action> flat(s->path);
+  flat.push_back(pe_action{0, 0, 0, PE_ACT_STOP, 0});
+  std::vector<uint8_t> saved;
+  std::vector<pe_result> res;
+  if (!run_states(e, flat, {0, (uint32_t)flat.size()}, {0}, {0}, {(uint64_t)s->d_snap}, saved, res,
+                  nullptr, err)) {
+    pe_state_destroy(s);
+    return PE_ERR_CUDA;
+  }
+  if (!saved[0]) {  // (the full-size retry path saves nothing)
+    set_err(err, PE_ERR_CAPACITY, "pe_state: state exceeds the engine's tight arena");
+    pe_state_destroy(s);
+    return PE_ERR_CAPACITY;
+  }
+  *out = s;
+  if (err) err->code = PE_OK;
+  return PE_OK;
+}
+
+void pe_state_destroy(pe_state* s) {
+  if (!s) return;
+  if (s->d_snap) cudaFree(s->d_snap);
+  delete s;
+}
+
+uint32_t pe_state_num_decisions(const pe_state* s) { return (uint32_t)s->path.size(); }
+
+pe_status pe_state_result(const pe_state* s, pe_result* out) {
+  if (!s || !out) return PE_ERR_INVALID_ARGUMENT;
+  *out = s->result;
+  return PE_OK;
+}
+
+pe_status pe_state_specs(const pe_state* s, uint32_t* arg_specs, uint32_t* result_spec,
+                         int32_t* stuck, uint32_t stuck_cap, uint32_t* n_stuck, pe_error* err) {
+  if (!s) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null state");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  // the parity trace layout of pe.h: [0] words, [1] A, A arg specs, result
+  // spec, n_stuck, (op, reason) pairs, ...
+  const int32_t* t = s->trace.data();
+  int32_t A = t[1];
+  if (arg_specs)
+    for (int32_t x = 0; x < A; ++x) arg_specs[x] = (uint32_t)t[2 + x];
+  if (result_spec) *result_spec = (uint32_t)t[2 + A];
+  int32_t ns = t[3 + A];
+  if (n_stuck) *n_stuck = (uint32_t)ns;
+  for (int32_t i = 0; stuck && i < ns && (uint32_t)i < stuck_cap; ++i) {
+    stuck[2 * i] = t[4 + A + 2 * i];
+    stuck[2 * i + 1] = t[5 + A + 2 * i];
+  }
+  return PE_OK;
+}
+
+pe_status pe_eval_from_states(pe_engine* e, const pe_state* const* parents, const pe_action* acts,
+                              const uint32_t* seq_off, uint32_t n, pe_result* out, void* stream,
+                              pe_error* err) {
+  if (!e || !parents || !seq_off || !out || (seq_off[n] && !acts)) {
+    set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
+    return PE_ERR_INVALID_ARGUMENT;
+  }
+  if (n == 0) return PE_OK;
+  if (!cuda_ok(cudaSetDevice(e->device), err, "cudaSetDevice")) return PE_ERR_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<pe_action> flat;
+  std::vector<uint32_t> off{0};
+  std::vector<uint64_t> from(n, 0), save(n, 0);
+  std::vector<int32_t> from_len(n, 0);
+  for (uint32_t c = 0; c < n; ++c) {
+    const pe_state* p = parents[c];
+    if (p && p->e != e) {
+      set_err(err, PE_ERR_INVALID_ARGUMENT, "state belongs to another engine");
+      return PE_ERR_INVALID_ARGUMENT;
+    }
+    if (!plain_decisions(acts + seq_off[c], seq_off[c + 1] - seq_off[c])) {
+      set_err(err, PE_ERR_INVALID_ARGUMENT, "pe_eval_from_states: TILE / TILE_GROUP actions only");
+      return PE_ERR_INVALID_ARGUMENT;
+    }
+    if (p) {
+      flat.insert(flat.end(), p->path.begin(), p->path.end());
+      from[c] = (uint64_t)p->d_snap;
+      from_len[c] = (int32_t)p->path.size();
+    }
+    flat.insert(flat.end(), acts + seq_off[c], acts + seq_off[c + 1]);
+    flat.push_back(pe_action{0, 0, 0, PE_ACT_STOP, 0});
+    off.push_back((uint32_t)flat.size());
+  }
+  std::vector<uint8_t> saved;
+  std::vector<pe_result> res;
+  if (!call_begin(e, st, err)) return PE_ERR_CUDA;
+  if (!run_states(e, flat, off, from, from_len, save, saved, res, st, err)) return PE_ERR_CUDA;
+  if (!call_end(e, st, err)) return PE_ERR_CUDA;
+  std::copy(res.begin(), res.end(), out);
   return PE_OK;
 }
 
@@ -1969,6 +2333,8 @@ extern "C" pe_status pe_search(pe_engine* e, const pe_search_config* cfg, uint32
     return PE_ERR_INVALID_ARGUMENT;
   }
   const pe_search_config& c = cfg ? *cfg : e->cfg;
+  // incremental leaf evaluation: a leaf starts from its parent's saved state
+  if (e->pc_budget_gb == 0 && !e->d_pc) e->pc_budget_gb = 4.0;
   std::vector<pe_action> ords(e->n_ordinals + 1);
   for (uint32_t o = 0; o < e->n_ordinals; ++o) pe_engine_ordinal_action(e, o, &ords[o]);
   ords[e->n_ordinals] = pe_action{0, 0, 0, PE_ACT_STOP, 0};

@@ -235,6 +235,33 @@ class Engine:
         if rc != capi.PE_OK:
             raise Error(f"pe_engine_set_state_reuse failed rc={rc}")
 
+    def set_prefix_cache(self, budget_gb: float) -> None:
+        """Incremental leaf evaluation (pe.h pe_engine_set_prefix_cache)."""
+        rc = self.lib.pe_engine_set_prefix_cache(self.h, float(budget_gb))
+        if rc != capi.PE_OK:
+            raise Error(f"pe_engine_set_prefix_cache failed rc={rc}")
+
+    def prefix_cache_stats(self):
+        h, s, n = C.c_uint64(), C.c_uint64(), C.c_int64()
+        self.lib.pe_engine_prefix_cache_stats(self.h, C.byref(h), C.byref(s), C.byref(n))
+        return {"hits": h.value, "saved": s.value, "entries": n.value}
+
+    def state(self, seq) -> "State":
+        """A propagated state after `seq` (pe_state_create)."""
+        return State(self, seq)
+
+    def eval_from_states(self, parents, seqs):
+        """candidate c = parents[c] (State or None) + seqs[c] (pe_eval_from_states)."""
+        acts, off = capi.actions_array(seqs)
+        n = len(seqs)
+        ps = (C.c_void_p * max(1, n))(*[p.h if p is not None else None for p in parents])
+        out = (PeResult * n)()
+        err = PeError()
+        rc = self.lib.pe_eval_from_states(self.h, ps, acts, off, n, out, None, C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        return list(out)
+
     def graph_bytes(self) -> int:
         return int(self.lib.pe_engine_graph_bytes(self.h))
 
@@ -343,6 +370,49 @@ class Engine:
                                     C.byref(err))
         if rc != capi.PE_OK:
             _raise(rc, err)
+
+
+class State:
+    """A propagated partitioning state held on the device (pe.h pe_state):
+    the decisions, their evaluation, per-argument / result specs and the
+    stuck list (pe_state_specs)."""
+
+    def __init__(self, eng: Engine, seq):
+        self.eng = eng
+        self.lib = eng.lib
+        acts, _ = capi.actions_array([seq])
+        h = C.c_void_p()
+        err = PeError()
+        rc = self.lib.pe_state_create(eng.h, acts, len(seq), C.byref(h), C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        self.h = h
+        self.seq = list(seq)
+
+    def result(self) -> PeResult:
+        r = PeResult()
+        self.lib.pe_state_result(self.h, C.byref(r))
+        return r
+
+    def specs(self):
+        """(arg spec words, result spec word, [(op, reason)] stuck list)."""
+        A = self.eng.graph.n_args
+        args = (C.c_uint32 * max(1, A))()
+        res = C.c_uint32()
+        cap = 4 * (self.eng.graph.n_ops + 1)
+        stk = (C.c_int32 * (2 * cap))()
+        ns = C.c_uint32()
+        err = PeError()
+        rc = self.lib.pe_state_specs(self.h, args, C.byref(res), stk, cap, C.byref(ns), C.byref(err))
+        if rc != capi.PE_OK:
+            _raise(rc, err)
+        return list(args)[:A], res.value, [(stk[2 * i], stk[2 * i + 1]) for i in range(ns.value)]
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.lib.pe_state_destroy(h)
+            self.h = None
 
 
 def describe(r: PeResult) -> str:

@@ -181,7 +181,13 @@ def config_program(cfg: int) -> str:
     if cfg == 3:
         return build_transformer(24, mesh=(("batch", 4), ("model", 2)), name="gpt2_medium",
                                  **GPT2_MEDIUM)
-    if cfg == 4:  # 48-layer training step: 13,757 ops, 1,153 arguments
+    if cfg == 4:
+        # 48-layer training step at MHLO granularity with 4-way gradient
+        # accumulation: 52,154 ops, 1,156 arguments ("just over 50k
+        # operations, and 1150 arguments")
+        return build_training_step(48, mesh=(("batch", 4), ("model", 2)), detailed=True,
+                                   microbatches=4, **GPT2_MEDIUM)
+    if cfg == 40:  # the round-1 config-4 graph (coarser ops): 13,757 ops, 1,153 arguments
         return build_training_step(48, mesh=(("batch", 4), ("model", 2)), **GPT2_MEDIUM)
     raise ValueError(cfg)
 
@@ -205,6 +211,11 @@ class Tape:
         return out
 
     def const(self, value, shape):
+        if getattr(self, "scalar_consts", False):
+            # MHLO style (what a JAX-lowered graph contains): a scalar
+            # constant broadcast to the use's shape
+            c = self.b.const(value, [])
+            return self.b.op("broadcast_in_dim", [c], list(shape), {"map": "[]"})
         return self.b.const(value, shape)
 
     def ew(self, kind, *ins):
@@ -317,18 +328,31 @@ class Tape:
 
 
 def build_training_step(layers=48, batch=8, seq=1024, d_model=1024, heads=16, d_ff=4096,
-                        mesh=(("batch", 4), ("model", 2)), name="train_step") -> str:
+                        mesh=(("batch", 4), ("model", 2)), name="train_step",
+                        detailed=False, microbatches=1) -> str:
     """One training step of the head-split transformer (SURVEY.md §8(d)
     config 4: "hand-derived backward plus optimiser state"): forward as
     build_transformer with learned layer-norm gains, loss = sum of the
     output, reverse-mode gradients of every parameter, and an Adam update
     (first/second moments are arguments with the parameter's scope); the
-    function returns the sum of the updated parameters."""
+    function returns the sum of the updated parameters.
+
+    detailed=True is the graph at the granularity a JAX/MHLO lowering has
+    (a 24-layer GPT-3-style model with "just over 50k operations,
+    and 1150 arguments"): scalar constants broadcast to shape, attention
+    scaling and a max-subtracted softmax (the max under stop-gradient),
+    dropout multipliers, the tanh-approximated GELU, and an Adam update with
+    bias correction, decoupled weight decay and global-norm gradient
+    clipping.  Same 8 parameters per layer (+ two moments each).
+    microbatches=k: gradient accumulation over k data inputs x0..x{k-1}
+    (one loss; each parameter's per-microbatch gradients are summed)."""
     B, S, D, H, F = batch, seq, d_model, heads, d_ff
     Dh = D // H
     bld = ProgramBuilder(name, list(mesh))
     t = Tape(bld)
-    x = bld.arg("x", [B, S, D])
+    t.scalar_consts = detailed
+    xs = [bld.arg("x", [B, S, D])] if microbatches == 1 else \
+        [bld.arg(f"x{k}", [B, S, D]) for k in range(microbatches)]
     params = []
     for i in range(layers):
         for w, shp, sc in (("wq", [D, H, Dh], "attention/q_proj"), ("wk", [D, H, Dh], "attention/k_proj"),
@@ -351,34 +375,75 @@ def build_training_step(layers=48, batch=8, seq=1024, d_model=1024, heads=16, d_
         y = t.ew("mul", xc, t.bcast(rs, [B, S, D], [0, 1]))
         return t.ew("mul", y, t.bcast(gain, [B, S, D], [2]))
 
-    h = x
-    for i in range(layers):
-        P = lambda w: f"l{i}_{w}"  # noqa: E731
-        a = ln(h, P("g1"))
-        q = t.dot(a, P("wq"), [2], [0])
-        k = t.dot(a, P("wk"), [2], [0])
-        v = t.dot(a, P("wv"), [2], [0])
-        sc = t.dot(q, k, [3], [3], [0, 2], [0, 2])
-        e = t.ew("exp", sc)
-        z = t.bcast(t.reduce_sum(e, [3]), [B, H, S, S], [0, 1, 2])
-        pr = t.ew("div", e, z)
-        ctx = t.dot(pr, v, [3], [1], [0, 1], [0, 2])
-        att = t.dot(ctx, P("wo"), [1, 3], [0, 1])
-        r1 = t.ew("add", h, att)
-        m = ln(r1, P("g2"))
-        hh = t.ew("tanh", t.dot(m, P("w1"), [2], [0]))
-        h = t.ew("add", r1, t.dot(hh, P("w2"), [2], [0]))
-    loss = t.reduce_sum(h, [0, 1, 2])
+    def dropout(v):  # keep-probability multiplier (a splat mask)
+        return t.ew("mul", v, t.const(0.9, t.shape(v))) if detailed else v
+
+    def gelu(v):  # 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+        sh = t.shape(v)
+        x3 = t.ew("mul", t.ew("mul", v, v), v)
+        inner = t.ew("mul", t.ew("add", v, t.ew("mul", x3, t.const(0.044715, sh))),
+                     t.const(0.7978845608, sh))
+        return t.ew("mul", t.ew("mul", v, t.const(0.5, sh)),
+                    t.ew("add", t.const(1.0, sh), t.ew("tanh", inner)))
+
+    def forward(h):
+        for i in range(layers):
+            P = lambda w: f"l{i}_{w}"  # noqa: E731
+            a = ln(h, P("g1"))
+            q = t.dot(a, P("wq"), [2], [0])
+            k = t.dot(a, P("wk"), [2], [0])
+            v = t.dot(a, P("wv"), [2], [0])
+            if detailed:
+                q = t.ew("mul", q, t.const(Dh ** -0.5, t.shape(q)))
+            sc = t.dot(q, k, [3], [3], [0, 2], [0, 2])
+            if detailed:
+                # numerically stable softmax: the row max under stop-gradient
+                # (recorded outside the tape, so no gradient flows through it)
+                mx = bld.op("reduce_max", [sc], [B, H, S], {"dims": "[3]"})
+                mxb = bld.op("broadcast_in_dim", [mx], [B, H, S, S], {"map": "[0,1,2]"})
+                sc = t.ew("sub", sc, mxb)
+            e = t.ew("exp", sc)
+            z = t.bcast(t.reduce_sum(e, [3]), [B, H, S, S], [0, 1, 2])
+            pr = dropout(t.ew("div", e, z))
+            ctx = t.dot(pr, v, [3], [1], [0, 1], [0, 2])
+            att = dropout(t.dot(ctx, P("wo"), [1, 3], [0, 1]))
+            r1 = t.ew("add", h, att)
+            m = ln(r1, P("g2"))
+            u = t.dot(m, P("w1"), [2], [0])
+            hh = gelu(u) if detailed else t.ew("tanh", u)
+            h = t.ew("add", r1, dropout(t.dot(hh, P("w2"), [2], [0])))
+        return h
+
+
+    loss = None
+    for x in xs:
+        lk = t.reduce_sum(forward(x), [0, 1, 2])
+        loss = lk if loss is None else t.ew("add", loss, lk)
     g = t.grads(loss, params)
+    if detailed:
+        # global-norm clipping: scale = clip * rsqrt(sum of squared grads + eps)
+        norm2 = None
+        for p in params:
+            sq = t.reduce_sum(t.ew("mul", g[p], g[p]), list(range(len(bld.shapes[p]))))
+            norm2 = sq if norm2 is None else t.ew("add", norm2, sq)
+        scale = t.ew("mul", t.ew("rsqrt", t.ew("add", norm2, t.const(1e-6, []))), t.const(1.0, []))
     total = None
     for p in params:
         s = bld.shapes[p]
         m0, v0 = opt[p]
         gp = g[p]
+        if detailed:
+            gp = t.ew("mul", gp, t.bcast(scale, s, []))
         m1 = t.ew("add", t.ew("mul", m0, t.const(0.9, s)), t.ew("mul", gp, t.const(0.1, s)))
         v1 = t.ew("add", t.ew("mul", v0, t.const(0.999, s)),
                   t.ew("mul", t.ew("mul", gp, gp), t.const(0.001, s)))
-        upd = t.ew("mul", m1, t.ew("rsqrt", t.ew("add", v1, t.const(1e-8, s))))
+        if detailed:  # bias correction (step 1) and decoupled weight decay
+            mh = t.ew("div", m1, t.const(0.1, s))
+            vh = t.ew("div", v1, t.const(0.001, s))
+            upd = t.ew("add", t.ew("mul", mh, t.ew("rsqrt", t.ew("add", vh, t.const(1e-8, s)))),
+                       t.ew("mul", p, t.const(0.01, s)))
+        else:
+            upd = t.ew("mul", m1, t.ew("rsqrt", t.ew("add", v1, t.const(1e-8, s))))
         p1 = t.ew("sub", p, t.ew("mul", upd, t.const(1e-3, s)))
         red = t.reduce_sum(p1, list(range(len(s))))
         total = red if total is None else t.ew("add", total, red)

@@ -102,7 +102,7 @@ int harness_rollout_batch(const char* pir, size_t len, const pe_search_config* c
   for (uint32_t i = 0; i < n; ++i)
     (c.*ro)(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd, h.cp,
             h.baseline, acts_out + (size_t)i * maxd, n_out + i, out[i],
-            legal_out ? legal_out + (size_t)i * lw : nullptr, lw, nullptr, 0, nullptr, false);
+            legal_out ? legal_out + (size_t)i * lw : nullptr, lw, pe::Resume());
   return 0;
 }
 
@@ -155,8 +155,12 @@ int harness_resume_rollouts(const char* pir, size_t len, const pe_search_config*
     int32_t k = std::min<int32_t>(d, (int32_t)na);
     c2.rollout<false>(acts.data(), k, 0, k, h.cp, h.baseline, tmp.data(), &nt, r, nullptr, 0);
     c2.save(snap.data());
+    pe::Resume rs;
+    rs.snap = snap.data();
+    rs.done = rs.draws = k;
+    rs.path = acts.data();
     c.rollout<false>(nullptr, 0, seeds[i], maxd, h.cp, h.baseline, acts_out + (size_t)i * maxd,
-                     n_out + i, out[i], nullptr, 0, snap.data(), k, acts.data(), false);
+                     n_out + i, out[i], nullptr, 0, rs);
   }
   return 0;
 }
