@@ -374,6 +374,149 @@ def run_engine(args):
     return 0
 
 
+# ------------------------------------------------------------- search metric
+SEARCH_METRIC = "search time to Megatron plan"
+
+
+def _search_setup(layers=24):
+    from paper_2112_02958_b200 import capi, engine, modelgen
+    text = modelgen.config_program(3) if layers == 24 else modelgen.build_transformer(
+        layers, mesh=(("batch", 4), ("model", 2)), **modelgen.GPT2_MEDIUM)
+    g = engine.Graph(text)
+    model = g.axis_index("model")
+    # SURVEY.md §8(d) config 3 / DESIGN.md §5: model axis searched over the
+    # parameters (scope groups), the batch axis a manual decision, memory
+    # budget 0.6 x the replicated peak (the paper's regime)
+    cfg = capi.default_search_config(group_scopes=1, scoped_only=1, auto_axes_mask=1 << model)
+    return text, g, cfg, model
+
+
+def _search_config(args, leaf_batch, episodes_to_found):
+    return {"workload": "MCTS on gpt2-medium-24L [batch=4, model=2], model axis searched, "
+                        "grouped parameters, budget 0.6 x replicated peak",
+            "leaf_batch": leaf_batch, "seed": args.seed, "episodes_to_megatron": episodes_to_found,
+            "megatron": "48 all_reduce / 0 all_gather on the model axis"}
+
+
+def run_search(args):
+    """BASELINE.json metric #2: wall-clock of the deterministic MCTS until its
+    best plan carries the Megatron signature, on the GPU engine (pe_search;
+    root-parallel pe_search_multi over NCCL under torchrun), next to the same
+    search on the reference CPU path (oracle/_ref evaluating every leaf batch
+    on all host threads).  Time = a re-run with the episode budget that first
+    reached the plan (the search is deterministic per seed)."""
+    from paper_2112_02958_b200 import capi, engine, search
+    dist, rank, ws = _dist()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    text, g, cfg, model = _search_setup()
+    lb = args.leaf_batch
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        import helpers as H
+        cp = capi.default_cost_params()
+        cp.memory_budget_bytes = int(0.6 * H.oracle_info(text, cfg)["baseline_bytes"])
+        ords = search.ordinal_actions(g, cfg)
+        lw = (len(ords) - 1 + 63) // 64
+        threads = os.cpu_count() or 1
+
+        def ev(prefixes, seeds):
+            return H.rollout_batch("oracle", text, prefixes, seeds, cfg, cp=cp, legal_words=lw,
+                                   threads=threads)
+        t0 = time.perf_counter()
+        p = search.run_mcts(ev, len(ords) - 1, ords, episodes=args.search_episodes, seed=args.seed,
+                            leaf_batch=lb)
+        t_budget = time.perf_counter() - t0
+        ok = search.megatron_signature(p.result, model, 24)
+        budget = ((p.found_at_episode + lb) // lb) * lb
+        t0 = time.perf_counter()
+        search.run_mcts(ev, len(ords) - 1, ords, episodes=budget, seed=args.seed, leaf_batch=lb)
+        t = time.perf_counter() - t0
+        line = {"impl": "reference", "metric": SEARCH_METRIC, "value": t, "unit": "s",
+                "n_gpus": args.gpus, "steps": 1, "warmup": 0, "ms_per_step": 1e3 * t,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+                "dtype": "int64", "data": "synthetic",
+                "config": _search_config(args, lb, budget), "megatron_found": bool(ok),
+                "plan": search.plan_actions(p), "search_s_full_budget": t_budget,
+                "cpu_baseline": {"value": t, "unit": "s", "cores": threads, "kind": "reference",
+                                 "sample": f"the full search to the plan ({budget} episodes)"},
+                "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+    import torch
+    torch.cuda.set_device(local)
+    base = engine.Engine(g, device=local, cfg=cfg).baseline_bytes
+    cp = capi.default_cost_params()
+    cp.memory_budget_bytes = int(0.6 * base)
+    eng = engine.Engine(g, device=local, cfg=cfg, cost=cp)
+    comm = search.NcclComm(ws, rank, local, dist) if ws > 1 else None
+    launches0 = eng.launch_count()
+
+    def run(episodes, seed):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if comm is not None:
+            p = search.mcts_search_multi(eng, comm, episodes=episodes, seed=seed, leaf_batch=lb,
+                                         merge_every=args.merge_every)
+        else:
+            p = search.mcts_search(eng, episodes=episodes, seed=seed, leaf_batch=lb)
+        return p, _max_over_ranks(dist, time.perf_counter() - t0,
+                                  torch.device("cuda", local) if dist else None)
+
+    for w in range(args.warmup):  # warm-up searches (other seeds)
+        run(lb, 10_000 + w)
+    with ClockSampler(local) as clk:
+        plan, t_budget = run(args.search_episodes, args.seed)
+        ok = search.megatron_signature(plan.result, model, 24)
+        budget = ((plan.found_at_episode + lb) // lb) * lb
+        p2, t = run(budget, args.seed)
+    same = search.plan_actions(p2) == search.plan_actions(plan)
+    hits = eng.prefix_cache_stats()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and ws == 1:
+        import helpers as H
+        if os.path.exists(H.ORACLE_SO):
+            ords = search.ordinal_actions(g, cfg)
+            lw = (len(ords) - 1 + 63) // 64
+            threads = os.cpu_count() or 1
+
+            def ev(prefixes, seeds):
+                return H.rollout_batch("oracle", text, prefixes, seeds, cfg, cp=cp,
+                                       legal_words=lw, threads=threads)
+            t0 = time.perf_counter()
+            cp_plan = search.run_mcts(ev, len(ords) - 1, ords, episodes=budget, seed=args.seed,
+                                      leaf_batch=lb)
+            tc = time.perf_counter() - t0
+            cpu = {"value": tc, "unit": "s", "cores": threads, "kind": "reference",
+                   "sample": f"the same search ({budget} episodes, leaf batch {lb})",
+                   "plan_identical": search.plan_actions(cp_plan) == search.plan_actions(plan)}
+    if comm is not None:
+        comm.close()
+    if rank == 0:
+        line = {"metric": SEARCH_METRIC, "value": t, "unit": "s", "n_gpus": ws, "steps": 1,
+                "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+                "config": dict(_search_config(args, lb, budget),
+                               parallelism=f"root-parallel x{ws} (NCCL merge every "
+                                           f"{args.merge_every} episodes)" if ws > 1 else "1 tree"),
+                "megatron_found": bool(ok), "replay_identical": bool(same),
+                "plan": search.plan_actions(plan), "found_at_episode": plan.found_at_episode,
+                "search_s_full_budget": t_budget, "episodes_per_s_full_budget":
+                    args.search_episodes / t_budget,
+                "prefix_cache": hits, "gpu_launches": eng.launch_count() - launches0,
+                "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": None,
+                        "d2h_bytes_per_step": None,
+                        "note": "the search API is host-level: every leaf batch's prefixes and "
+                                "seeds go H2D and results D2H inside the timed search"},
+                "cpu_baseline": cpu, "clocks": clk.summary()}
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------- config 4 sweep
 def cpu_capped(text, cfg, cap_s, threads, seed0):
     """Reference CPU rollouts on `threads` host threads, each thread taking
@@ -513,7 +656,15 @@ def main():
                     help="config 4 sweep sizes (candidates per launch)")
     ap.add_argument("--cpu-cap-s", type=float, default=60.0,
                     help="config 4: per-thread cap of the reference CPU sample")
+    ap.add_argument("--metric", default="candidates", choices=["candidates", "search"],
+                    help="candidates: cand/s (headline); search: search time to the Megatron plan")
+    ap.add_argument("--leaf-batch", type=int, default=256)
+    ap.add_argument("--search-episodes", type=int, default=2048)
+    ap.add_argument("--merge-every", type=int, default=256)
+    ap.add_argument("--seed", type=int, default=0)
     args = ap.parse_args()
+    if args.metric == "search":
+        return run_search(args)
     if args.config == 4:
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "config 4 reference timing is the "

@@ -445,6 +445,23 @@ pe_status pe_search(pe_engine* e, const pe_search_config* cfg, uint32_t merge_ev
                     uint32_t rank, pe_merge_fn merge, void* merge_user, pe_plan* out,
                     pe_error* err);
 
+/* ---- root-parallel search over NCCL (SURVEY.md §8(b),(e)) ----
+ * One tree per GPU (seed + rank, rank = the communicator's); every
+ * merge_every episodes the root children's (N, W) int64 statistics are
+ * all-reduced (ncclAllReduce SUM on a device buffer), and at the end MAX
+ * reductions pick the best plan (ties -> lowest rank); every rank returns it.
+ * `comm` is an ncclComm_t (void* here so this header does not need nccl.h);
+ * NCCL is resolved at run time from the process (libnccl.so.2). */
+pe_status pe_search_multi(pe_engine* e, const pe_search_config* cfg, uint32_t merge_every,
+                          void* comm, pe_plan* out, pe_error* err);
+/* Helpers for callers without their own NCCL binding: ncclGetUniqueId (128
+ * bytes, to broadcast out of band), ncclCommInitRank on `device`, and
+ * ncclCommDestroy. */
+pe_status pe_nccl_unique_id(uint8_t* out128, pe_error* err);
+pe_status pe_nccl_comm_create(const uint8_t* id128, int32_t nranks, int32_t rank, int32_t device,
+                              void** comm, pe_error* err);
+void pe_nccl_comm_destroy(void* comm);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

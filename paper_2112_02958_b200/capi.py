@@ -203,6 +203,12 @@ SIGNATURES = {
     "pe_state_specs": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                  C.POINTER(C.c_int32), C.c_uint32, C.POINTER(C.c_uint32),
                                  C.POINTER(PeError)]),
+    "pe_search_multi": (C.c_int, [_P, C.POINTER(PeSearchConfig), C.c_uint32, _P,
+                                  C.POINTER(PePlan), C.POINTER(PeError)]),
+    "pe_nccl_unique_id": (C.c_int, [_P, C.POINTER(PeError)]),
+    "pe_nccl_comm_create": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_P),
+                                      C.POINTER(PeError)]),
+    "pe_nccl_comm_destroy": (None, [_P]),
     "pe_eval_from_states": (C.c_int, [_P, _P, _P, _P, C.c_uint32, _P, _P, C.POINTER(PeError)]),
     "pe_mcts_run": (C.c_int, [C.POINTER(PeMctsParams), ROLLOUT_FN, _P, MERGE_FN, _P, _P,
                               C.POINTER(PePlan), C.POINTER(PeError)]),

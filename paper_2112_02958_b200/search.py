@@ -76,6 +76,59 @@ def mcts_search(engine, episodes=500, seed=0, leaf_batch=256, uct_c=1.414, merge
     return plan
 
 
+class NcclComm:
+    """An NCCL communicator made by the engine library (pe_nccl_comm_create):
+    rank 0's unique id travels over `dist` (any torch.distributed backend),
+    or no exchange at all when nranks == 1."""
+
+    def __init__(self, nranks: int, rank: int, device: int, dist=None):
+        self.lib = capi.load()
+        uid = (C.c_uint8 * 128)()
+        err = PeError()
+        if rank == 0:
+            rc = self.lib.pe_nccl_unique_id(uid, C.byref(err))
+            if rc != capi.PE_OK:
+                raise RuntimeError(err.message.decode())
+        if nranks > 1:
+            import torch
+            t = torch.tensor(list(uid), dtype=torch.uint8)
+            if dist.get_backend() == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, 0)
+            for i, x in enumerate(t.cpu().tolist()):
+                uid[i] = x
+        h = C.c_void_p()
+        rc = self.lib.pe_nccl_comm_create(uid, nranks, rank, device, C.byref(h), C.byref(err))
+        if rc != capi.PE_OK:
+            raise RuntimeError(err.message.decode())
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.pe_nccl_comm_destroy(self.h)
+            self.h = None
+
+
+def mcts_search_multi(engine, comm: NcclComm, episodes=500, seed=0, leaf_batch=256, uct_c=1.414,
+                      merge_every=256) -> PePlan:
+    """Root-parallel mcts_search over NCCL (pe.h pe_search_multi): the root
+    statistics are all-reduced on the device every `merge_every` episodes."""
+    cfg = capi.PeSearchConfig()
+    C.memmove(C.byref(cfg), C.byref(engine.cfg), C.sizeof(cfg))
+    cfg.episodes = episodes
+    cfg.seed = seed
+    cfg.leaf_batch = leaf_batch
+    cfg.uct_c = uct_c
+    plan = PePlan()
+    err = PeError()
+    rc = engine.lib.pe_search_multi(engine.h, C.byref(cfg), merge_every, comm.h, C.byref(plan),
+                                    C.byref(err))
+    if rc != capi.PE_OK:
+        from .engine import _raise
+        _raise(rc, err)
+    return plan
+
+
 def run_mcts(evaluate, n_ordinals, ordinal_actions, episodes=500, seed=0, leaf_batch=256,
              uct_c=1.414, max_decisions=32, merge=None, merge_every=0, rank=0, lib=None) -> PePlan:
     """pe_mcts_run with a Python evaluator.  `evaluate(prefixes, seeds)`

@@ -75,8 +75,12 @@ def test_megatron_two_layer_and_reshape_hazard(oracle_lib, harness_lib):
 def test_training_step_graphs_match_oracle(oracle_lib, harness_lib):
     # config-4 family (forward + reverse-mode gradients + Adam) at toy size:
     # rollouts, legal sets and full SPMD traces identical
-    for layers, mesh in ((1, (("m", 2),)), (2, (("batch", 2), ("model", 2)))):
-        text = modelgen.build_training_step(layers, mesh=mesh, **modelgen.TOY)
+    # (the last two: config 4's own generator -- MHLO-granularity ops,
+    # stable softmax, GELU, dropout, clipped Adam, gradient accumulation)
+    for layers, mesh, kw in ((1, (("m", 2),), {}), (2, (("batch", 2), ("model", 2)), {}),
+                             (1, (("m", 2),), dict(detailed=True, microbatches=2)),
+                             (1, (("batch", 2), ("model", 2)), dict(detailed=True, microbatches=2))):
+        text = modelgen.build_training_step(layers, mesh=mesh, **kw, **modelgen.TOY)
         cfg = capi.default_search_config(group_scopes=0)
         lw = (H.oracle_info(text, cfg)["n_ordinals"] + 63) // 64
         n = 60

@@ -244,11 +244,15 @@ def test_infer_rest_device_vs_reference(oracle_lib, cfgno):
         assert not H.compare_results(a, b)
 
 
-def test_training_step_device_vs_oracle(oracle_lib):
-    text = modelgen.build_training_step(2, mesh=(("batch", 2), ("model", 2)), **modelgen.TOY)
-    cfg = capi.default_search_config(group_scopes=0)
+@pytest.mark.parametrize("detailed,group", [(False, 0), (True, 0), (True, 1)])
+def test_training_step_device_vs_oracle(oracle_lib, detailed, group):
+    # the config-4 generator at toy size (detailed: MHLO granularity with
+    # 4-way gradient accumulation, as config 4 itself)
+    kw = dict(detailed=True, microbatches=4) if detailed else {}
+    n = 128 if detailed else 256
+    text = modelgen.build_training_step(2, mesh=(("batch", 2), ("model", 2)), **kw, **modelgen.TOY)
+    cfg = capi.default_search_config(group_scopes=group)
     eng = _engine(text, cfg)
-    n = 256
     res, seqs, legal = eng.rollout_batch([[]] * n, list(range(n)), legal=True)
     ref, rseqs, rlegal = H.rollout_batch("oracle", text, [[]] * n, list(range(n)), cfg,
                                          legal_words=eng.legal_words, threads=os.cpu_count() or 1)
@@ -283,11 +287,11 @@ def test_calibrated_arena_preserves_results(oracle_lib, monkeypatch):
 
 
 def test_config4_training_step_runs():
-    # config 4 at full size (48 layers, 13,757 ops, 1,153 arguments): every
+    # config 4 at full size (48 layers, 52,154 ops, 1,156 arguments): every
     # rollout evaluates (tight arena or retry), no failures
     text = modelgen.config_program(4)
     eng = _engine(text, capi.default_search_config(group_scopes=1))
-    assert eng.graph.n_ops == 13757 and eng.graph.n_args == 1153
+    assert eng.graph.n_ops == 52154 and eng.graph.n_args == 1156
     res, seqs, _ = eng.rollout_batch([[]] * 256, list(range(256)))
     assert all(r.status == 0 for r in res)
     assert all(r.n_spmd_ops >= eng.graph.n_ops for r in res)

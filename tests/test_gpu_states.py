@@ -56,9 +56,8 @@ def test_parent_plus_one_action_equals_full_replay(oracle_lib, cfgno):
 @pytest.mark.parametrize("tight", [None, "8"])
 def test_prefix_cache_preserves_rollouts(oracle_lib, monkeypatch, tight):
     # MCTS-like traffic: prefixes growing one action at a time; the cached
-    # engine starts each from its longest cached prefix.  With the tight
-    # arena forced to overflow (retry path) nothing is cached and results
-    # still match.
+    # engine starts each from its longest cached prefix, also when the tight
+    # arena is forced to overflow and candidates take the retry path.
     if tight:
         monkeypatch.setenv("PE_DEBUG_TIGHT_EM_CAP", tight)
     text = modelgen.config_program(2)
@@ -75,8 +74,7 @@ def test_prefix_cache_preserves_rollouts(oracle_lib, monkeypatch, tight):
         r2, s2, l2 = plain.rollout_batch(prefixes, seeds, legal=True)
         assert s1 == s2 and l1 == l2
         assert all(not H.compare_results(a, b) for a, b in zip(r1, r2))
+    # (with the SPMD-op cap forced down, lowering overflows after the prefix
+    # state was saved: the retry path re-evaluates from the untiled graph)
     stats = cached.prefix_cache_stats()
-    if tight:
-        assert stats["saved"] == 0
-    else:
-        assert stats["hits"] > 0 and stats["saved"] > 0
+    assert stats["hits"] > 0 and stats["saved"] > 0

@@ -9,6 +9,6 @@ while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
     -Xcompiler -fPIC --expt-relaxed-constexpr $flags -shared -I "$ROOT/include" -I "$C" \
-    "$C/pe_engine.cu" "$C/pe_graph.cc" "$C/pe_pir.cc" "$C/pe_search.cc" -o "$ROOT/variants/$name.so" &
+    "$C/pe_engine.cu" "$C/pe_graph.cc" "$C/pe_pir.cc" "$C/pe_search.cc" "$C/pe_nccl.cc" -ldl -o "$ROOT/variants/$name.so" &
 done
 wait
