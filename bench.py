@@ -603,6 +603,49 @@ def run_sweep(args):
                          "mean_spmd_ops": float(f("n_spmd_ops").mean())})
             print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
     top = rows[-1]
+    # second variant: MCTS leaf evaluation = a
+    # parent state + 1 action.  Parents: 2-decision prefixes of the last
+    # batch's rollouts, held as pe_state handles; candidates: every legal
+    # action of every parent, evaluated from the parent's state
+    # (pe_eval_from_states) and, for comparison, by full replay from the
+    # untiled graph (pe_eval_batch); the two must agree bit-for-bit.
+    import numpy as np
+    a_host = acts.view(sizes[-1], maxd, 8).cpu().numpy()
+    n_host = na.cpu().numpy()
+    parents, seen = [], set()
+    for i in range(sizes[-1]):
+        if n_host[i] >= 3:
+            v = a_host[i].view(np.uint32)[:, 0]
+            pre = tuple((int(v[k]), int(a_host[i, k, 4]), int(a_host[i, k, 5]), int(a_host[i, k, 6]))
+                        for k in range(2))
+            if pre not in seen:
+                seen.add(pre)
+                parents.append(list(pre))
+        if len(parents) >= args.p1_parents:
+            break
+    cands_p, cands_a = [], []
+    for pre in parents:
+        st = eng.state(pre)
+        _, _, legal = eng.rollout_batch([pre + [(0, 0, 0, capi.PE_ACT_STOP)]], [0], legal=True)
+        for o in range(eng.n_ordinals):
+            if (legal[0][o // 64] >> (o % 64)) & 1:
+                a = eng.ordinal_action(o)
+                cands_p.append(st)
+                cands_a.append([(a.value, a.dim, a.axis, a.kind)])
+    eng.eval_from_states(cands_p[:64], cands_a[:64])  # warm-up
+    t0 = time.perf_counter()
+    inc = eng.eval_from_states(cands_p, cands_a)
+    t_inc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    full = eng.eval_batch([p.seq + a for p, a in zip(cands_p, cands_a)])
+    t_full = time.perf_counter() - t0
+    import helpers as H
+    p1 = {"parents": len(parents), "candidates": len(cands_a),
+          "cand_per_s_from_parent_state": len(cands_a) / t_inc,
+          "cand_per_s_full_replay": len(cands_a) / t_full,
+          "mismatches_vs_full_replay": sum(1 for x, y in zip(inc, full) if H.compare_results(x, y)),
+          "timing": "host C-ABI calls (pe_eval_from_states / pe_eval_batch), copies included"}
+    print(json.dumps(p1), file=sys.stderr, flush=True)
     # e2e: host buffers through the C-ABI at the largest size (copies timed)
     B = sizes[-1]
     t0 = time.perf_counter()
@@ -628,7 +671,7 @@ def run_sweep(args):
                        "graph_ops": g.n_ops, "graph_args": g.n_args, "sizes": sizes,
                        "arena_bytes": eng.arena_bytes(), "slots": eng.slots(),
                        "l2": "256 MB flush before every launch"},
-            "sweep": rows,
+            "sweep": rows, "parent_plus_one": p1,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * 8 + (B + 1) * 4,
                     "d2h_bytes_per_step": B * (maxd * 8 + 4 + C.sizeof(capi.PeResult))},
             "roofline": {"bound": "hbm", "achieved": top["cand_per_s"] * b_cand / 1e9, "peak": peak,
@@ -654,6 +697,8 @@ def main():
                     help="3: the headline (GPT-2-medium 24L rollouts); 4: the 1K..1M sweep")
     ap.add_argument("--sizes", default="1024,4096,16384,65536",
                     help="config 4 sweep sizes (candidates per launch)")
+    ap.add_argument("--p1-parents", type=int, default=64,
+                    help="config 4: parent states of the parent + 1 action variant")
     ap.add_argument("--cpu-cap-s", type=float, default=60.0,
                     help="config 4: per-thread cap of the reference CPU sample")
     ap.add_argument("--metric", default="candidates", choices=["candidates", "search"],

@@ -666,7 +666,7 @@ void oracle_default_search_config(pe_search_config* out) {
   out->episodes = 500;
   out->seed = 0;
   out->uct_c = 1.414;
-  out->leaf_batch = 256;
+  out->leaf_batch = 8192;
 }
 
 // Evaluate explicit action sequences.  Returns 0 on success, else an error

@@ -140,7 +140,7 @@ def default_cost_params() -> PeCostParams:
 
 
 def default_search_config(**kw) -> PeSearchConfig:
-    c = PeSearchConfig(0xFFFFFFFF, 32, 1, 500, 0, 1.414, 256, 0, 0, None, 0, 0)
+    c = PeSearchConfig(0xFFFFFFFF, 32, 1, 500, 0, 1.414, 8192, 0, 0, None, 0, 0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c

@@ -532,7 +532,7 @@ void pe_default_search_config(pe_search_config* out) {
   out->episodes = 500;
   out->seed = 0;
   out->uct_c = 1.414;
-  out->leaf_batch = 256;
+  out->leaf_batch = 8192;  // one launch fills the GPU; DESIGN.md §5 (time-to-plan table)
 }
 
 // ------------------------------------------------------------------ graph
@@ -2342,7 +2342,7 @@ extern "C" pe_status pe_search(pe_engine* e, const pe_search_config* cfg, uint32
   p.n_ordinals = e->n_ordinals;
   p.max_decisions = e->cfg.max_decisions;  // the rollout kernel's cap
   p.episodes = c.episodes;
-  p.leaf_batch = c.leaf_batch ? c.leaf_batch : 256;
+  p.leaf_batch = c.leaf_batch ? c.leaf_batch : 8192;
   p.merge_every = merge_every;
   p.rank = rank;
   p.seed = c.seed;

@@ -57,7 +57,7 @@ def _null_merge():
     return C.cast(None, capi.MERGE_FN)
 
 
-def mcts_search(engine, episodes=500, seed=0, leaf_batch=256, uct_c=1.414, merge=None,
+def mcts_search(engine, episodes=500, seed=0, leaf_batch=8192, uct_c=1.414, merge=None,
                 merge_every=0, rank=0) -> PePlan:
     cfg = capi.PeSearchConfig()
     C.memmove(C.byref(cfg), C.byref(engine.cfg), C.sizeof(cfg))
@@ -109,7 +109,7 @@ class NcclComm:
             self.h = None
 
 
-def mcts_search_multi(engine, comm: NcclComm, episodes=500, seed=0, leaf_batch=256, uct_c=1.414,
+def mcts_search_multi(engine, comm: NcclComm, episodes=500, seed=0, leaf_batch=8192, uct_c=1.414,
                       merge_every=256) -> PePlan:
     """Root-parallel mcts_search over NCCL (pe.h pe_search_multi): the root
     statistics are all-reduced on the device every `merge_every` episodes."""

@@ -68,3 +68,29 @@ def test_bench_launch_shape_equals_single_wave_and_oracle(oracle_lib, cfgno, n_o
     mism = [i for i, k in enumerate(idx)
             if H.compare_results(capi.PeResult.from_buffer_copy(r_full[k].tobytes()), ref[i])]
     assert not mism, mism[:8]
+
+
+def test_config4_multi_wave_launch_equals_single_wave():
+    # config 4 (52,154 ops) is slot-limited by its arena: a launch of
+    # 2 x slots + 37 candidates runs second and third waves through the work
+    # counter; every candidate equals its evaluation in launches of at most
+    # one wave.  (The reference CPU path needs well over 30 minutes per
+    # candidate here -- profiles/r2_cfg4_cpu_baseline.json -- so the oracle
+    # parity of this generator is checked at toy size in test_gpu_parity.py
+    # and tests/test_core_fuzz.py.)
+    text = modelgen.config_program(4)
+    cfg = capi.default_search_config(group_scopes=1)
+    eng = engine.Engine(engine.Graph(text), device=0, cfg=cfg)
+    slots = eng.slots()
+    n = 2 * slots + 37
+    seeds = np.arange(n, dtype=np.uint64) + np.uint64(77_000)
+    r_full, a_full, n_full = eng.rollout_roots_np(seeds)
+    wave = min(slots, 4096)
+    parts = [eng.rollout_roots_np(seeds[i:i + wave]) for i in range(0, n, wave)]
+    r_w = np.concatenate([p[0] for p in parts])
+    a_w = np.concatenate([p[1] for p in parts])
+    n_w = np.concatenate([p[2] for p in parts])
+    bad = _rows_equal(r_full, a_full, n_full, r_w, a_w, n_w)
+    assert bad.size == 0, (bad.size, bad[:8])
+    st_off = capi.PeResult.status.offset // 4
+    assert (r_full.view(np.int32)[:, st_off] == 0).all()
