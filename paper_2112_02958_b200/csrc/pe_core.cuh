@@ -313,6 +313,14 @@ struct Pull {
 // entry k0 on and `draws` RNG draws already consumed; the state after the
 // whole prefix may be saved for later candidates (prefix-state cache,
 // pe_state handles).
+// Rollout features compiled into a kernel instantiation (the hot kernel's
+// code size and register allocation bound its speed; the
+// default launch carries neither): kFInferRest = InferRest actions / pauses,
+// kFResume = start from / save saved states.
+constexpr int kFInferRest = 1;
+constexpr int kFResume = 2;
+constexpr int kFAll = kFInferRest | kFResume;
+
 struct Resume {
   const uint8_t* snap = nullptr;
   int32_t done = 0;
@@ -1829,7 +1837,7 @@ struct Cand {
   // launches the RS instantiation only when the worklist asks for it, so
   // the default kernel carries none of its code (code size bounds this
   // kernel: instruction-cache stalls).
-  template <bool RS>
+  template <bool RS, int F = kFAll>
   //
   // rs: start from a saved state instead of init() and
   // replaying the decisions it covers -- the scheduling trie's states of
@@ -1844,7 +1852,8 @@ struct Cand {
     tick_start();
     int32_t steps = 0, nacts = 0;
     bool propagated = false, terminal = false;
-    if (rs.snap) {
+    constexpr bool IR = (F & kFInferRest) != 0, RES = (F & kFResume) != 0;
+    if (RES && rs.snap) {
       load(rs.snap);
       for (int32_t k = 0; k < rs.done && k < maxd; ++k) acts_out[k] = rs.path[k];
       steps = nacts = rs.done;
@@ -1864,7 +1873,7 @@ struct Cand {
     // before enumerating legal actions -- i.e. after every whole decision,
     // as the oracle does after each apply_action
     bool rs_due = false;
-    for (int32_t k = bad() ? np : rs.k0; k < np; ++k) {
+    for (int32_t k = RES ? (bad() ? np : rs.k0) : 0; k < np; ++k) {
       if (RS && rs_due && !(prefix[k].pad & PE_ACT_FLAG_INFERRED)) {
         resurface_update();
         rs_due = false;
@@ -1876,7 +1885,7 @@ struct Cand {
       }
       if (prefix[k].kind == PE_ACT_INFER_REST) {  // expanded by the host
         if (!(prefix[k].pad & PE_ACT_FLAG_EXPANDED)) {
-          if (g.ir_pause) {
+          if (IR && g.ir_pause) {
             pause(r, acts_out, nacts, maxd, steps, k, 0);
             *n_out = (uint32_t)(nacts < maxd ? nacts : maxd);
             return;
@@ -1913,7 +1922,7 @@ struct Cand {
       }
     }
     if (RS && rs_due && !bad() && status == PE_CAND_OK) resurface_update();
-    if (rs.save && !bad() && status == PE_CAND_OK) {
+    if (RES && rs.save && !bad() && status == PE_CAND_OK) {
       save(rs.save);
       if (rs.saved) *rs.saved = 1;
     }
@@ -1921,24 +1930,24 @@ struct Cand {
       if (legal_out) {
         int32_t nl = build_legal<RS>();
         for (int32_t i = 0; i < nl; ++i) legal_out[a.lg()[i] >> 6] |= 1ull << (a.lg()[i] & 63);
-        if (g.ir_ord >= 0 && infer_rest_legal())
+        if (IR && g.ir_ord >= 0 && infer_rest_legal())
           legal_out[g.ir_ord >> 6] |= 1ull << (g.ir_ord & 63);
       }
       // (each decision draws once: splitmix adds the golden gamma per draw)
-      uint64_t st = seed + (uint64_t)rs.draws * 0x9E3779B97F4A7C15ull;
-      int32_t draws = rs.draws;
+      uint64_t st = seed + (RES ? (uint64_t)rs.draws * 0x9E3779B97F4A7C15ull : 0);
+      int32_t draws = RES ? rs.draws : 0;
       while (!terminal) {
         if (steps >= maxd) break;
         tick(4);
         int32_t nl = build_legal<RS>();
         // InferRest follows the TileValue actions (SPEC legal_actions order)
-        int32_t ir = g.ir_ord >= 0 && infer_rest_legal() ? 1 : 0;
+        int32_t ir = IR && g.ir_ord >= 0 && infer_rest_legal() ? 1 : 0;
         if (nl + ir == 0) break;
         uint64_t ws = steps >= 1 ? 2 : 1;
         uint64_t pick = splitmix(st) % ((uint64_t)(nl + ir) + ws);
         ++draws;
         if (pick >= (uint64_t)(nl + ir)) break;
-        if (pick == (uint64_t)nl) {
+        if (IR && pick == (uint64_t)nl) {
           pause(r, acts_out, nacts, maxd, steps, -1, draws);
           *n_out = (uint32_t)(nacts < maxd ? nacts : maxd);
           return;

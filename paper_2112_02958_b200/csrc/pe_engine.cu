@@ -239,7 +239,7 @@ struct CacheView {
   uint8_t* saved = nullptr;
 };
 
-template <bool RETRY, bool RS>
+template <bool RETRY, bool RS, int F>
 __global__ void __launch_bounds__(kSmBlock, 1)
 pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ pe::Layout L,
                   uint8_t* arena, uint32_t slots,
@@ -267,7 +267,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
     // start from a saved state: the candidate's trie node's, or its longest
     // cached prefix's
     pe::Resume rs;
-    if (sv.keys) {
+    if ((F & pe::kFResume) && sv.keys) {
       uint32_t key = sv.keys[i], node = key / sv.kstride;
       int4 nd = sv.tnode[node];
       if (nd.w >= 0) {
@@ -277,7 +277,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
         rs.stop = key % sv.kstride == 0;  // its next draw is Stop
       }
     }
-    if (cv.from) {
+    if ((F & pe::kFResume) && cv.from) {
       if (cv.from[i]) {
         rs.snap = reinterpret_cast<const uint8_t*>(cv.from[i]);
         rs.done = rs.k0 = cv.from_len[i];
@@ -292,7 +292,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
     unsigned long long t_begin = gtimer();
 #endif
     pe_result r;
-    c.template rollout<RS>(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd,
+    c.template rollout<RS, F>(prefix + poff[i], (int32_t)(poff[i + 1] - poff[i]), seeds[i], maxd,
                            cp, baseline, acts_out + (uint64_t)i * maxd, n_out + i, r,
                            legal_out ? legal_out + (uint64_t)i * legal_words : nullptr,
                            legal_words, rs);
@@ -356,7 +356,7 @@ pe_calib_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
   for (uint32_t k = slot; k < n; k += slots) {
     pe_result r;
-    c.template rollout<false>(nullptr, 0, 0x5EEDull * (k + 1), maxd, cp, 1,
+    c.template rollout<false, 0>(nullptr, 0, 0x5EEDull * (k + 1), maxd, cp, 1,
                               acts + (uint64_t)k * maxd, n_out + k, r, nullptr, 0);
     atomicMax(&hw[0], c.nslots);
     atomicMax(&hw[1], c.nloops);
@@ -381,7 +381,7 @@ pe_probe_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__
   for (uint32_t k = slot; k < n; k += slots) {
     int32_t np = (int32_t)(poff[k + 1] - poff[k]);
     pe_result r;
-    c.template rollout<false>(prefix + poff[k], np, 0, np, cp, baseline,
+    c.template rollout<false, 0>(prefix + poff[k], np, 0, np, cp, baseline,
                               acts_out + (uint64_t)k * acts_stride, n_out + k, r,
                               legal_out + (uint64_t)k * legal_words, legal_words);
     out[k] = r;
@@ -1201,7 +1201,7 @@ bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefix
         (uint64_t*)buf[6], lw, e->d_snap, e->snap_stride, (int32_t*)buf[7]);
     // overflowed probes: legal sets from full-size arenas (no snapshot); the
     // uniform maxd only adds draws after the prefix, its legal set is final
-    pe_rollout_kernel<true, false><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+    pe_rollout_kernel<true, false, 0><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
         e->dview, e->big_layout, e->d_big_arena, bs, (const pe_action*)buf[0],
         (const uint32_t*)buf[1], (const uint64_t*)buf[2], n, maxd, e->cp, e->baseline,
         (pe_action*)buf[3], (uint32_t*)buf[4], (pe_result*)buf[5], (uint64_t*)buf[6], lw,
@@ -1470,9 +1470,26 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
                                       CacheView(), max_acts);
     return cudaGetLastError();
   };
-  cudaError_t lerr = e->wl.resurface
-                         ? launch(pe_rollout_kernel<false, true>, pe_rollout_kernel<true, true>)
-                         : launch(pe_rollout_kernel<false, false>, pe_rollout_kernel<true, false>);
+  // the instantiation with only the features this launch needs (the
+  // default -- root rollouts, no InferRest, no saved states -- has none);
+  // resurfacing engines never use saved states
+  const bool ir = gv.ir_ord >= 0 || gv.ir_pause;
+  const bool res = (sv.keys && sv.snap) || cv.from;
+  cudaError_t lerr;
+  if (e->wl.resurface)
+    lerr = ir ? launch(pe_rollout_kernel<false, true, pe::kFInferRest>,
+                       pe_rollout_kernel<true, true, pe::kFInferRest>)
+              : launch(pe_rollout_kernel<false, true, 0>, pe_rollout_kernel<true, true, 0>);
+  else if (ir && res)
+    lerr = launch(pe_rollout_kernel<false, false, pe::kFAll>,
+                  pe_rollout_kernel<true, false, pe::kFInferRest>);
+  else if (ir)
+    lerr = launch(pe_rollout_kernel<false, false, pe::kFInferRest>,
+                  pe_rollout_kernel<true, false, pe::kFInferRest>);
+  else if (res)
+    lerr = launch(pe_rollout_kernel<false, false, pe::kFResume>, pe_rollout_kernel<true, false, 0>);
+  else
+    lerr = launch(pe_rollout_kernel<false, false, 0>, pe_rollout_kernel<true, false, 0>);
   e->launches += 2;
   return lerr;
 }
