@@ -113,12 +113,12 @@ struct Layout {
   // are interleaved [index][lane] at record granularity
   uint64_t vrec, lrec, arec, looprec, emrec;
   uint64_t rs, rsb;
-  uint64_t opnd, fs, stk, seen, em_opnd, carry, lg, dirty;
+  uint64_t opnd, fs, stk, seen, em_opnd, em_spec, carry, lg, dirty, st8, st4;
+  uint32_t has_opnd;  // the SPMD operand log (parity traces) is allocated
   uint64_t bytes;  // one group arena
 };
 
-constexpr int kRec = 32;    // VRec, LowRec, LoopRec
-constexpr int kRec64 = 64;  // ArgRec, EmRec
+constexpr int kRec = 32;    // VRec, LowRec, LoopRec, ArgRec, EmRec
 
 // A lane's view of its group arena: lane-adjusted base pointers (one per
 // record / element size) and the layout's offsets, which live in the kernel
@@ -127,13 +127,15 @@ constexpr int kRec64 = 64;  // ArgRec, EmRec
 //                12 uses 16 slcnt 20 bnext 24 bprev 28 vpos
 //   LowRec [V]   0 buf 4 spec 8 acq 16 g[4]            (REF spmd.cc:42 Lowered)
 //   ArgRec [A]   0 direct-in-loop 4 slice demand 8 atomic 12 SPMD arg spec
-//                16 arg local bytes 24/32/40 final registered gb/lb/spec
+//                16 arg local bytes 24 final registered spec (trace)
 //   LoopRec[L]   0 kind 1 axis 2 dim 4 head 8 tail 12 yield 16 result type
 //   EmRec  [EM]  0 head 4 first operand 8 last use 12 operand offset
-//                16 local bytes 24 liveness delta 32/40/48 final gb/lb/spec
+//                16 local bytes 24 liveness delta
+//   flat         collective_stats accumulators: st8 = all_reduce / all_gather
+//                bytes per axis, st4 = their counts + slice_by_coord counts
 struct Arena {
   const struct Layout* L;
-  uint8_t *b1, *b4, *r32, *r64;
+  uint8_t *b1, *b4, *b8, *r32;
 #define PE_REC(name, T, base, arr, off, STRIDE) \
   PE_HD Field<T, STRIDE> name() const { return {base + L->arr + (off)}; }
   PE_REC(vk, uint8_t, r32, vrec, 0, kLanes * kRec)
@@ -152,15 +154,13 @@ struct Arena {
   PE_REC(lo_acq, uint32_t, r32, lrec, 8, kLanes * kRec)
   PE_REC(lo_g, G4, r32, lrec, 16, kLanes * kRec)
   PE_REC(lo_h, LowHead, r32, lrec, 0, kLanes * kRec)
-  PE_REC(adirect, int32_t, r64, arec, 0, kLanes * kRec64)
-  PE_REC(aslice, int32_t, r64, arec, 4, kLanes * kRec64)
-  PE_REC(awrapped, uint8_t, r64, arec, 8, kLanes * kRec64)
-  PE_REC(aspec0, uint32_t, r64, arec, 12, kLanes * kRec64)
-  PE_REC(alb0, int64_t, r64, arec, 16, kLanes * kRec64)
-  PE_REC(arg_gb, int64_t, r64, arec, 24, kLanes * kRec64)
-  PE_REC(arg_lb, int64_t, r64, arec, 32, kLanes * kRec64)
-  PE_REC(arg_spec, uint32_t, r64, arec, 40, kLanes * kRec64)
-  PE_REC(ar0, V4, r64, arec, 0, kLanes * kRec64)
+  PE_REC(adirect, int32_t, r32, arec, 0, kLanes * kRec)
+  PE_REC(aslice, int32_t, r32, arec, 4, kLanes * kRec)
+  PE_REC(awrapped, uint8_t, r32, arec, 8, kLanes * kRec)
+  PE_REC(aspec0, uint32_t, r32, arec, 12, kLanes * kRec)
+  PE_REC(alb0, int64_t, r32, arec, 16, kLanes * kRec)
+  PE_REC(arg_spec, uint32_t, r32, arec, 24, kLanes * kRec)
+  PE_REC(ar0, V4, r32, arec, 0, kLanes * kRec)
   PE_REC(lkind, uint8_t, r32, looprec, 0, kLanes * kRec)
   PE_REC(laxis, uint8_t, r32, looprec, 1, kLanes * kRec)
   PE_REC(ldim, int8_t, r32, looprec, 2, kLanes * kRec)
@@ -170,19 +170,17 @@ struct Arena {
   PE_REC(ltype, int32_t, r32, looprec, 16, kLanes * kRec)
   PE_REC(lq0, V4, r32, looprec, 0, kLanes * kRec)   // kind|axis|dim, head, tail, yield
   PE_REC(lq1, V4, r32, looprec, 16, kLanes * kRec)  // result type
-  PE_REC(em_head, int32_t, r64, emrec, 0, kLanes * kRec64)
-  PE_REC(em_op0, int32_t, r64, emrec, 4, kLanes * kRec64)
-  PE_REC(em_last, int32_t, r64, emrec, 8, kLanes * kRec64)
-  PE_REC(em_ooff, int32_t, r64, emrec, 12, kLanes * kRec64)
-  PE_REC(em_lb, int64_t, r64, emrec, 16, kLanes * kRec64)
-  PE_REC(delta, int64_t, r64, emrec, 24, kLanes * kRec64)
-  PE_REC(em_gb, int64_t, r64, emrec, 32, kLanes * kRec64)
-  PE_REC(em_blb, int64_t, r64, emrec, 40, kLanes * kRec64)
-  PE_REC(em_spec, uint32_t, r64, emrec, 48, kLanes * kRec64)
-  PE_REC(em_q0, V4, r64, emrec, 0, kLanes * kRec64)      // head op0 last ooff
-  PE_REC(em_q1, I64x2, r64, emrec, 16, kLanes * kRec64)  // local bytes, delta
-  PE_REC(em_q2, I64x2, r64, emrec, 32, kLanes * kRec64)  // final gb, lb
-  PE_REC(em_q3, V4, r64, emrec, 48, kLanes * kRec64)     // final spec
+  PE_REC(em_head, int32_t, r32, emrec, 0, kLanes * kRec)
+  PE_REC(em_op0, int32_t, r32, emrec, 4, kLanes * kRec)
+  PE_REC(em_last, int32_t, r32, emrec, 8, kLanes * kRec)
+  PE_REC(em_ooff, int32_t, r32, emrec, 12, kLanes * kRec)
+  PE_REC(em_lb, int64_t, r32, emrec, 16, kLanes * kRec)
+  PE_REC(delta, int64_t, r32, emrec, 24, kLanes * kRec)
+  PE_REC(em_q0, V4, r32, emrec, 0, kLanes * kRec)      // head op0 last ooff
+  PE_REC(em_q1, I64x2, r32, emrec, 16, kLanes * kRec)  // local bytes, delta
+  PE_REC(em_spec, uint32_t, b4, em_spec, 0, kLanes * 4)  // final registered spec (trace)
+  PE_REC(st8, int64_t, b8, st8, 0, kLanes * 8)
+  PE_REC(st4, int32_t, b4, st4, 0, kLanes * 4)
   PE_REC(opnd, int32_t, b4, opnd, 0, kLanes * 4)
   PE_REC(fs, int32_t, b4, fs, 0, kLanes * 4)
   PE_REC(stk, int32_t, b4, stk, 0, kLanes * 4)
@@ -205,7 +203,7 @@ PE_HD int32_t pe_ctz(uint32_t x) { return __builtin_ctz(x); }
 PE_HD uint64_t align8(uint64_t x) { return (x + 7) & ~uint64_t(7); }
 PE_HD uint64_t align128(uint64_t x) { return (x + 127) & ~uint64_t(127); }
 
-inline Layout relayout(const GraphView& g, const Caps& caps);
+inline Layout relayout(const GraphView& g, const Caps& caps, bool opnd_log);
 
 // Host-side sizing.  The FULL layout's bounds are
 // structural: every original op is pulled or migrated at most once, every
@@ -232,13 +230,16 @@ inline Layout make_layout(const GraphView& g, bool tight = false) {
     L.caps.EM = 3 * (N + S) + 2 * L.caps.L + A + 64;
     L.caps.EO = E + 2 * L.caps.EM + 64;
   }
-  return relayout(g, L.caps);
+  // (only the full-size arenas keep the SPMD operand log: parity traces run
+  // in them)
+  return relayout(g, L.caps, !tight);
 }
 
 // Byte offsets of every array of a group arena for the given capacities.
-inline Layout relayout(const GraphView& g, const Caps& caps) {
+inline Layout relayout(const GraphView& g, const Caps& caps, bool opnd_log) {
   Layout L{};
   L.caps = caps;
+  L.has_opnd = opnd_log ? 1u : 0u;
   int64_t A = g.A, N = g.N, E = g.E;
   uint64_t o = 0;
   auto take = [&](int64_t elems, int64_t elem_bytes) {
@@ -248,14 +249,17 @@ inline Layout relayout(const GraphView& g, const Caps& caps) {
   };
   L.vrec = take(caps.V, kRec);
   L.lrec = take(caps.V, kRec);
-  L.arec = take(A, kRec64);
+  L.arec = take(A, kRec);
   L.looprec = take(caps.L, kRec);
-  L.emrec = take((int64_t)caps.EM + 1, kRec64);
+  L.emrec = take((int64_t)caps.EM + 1, kRec);
   L.opnd = take(E, 4);
   L.fs = take(caps.FS, 4);
   L.stk = take(2 * N, 4);
   L.seen = take(N, 1);
-  L.em_opnd = take(caps.EO, 4);
+  L.em_opnd = take(opnd_log ? caps.EO : 0, 4);
+  L.em_spec = take((int64_t)caps.EM + 1, 4);
+  L.st8 = take(2 * kMaxAxes, 8);
+  L.st4 = take(3 * kMaxAxes, 4);
   L.carry = take(A / 32 + 1, 4);
   // legal list: static ordinals, plus every resurfaced op's when enabled
   L.lg = take(g.n_ord + (g.resurface ? N * kMaxRank * g.n_auto : 0), 4);
@@ -272,8 +276,8 @@ PE_HD Arena carve(const Layout& L, uint8_t* base, int lane = 0) {
   a.L = &L;
   a.b1 = base + (uint64_t)lane;
   a.b4 = base + (uint64_t)lane * 4;
+  a.b8 = base + (uint64_t)lane * 8;
   a.r32 = base + (uint64_t)lane * kRec;
-  a.r64 = base + (uint64_t)lane * kRec64;
   return a;
 }
 
@@ -1142,23 +1146,17 @@ struct Cand {
     for (int d = 0; d < kMaxRank; ++d) gg.v[d] = w.g[d];
     a.lo_g()[v] = gg;
   }
-  PE_HD void register_type(int32_t buf, const Low& w) {
-    register_type(buf, w, 4 * local_elems(w));
-  }
-  // (lb = the record's local bytes when the caller already has them)
-  PE_HD void register_type(int32_t buf, const Low& w, int64_t lb) {
-    register_type_gb(buf, w.spec, global_bytes(w), lb);
-  }
-  // (and gb = its global bytes)
-  PE_HD void register_type_gb(int32_t buf, uint32_t spec, int64_t gb, int64_t lb) {
-    if (buf < g.A) {
-      a.arg_gb()[buf] = gb;
-      a.arg_lb()[buf] = lb;
-      a.arg_spec()[buf] = spec;
-    } else {
-      a.em_q2()[buf - g.A] = I64x2{gb, lb};
-      a.em_q3()[buf - g.A] = V4{(int32_t)spec, 0, 0, 0};
-    }
+  // register_type (REF spmd.cc): the buffer's final DistType.  Only the
+  // parity trace reads it: collective_stats takes each operand's type at
+  // the collective's emission (emit_coll), which is its final one -- a
+  // buffer is re-registered only by finish_loop for its loop's yield, the
+  // last item of the body, so no collective consumed it earlier, or, when
+  // the yield is a slice that kept its source's sharded buffer, with the
+  // identical type.
+  PE_HD void note_type(int32_t buf, uint32_t spec) {
+    if (!tracing) return;
+    if (buf < g.A) a.arg_spec()[buf] = spec;
+    else a.em_spec()[buf - g.A] = spec;
   }
   // opens an SPMD op (first operand op0 or -1, local result bytes lb; the
   // record's first 32 bytes are written whole); operands are then appended
@@ -1192,6 +1190,18 @@ struct Cand {
   // so each emitting loop inlines a single copy (code size).
   PE_HD void emit_coll(Low& w, int32_t kind, int32_t ax, int d) {
     int32_t src = w.buf;
+    // collective_stats (REF spmd.cc:405-434) on the operand's type, which
+    // is final at emission (note_type): all_reduce bytes = its global
+    // bytes, all_gather bytes = its local bytes x (axis size - 1)
+    if (kind == kAllReduce) {
+      a.st8()[ax] += global_bytes(w);
+      a.st4()[ax]++;
+    } else if (kind == kAllGather) {
+      a.st8()[kMaxAxes + ax] += 4 * local_elems(w) * (asz(ax) - 1);
+      a.st4()[kMaxAxes + ax]++;
+    } else {
+      a.st4()[2 * kMaxAxes + ax]++;
+    }
     if (kind == kAllGather) {
       w.spec = spec_set_axis(w.spec, d, 0);
       w.acq &= ~(1u << d);
@@ -1206,7 +1216,7 @@ struct Cand {
     if (j < 0) return;
     add_operand(j, src);
     w.buf = g.A + j;
-    register_type(w.buf, w, lb);
+    note_type(w.buf, w.spec);
   }
   PE_HD void emit_all_reduce(Low& w, int32_t ax) { emit_coll(w, kAllReduce, ax, -1); }
   // materialize_for_direct_use (REF spmd.cc:119-129); loop_axis = -1 at top.
@@ -1364,7 +1374,7 @@ struct Cand {
         break;
     }
     r.buf = g.A + j;
-    register_type_gb(r.buf, r.spec, 4 * out_elems * gmul, 4 * out_elems);
+    note_type(r.buf, r.spec);
     store(v, r);
   }
 
@@ -1461,9 +1471,11 @@ struct Cand {
         }
       for (int d = 0; d < kMaxRank; ++d) w.g[d] = g.shape(lt)[d];
     }
-    // both kinds register the loop's result type (one inlined copy); a
-    // reduce loop then all-reduces it over the loop axis
-    register_type(w.buf, w);
+    // both kinds register the loop's result type (one inlined copy; its
+    // local shape must exist, REF mesh.cc:110-124); a reduce loop then
+    // all-reduces it over the loop axis
+    local_elems(w);
+    note_type(w.buf, w.spec);
     if (!tile) {
       emit_all_reduce(w, lax);
       if (bad()) return;
@@ -1480,6 +1492,8 @@ struct Cand {
     nem = 0;
     neo = 0;
     flops = 0;
+    for (int x = 0; x < 2 * kMaxAxes; ++x) a.st8()[x] = 0;
+    for (int x = 0; x < 3 * kMaxAxes; ++x) a.st4()[x] = 0;
     for (int32_t x = 0; x < g.A; ++x) {
       Low w;
       int rank = g.vrank[x];
@@ -1494,7 +1508,7 @@ struct Cand {
       }
       store(x, w);
       int64_t lb = 4 * local_elems(w);
-      register_type(x, w, lb);
+      note_type(x, w.spec);
       a.aspec0()[x] = w.spec;
       a.alb0()[x] = lb;
     }
@@ -1551,19 +1565,19 @@ struct Cand {
   // ------------------------------------------------------------ scoring
   PE_HD void score(const pe_cost_params& cp, int64_t baseline, int32_t steps,
                    pe_result& r) {
+    // collective_stats (REF spmd.cc:405-434), accumulated at emission
     for (int x = 0; x < PE_MAX_AXES; ++x) {
-      r.ar_bytes[x] = 0;
-      r.ag_bytes[x] = 0;
-      r.ar_cnt[x] = 0;
-      r.ag_cnt[x] = 0;
-      r.sbc_cnt[x] = 0;
+      r.ar_bytes[x] = a.st8()[x];
+      r.ag_bytes[x] = a.st8()[kMaxAxes + x];
+      r.ar_cnt[x] = a.st4()[x];
+      r.ag_cnt[x] = a.st4()[kMaxAxes + x];
+      r.sbc_cnt[x] = a.st4()[2 * kMaxAxes + x];
     }
-    // One pass over the SPMD ops: collective_stats (REF spmd.cc:405-434)
-    // over final registered types, and the liveness sweep (SURVEY.md
-    // B.5.1): new_op set delta[j] = +lb[j]; -lb[j] lands after the
-    // buffer's last use (> j), so by the time the sweep reaches j every
-    // subtraction landing there is already in delta[j] and the running sum
-    // is taken in the same pass.
+    // One pass over the SPMD ops, the liveness sweep:
+    // new_op set delta[j] = +lb[j]; -lb[j] lands after the buffer's last
+    // use (> j), so by the time the sweep reaches j every subtraction
+    // landing there is already in delta[j] and the running sum is taken in
+    // the same pass.
     if (result_buf >= g.A) a.em_last()[result_buf - g.A] = nem - 1;
     a.delta()[nem] = 0;
     int64_t run = 0, best = 0;
@@ -1573,18 +1587,6 @@ struct Cand {
       int64_t lb = q1.x;
       run += q1.y;
       if (run > best) best = run;
-      int32_t kind = q.x & 0xFF, ax = ((q.x >> 8) & 0xF) - 1;
-      if (kind == kAllReduce) {
-        int32_t b = q.y;
-        r.ar_cnt[ax]++;
-        r.ar_bytes[ax] += b < g.A ? a.arg_gb()[b] : a.em_gb()[b - g.A];
-      } else if (kind == kAllGather) {
-        int32_t b = q.y;
-        r.ag_cnt[ax]++;
-        r.ag_bytes[ax] += (b < g.A ? a.arg_lb()[b] : a.em_blb()[b - g.A]) * (asz(ax) - 1);
-      } else if (kind == kSliceByCoord) {
-        r.sbc_cnt[ax]++;
-      }
 #ifndef PE_EXP_NO_DELTA
       a.delta()[q.z + 1] -= lb;
 #endif
@@ -1699,7 +1701,8 @@ struct Cand {
   PE_HD void eval(const pe_action* acts, int32_t n, const pe_cost_params& cp,
                   int64_t baseline, pe_result& r, int32_t* trace, uint32_t trace_words,
                   uint8_t* argflags = nullptr) {
-    tracing = trace != nullptr && trace_words > 0;
+    // (traces are taken in full-size arenas, which keep the operand log)
+    tracing = trace != nullptr && trace_words > 0 && a.L->has_opnd;
     tick_start();
     init();
     tick(0);

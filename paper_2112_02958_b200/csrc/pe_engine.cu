@@ -825,7 +825,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
     // retry path (tests/test_gpu_parity.py::test_capacity_retry_path)
     pe::Caps c = e->layout.caps;
     c.EM = std::max(4, std::atoi(dbg));
-    e->layout = pe::relayout(v, c);
+    e->layout = pe::relayout(v, c, false);
   }
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -901,7 +901,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
     c.FS = std::min(c.FS, grow(hw[2], 16));
     c.EM = std::min(c.EM, grow(hw[3], 128));
     c.EO = std::min(c.EO, grow(hw[4], 128));
-    e->layout = pe::relayout(v, c);
+    e->layout = pe::relayout(v, c, false);
     fit_groups = (budget - big_groups * e->big_layout.bytes) /
                  std::max<uint64_t>(e->layout.bytes, 1);
   }
@@ -1119,9 +1119,13 @@ pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* 
   uint32_t slots = launch_slots(e, n);
   if (!cuda_ok(cudaMemsetAsync(e->d_ctr, 0, sizeof(uint32_t), st), err, "reset work counter"))
     return PE_ERR_CUDA;
-  pe_eval_kernel<false><<<(slots + kBlock - 1) / kBlock, kBlock, 0, st>>>(
-      e->dview, e->layout, e->d_arena, slots, d_acts, d_off, n, e->cp, e->baseline, d_out,
-      d_trace, trace_words, d_flags, e->d_ctr);
+  // parity traces need the SPMD operand log, which only the full-size
+  // arenas keep: traced batches run there (the main pass has nothing to do)
+  const bool full = d_trace != nullptr && trace_words > 0;
+  uint32_t ms = full ? std::min<uint32_t>(e->big_slots, n) : slots;
+  pe_eval_kernel<false><<<(ms + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+      e->dview, full ? e->big_layout : e->layout, full ? e->d_big_arena : e->d_arena, ms, d_acts,
+      d_off, n, e->cp, e->baseline, d_out, d_trace, trace_words, d_flags, e->d_ctr);
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
   pe_eval_kernel<true><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
       e->dview, e->big_layout, e->d_big_arena, bs, d_acts, d_off, n, e->cp, e->baseline, d_out,
