@@ -688,6 +688,7 @@ def run_sweep(args):
                                    "mesh [batch=4, model=2], grouped worklist, root rollouts",
                        "graph_ops": g.n_ops, "graph_args": g.n_args, "sizes": sizes,
                        "arena_bytes": eng.arena_bytes(), "slots": eng.slots(),
+                       "arena_caps": eng.arena_caps(),
                        "l2": "256 MB flush before every launch"},
             "sweep": rows, "parent_plus_one": p1,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * 8 + (B + 1) * 4,

@@ -329,6 +329,9 @@ int64_t pe_engine_baseline_bytes(const pe_engine* e);
 /* bytes of the per-candidate arena, and candidate slots per launch */
 int64_t pe_engine_arena_bytes(const pe_engine* e);
 uint32_t pe_engine_slots(const pe_engine* e);
+/* capacities of the tight arena: value slots, loops, front stack, SPMD
+ * ops, operand references */
+void pe_engine_arena_caps(const pe_engine* e, int32_t* caps5);
 /* bytes of the compiled graph image resident in HBM */
 int64_t pe_engine_graph_bytes(const pe_engine* e);
 /* kernel launches issued by this engine since creation */

@@ -189,6 +189,7 @@ SIGNATURES = {
     "pe_engine_baseline_bytes": (C.c_int64, [_P]),
     "pe_engine_arena_bytes": (C.c_int64, [_P]),
     "pe_engine_slots": (C.c_uint32, [_P]),
+    "pe_engine_arena_caps": (None, [_P, C.POINTER(C.c_int32)]),
     "pe_engine_launch_count": (C.c_uint64, [_P]),
     "pe_engine_sched_nodes": (C.c_int64, [_P]),
     "pe_engine_set_state_reuse": (C.c_int, [_P, C.c_double]),
@@ -226,7 +227,7 @@ def load(path: str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("PE_LIB") or LIB_PATH  # PE_LIB: a debug build
     if not os.path.exists(p):
         raise RuntimeError(
             f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -79,11 +79,36 @@ struct Caps {
 #endif
 constexpr int kLanes = PE_LANES;
 
+// PE_BOUNDS_CHECK (debug builds, tests/test_gpu_bounds.py): every arena
+// access must fall inside the candidate's group arena, else the kernel traps
+// (the device-side stand-in for compute-sanitizer's memcheck on this path;
+// overlaps between a lane's own arrays show up as parity failures).
+#ifdef PE_BOUNDS_CHECK
+PE_HD void pe_bounds_fail() {
+#ifdef __CUDA_ARCH__
+  __trap();
+#else
+  __builtin_trap();
+#endif
+}
+template <typename T, int STRIDE>
+struct Field {
+  uint8_t* p;
+  const uint8_t* lo;
+  const uint8_t* hi;
+  PE_HD T& operator[](int64_t i) const {
+    uint8_t* q = p + i * STRIDE;
+    if (q < lo || q + sizeof(T) > hi) pe_bounds_fail();
+    return *reinterpret_cast<T*>(q);
+  }
+};
+#else
 template <typename T, int STRIDE>
 struct Field {
   uint8_t* p;
   PE_HD T& operator[](int64_t i) const { return *reinterpret_cast<T*>(p + i * STRIDE); }
 };
+#endif
 template <typename T>
 using LF = Field<T, kLanes * (int)sizeof(T)>;
 
@@ -136,8 +161,14 @@ constexpr int kRec = 32;    // VRec, LowRec, LoopRec, ArgRec, EmRec
 struct Arena {
   const struct Layout* L;
   uint8_t *b1, *b4, *b8, *r32;
+#ifdef PE_BOUNDS_CHECK
+  const uint8_t *lo, *hi;  // the group arena
+#define PE_REC(name, T, base, arr, off, STRIDE) \
+  PE_HD Field<T, STRIDE> name() const { return {base + L->arr + (off), lo, hi}; }
+#else
 #define PE_REC(name, T, base, arr, off, STRIDE) \
   PE_HD Field<T, STRIDE> name() const { return {base + L->arr + (off)}; }
+#endif
   PE_REC(vk, uint8_t, r32, vrec, 0, kLanes * kRec)
   PE_REC(vh, uint32_t, r32, vrec, 0, kLanes * kRec)
   PE_REC(vref, int32_t, r32, vrec, 4, kLanes * kRec)
@@ -278,6 +309,10 @@ PE_HD Arena carve(const Layout& L, uint8_t* base, int lane = 0) {
   a.b4 = base + (uint64_t)lane * 4;
   a.b8 = base + (uint64_t)lane * 8;
   a.r32 = base + (uint64_t)lane * kRec;
+#ifdef PE_BOUNDS_CHECK
+  a.lo = base;
+  a.hi = base + L.bytes;
+#endif
   return a;
 }
 

@@ -963,6 +963,11 @@ int64_t pe_engine_baseline_bytes(const pe_engine* e) { return e->baseline; }
 int64_t pe_engine_arena_bytes(const pe_engine* e) {
   return (int64_t)(e->layout.bytes / pe::kLanes);  // per candidate
 }
+void pe_engine_arena_caps(const pe_engine* e, int32_t* caps5) {
+  const pe::Caps& c = e->layout.caps;
+  int32_t v[5] = {c.V, c.L, c.FS, c.EM, c.EO};
+  for (int k = 0; k < 5; ++k) caps5[k] = v[k];
+}
 uint32_t pe_engine_slots(const pe_engine* e) { return e->slots; }
 uint64_t pe_engine_launch_count(const pe_engine* e) { return e->launches; }
 int64_t pe_engine_sched_nodes(const pe_engine* e) { return (int64_t)e->t_nl.size(); }

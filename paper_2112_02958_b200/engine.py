@@ -268,6 +268,11 @@ class Engine:
     def arena_bytes(self) -> int:
         return int(self.lib.pe_engine_arena_bytes(self.h))
 
+    def arena_caps(self) -> dict:
+        c = (C.c_int32 * 5)()
+        self.lib.pe_engine_arena_caps(self.h, c)
+        return dict(zip(("values", "loops", "front", "spmd_ops", "operand_refs"), list(c)))
+
     def slots(self) -> int:
         return int(self.lib.pe_engine_slots(self.h))
 

@@ -14,8 +14,14 @@ from paper_2112_02958_b200 import capi
 from paper_2112_02958_b200.capi import PeAction, PeResult, PeSearchConfig, PeCostParams
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ORACLE_SO = os.path.join(ROOT, "oracle", "_ref", "liboracle.so")
-HARNESS_SO = os.path.join(ROOT, "tests", "native", "_build", "libpe_host_harness.so")
+ORACLE_SO = os.path.join(ROOT, "oracle", "_ref",
+                         "liboracle_asan.so" if os.environ.get("PE_ASAN") else "liboracle.so")
+# PE_ASAN=1: AddressSanitizer + UBSan builds of the host harness (with arena
+# bounds checks) and of the oracle (tests/test_asan.py runs them)
+HARNESS_SO = os.path.join(ROOT, "tests", "native", "_build",
+                          "libpe_host_harness_asan.so" if os.environ.get("PE_ASAN")
+                          else "libpe_host_harness.so")
+SAN_FLAGS = ["-fsanitize=address,undefined", "-fno-omit-frame-pointer", "-DPE_BOUNDS_CHECK"]
 
 _P = C.c_void_p
 
@@ -33,6 +39,7 @@ def build_harness() -> str:
             return HARNESS_SO
     os.makedirs(os.path.dirname(HARNESS_SO), exist_ok=True)
     subprocess.check_call(["g++", "-std=c++17", "-O2", "-g", "-fPIC", "-shared",
+                           *(SAN_FLAGS if os.environ.get("PE_ASAN") else []),
                            "-I", os.path.join(ROOT, "include"),
                            "-I", os.path.join(ROOT, "paper_2112_02958_b200", "csrc"),
                            *src, "-o", HARNESS_SO])
@@ -41,7 +48,8 @@ def build_harness() -> str:
 
 def build_oracle() -> str:
     if not os.path.exists(ORACLE_SO):
-        subprocess.check_call(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"])
+        target = ["asan"] if os.environ.get("PE_ASAN") else []
+        subprocess.check_call(["make", "-C", os.path.join(ROOT, "oracle"), "-j8", *target])
     return ORACLE_SO
 
 
