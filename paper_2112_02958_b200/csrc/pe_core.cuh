@@ -288,7 +288,7 @@ inline Layout relayout(const GraphView& g, const Caps& caps, bool opnd_log) {
   L.stk = take(2 * N, 4);
   L.seen = take(N, 1);
   L.em_opnd = take(opnd_log ? caps.EO : 0, 4);
-  L.em_spec = take((int64_t)caps.EM + 1, 4);
+  L.em_spec = take(opnd_log ? (int64_t)caps.EM + 1 : 0, 4);  // (trace only)
   L.st8 = take(2 * kMaxAxes, 8);
   L.st4 = take(3 * kMaxAxes, 4);
   L.carry = take(A / 32 + 1, 4);
