@@ -238,6 +238,7 @@ def run_engine(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    eng.kernel_times(True)  # engine-side events around each main launch
     with ClockSampler(local) as clk:
         for i in range(K):
             flush.zero_()  # L2 flushed between timed iterations (outside the events)
@@ -245,6 +246,7 @@ def run_engine(args):
             step(i)
             stops[i].record(stream)
         torch.cuda.synchronize(dev)
+    kern_ms = eng.kernel_times(False)
     if dist:
         dist.barrier()
     launches = eng.launch_count() - launches0
@@ -325,14 +327,22 @@ def run_engine(args):
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    kern_s = sum(step_ms) / 1e3 / K
+    # the dominant kernel's own duration: CUDA events the engine records
+    # around its main rollout launch on the launching stream (pe.h
+    # pe_engine_set_kernel_timing), averaged over the timed steps
+    kern_s = sum(kern_ms) / 1e3 / K if kern_ms else sum(step_ms) / 1e3 / K
     achieved = b_cand * B / kern_s / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
+    # DRAM traffic of that kernel per launch, from the committed ncu --set
+    # full capture of the same launch (tools/ncu_traffic.py); only when it
+    # was captured at this batch size and engine build
+    traffic, traffic_src = None, None
+    tf = os.path.join(ROOT, "profiles", "r2_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("bytes_per_launch_per_candidate")
-            traffic = traffic * B if traffic else None
+            t = json.load(open(tf))
+            if int(t.get("candidates", -1)) == B:
+                traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+                traffic_src = t.get("source")
         except Exception:
             traffic = None
 
@@ -362,7 +372,8 @@ def run_engine(args):
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
                              "algorithmic_bytes_per_candidate": b_cand,
-                             "kernel": "pe_rollout_kernel",
+                             "kernel": "pe_rollout_kernel (main launch; engine-side CUDA events)",
+                             "kernel_ms_per_launch": 1e3 * kern_s, "traffic_source": traffic_src,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
                 "cpu_baseline": cpu,
                 "parity_sample": parity,

@@ -332,6 +332,12 @@ uint32_t pe_engine_slots(const pe_engine* e);
 /* capacities of the tight arena: value slots, loops, front stack, SPMD
  * ops, operand references */
 void pe_engine_arena_caps(const pe_engine* e, int32_t* caps5);
+/* Measurement: with timing on, every main rollout launch is bracketed by a
+ * pair of CUDA events on its stream; pe_engine_kernel_times waits for them,
+ * writes the durations (ms) of the launches since the last call and returns
+ * their number. */
+void pe_engine_set_kernel_timing(pe_engine* e, int32_t on);
+uint32_t pe_engine_kernel_times(pe_engine* e, float* ms, uint32_t cap);
 /* bytes of the compiled graph image resident in HBM */
 int64_t pe_engine_graph_bytes(const pe_engine* e);
 /* kernel launches issued by this engine since creation */

@@ -190,6 +190,8 @@ SIGNATURES = {
     "pe_engine_arena_bytes": (C.c_int64, [_P]),
     "pe_engine_slots": (C.c_uint32, [_P]),
     "pe_engine_arena_caps": (None, [_P, C.POINTER(C.c_int32)]),
+    "pe_engine_set_kernel_timing": (None, [_P, C.c_int32]),
+    "pe_engine_kernel_times": (C.c_uint32, [_P, C.POINTER(C.c_float), C.c_uint32]),
     "pe_engine_launch_count": (C.c_uint64, [_P]),
     "pe_engine_sched_nodes": (C.c_int64, [_P]),
     "pe_engine_set_state_reuse": (C.c_int, [_P, C.c_double]),

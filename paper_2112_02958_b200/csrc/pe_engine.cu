@@ -103,6 +103,10 @@ struct pe_engine {
   std::vector<std::string> pc_pending;  // per candidate of the current call
   uint64_t* d_cv = nullptr;  // from | save addresses, from_len, saved flags
   size_t cv_cap = 0;
+  // main rollout launch timing (pe_engine_set_kernel_timing): an event pair
+  // around each main launch on its stream
+  bool ktiming = false;
+  std::vector<cudaEvent_t> kev, kev_free;
 };
 
 struct pe_state {
@@ -954,6 +958,8 @@ void pe_engine_destroy(pe_engine* e) {
   if (e->d_pc) cudaFree(e->d_pc);
   if (e->d_cv) cudaFree(e->d_cv);
   if (e->done) cudaEventDestroy(e->done);
+  for (cudaEvent_t k : e->kev) cudaEventDestroy(k);
+  for (cudaEvent_t k : e->kev_free) cudaEventDestroy(k);
   delete e;
 }
 
@@ -963,6 +969,22 @@ int64_t pe_engine_baseline_bytes(const pe_engine* e) { return e->baseline; }
 int64_t pe_engine_arena_bytes(const pe_engine* e) {
   return (int64_t)(e->layout.bytes / pe::kLanes);  // per candidate
 }
+void pe_engine_set_kernel_timing(pe_engine* e, int32_t on) { e->ktiming = on != 0; }
+
+uint32_t pe_engine_kernel_times(pe_engine* e, float* ms, uint32_t cap) {
+  uint32_t n = 0;
+  for (size_t k = 0; k + 1 < e->kev.size(); k += 2) {
+    float t = 0;
+    cudaEventSynchronize(e->kev[k + 1]);
+    if (cudaEventElapsedTime(&t, e->kev[k], e->kev[k + 1]) != cudaSuccess) t = -1;
+    if (ms && n < cap) ms[n] = t;
+    ++n;
+  }
+  e->kev_free.insert(e->kev_free.end(), e->kev.begin(), e->kev.end());
+  e->kev.clear();
+  return n;
+}
+
 void pe_engine_arena_caps(const pe_engine* e, int32_t* caps5) {
   const pe::Caps& c = e->layout.caps;
   int32_t v[5] = {c.V, c.L, c.FS, c.EM, c.EO};
@@ -1466,10 +1488,27 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
     lc.stream = st;
     lc.attrs = at;
     lc.numAttrs = e->l2_persist ? 1 : 0;
+    cudaEvent_t k0 = nullptr, k1 = nullptr;
+    if (e->ktiming) {
+      for (cudaEvent_t* k : {&k0, &k1}) {
+        if (!e->kev_free.empty()) {
+          *k = e->kev_free.back();
+          e->kev_free.pop_back();
+        } else if (cudaEventCreate(k) != cudaSuccess) {
+          *k = nullptr;
+        }
+      }
+      if (k0 && k1) cudaEventRecord(k0, st);
+    }
     cudaError_t le = cudaLaunchKernelEx(&lc, main_k, gv, e->layout, e->d_arena, slots, d_prefix,
                                         d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
                                         d_nacts, d_out, d_legal, lw, e->d_ctr + 1, perm, sv,
                                         cv, max_acts);
+    if (e->ktiming && k0 && k1) {
+      cudaEventRecord(k1, st);
+      e->kev.push_back(k0);
+      e->kev.push_back(k1);
+    }
     // the retry launch reads the statuses the main launch writes: never
     // queue it behind a main launch that failed to start
     if (le != cudaSuccess) return le;

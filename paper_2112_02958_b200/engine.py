@@ -268,6 +268,14 @@ class Engine:
     def arena_bytes(self) -> int:
         return int(self.lib.pe_engine_arena_bytes(self.h))
 
+    def kernel_times(self, on: bool):
+        """Main-launch durations (ms) since the last call, then timing on/off
+        (pe_engine_set_kernel_timing / pe_engine_kernel_times)."""
+        buf = (C.c_float * 4096)()
+        n = self.lib.pe_engine_kernel_times(self.h, buf, 4096)
+        self.lib.pe_engine_set_kernel_timing(self.h, 1 if on else 0)
+        return [buf[i] for i in range(min(n, 4096))]
+
     def arena_caps(self) -> dict:
         c = (C.c_int32 * 5)()
         self.lib.pe_engine_arena_caps(self.h, c)
