@@ -833,11 +833,13 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   }
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  // arena budget: up to 70 % of free HBM, at most 120 GiB (a second engine
-  // created later sizes itself from what is then free; the rest is headroom
-  // for the caller's buffers); PE_ARENA_BUDGET_GB overrides.  Large graphs
-  // (config 4: 5.4 MB per candidate) are slot-limited by this budget.
-  size_t budget = std::min<size_t>((size_t)(free_b * 0.70), (size_t)120 << 30);
+  // arena budget: up to 85 % of free HBM, at most 150 GiB (a second engine
+  // created later sizes itself from what is then free; the rest -- >= 27 GB
+  // on a 180 GB B200 -- is headroom for the caller's buffers and the prefix
+  // cache); PE_ARENA_BUDGET_GB overrides.  Only large graphs are slot-limited
+  // by it (config 4: 14.3 MB per candidate); 1/16 of it backs the full-size
+  // retry arenas, which calibrated tight arenas rarely send work to.
+  size_t budget = std::min<size_t>((size_t)(free_b * 0.85), (size_t)150 << 30);
   if (const char* gb = std::getenv("PE_ARENA_BUDGET_GB"))
     budget = std::min<size_t>(free_b, (size_t)(std::atof(gb) * (double)(1ull << 30)));
   // one resident thread per slot: kMinBlocks blocks of kBlock threads per SM;
@@ -846,7 +848,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   uint64_t want = (uint64_t)e->sm_count * PE_SM_THREADS / kThreadsPerSlot;
   uint64_t big_groups = std::min<uint64_t>(
       (uint64_t)e->sm_count * 8 / lanes,
-      std::max<uint64_t>(1, (budget / 8) / std::max<uint64_t>(e->big_layout.bytes, 1)));
+      std::max<uint64_t>(1, (budget / 16) / std::max<uint64_t>(e->big_layout.bytes, 1)));
   e->big_slots = (uint32_t)(big_groups * lanes);
   // arenas start zeroed: the per-op `seen` marks of the stuck analysis are
   // cleared by each candidate after use, never wholesale
