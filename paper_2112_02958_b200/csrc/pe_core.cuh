@@ -62,7 +62,8 @@ struct Caps {
 // PE_LANES = 1 (plain structure of arrays).
 //   value slots   vhdr (kind | tile flag | loop axis | loop dim), vref, vaux,
 //                 uses, slcnt, body links, top-level position
-//   lowering      lo_buf, lo_spec, lo_acq, lo_g (REF spmd.cc:42 `Lowered`)
+//   lowering      lo_buf, lo_spec, lo_aux (acq | shape code), lo_gv (REF
+//                 spmd.cc:42 `Lowered`; the global shape as a code, see Low)
 //   arguments     direct-in-loop count, slice demand, atomic flag, SPMD arg
 //                 type, final registered type of the argument buffer
 //   loops         kind, axis, dim, body list, yield, result type
@@ -128,8 +129,8 @@ struct alignas(16) I64x2 {
 struct alignas(16) LowHead {
   int32_t buf;
   uint32_t spec;
-  uint32_t acq;
-  int32_t pad;
+  uint32_t aux;  // acq | shape code << 4
+  int32_t gv;
 };
 
 struct Layout {
@@ -160,7 +161,7 @@ constexpr int kRec = 32;    // VRec, LowRec, LoopRec, ArgRec, EmRec
 //                bytes per axis, st4 = their counts + slice_by_coord counts
 struct Arena {
   const struct Layout* L;
-  uint8_t *b1, *b4, *b8, *r32;
+  uint8_t *b1, *b4, *b8, *r16, *r32;
 #ifdef PE_BOUNDS_CHECK
   const uint8_t *lo, *hi;  // the group arena
 #define PE_REC(name, T, base, arr, off, STRIDE) \
@@ -180,11 +181,8 @@ struct Arena {
   PE_REC(vpos, int32_t, r32, vrec, 28, kLanes * kRec)
   PE_REC(vr0, V4, r32, vrec, 0, kLanes * kRec)   // vhdr vref vaux uses
   PE_REC(vr1, V4, r32, vrec, 16, kLanes * kRec)  // slcnt bnext bprev vpos
-  PE_REC(lo_buf, int32_t, r32, lrec, 0, kLanes * kRec)
-  PE_REC(lo_spec, uint32_t, r32, lrec, 4, kLanes * kRec)
-  PE_REC(lo_acq, uint32_t, r32, lrec, 8, kLanes * kRec)
-  PE_REC(lo_g, G4, r32, lrec, 16, kLanes * kRec)
-  PE_REC(lo_h, LowHead, r32, lrec, 0, kLanes * kRec)
+  PE_REC(lo_buf, int32_t, r16, lrec, 0, kLanes * 16)
+  PE_REC(lo_h, LowHead, r16, lrec, 0, kLanes * 16)
   PE_REC(adirect, int32_t, r32, arec, 0, kLanes * kRec)
   PE_REC(aslice, int32_t, r32, arec, 4, kLanes * kRec)
   PE_REC(awrapped, uint8_t, r32, arec, 8, kLanes * kRec)
@@ -279,7 +277,7 @@ inline Layout relayout(const GraphView& g, const Caps& caps, bool opnd_log) {
     return at;
   };
   L.vrec = take(caps.V, kRec);
-  L.lrec = take(caps.V, kRec);
+  L.lrec = take(caps.V, 16);
   L.arec = take(A, kRec);
   L.looprec = take(caps.L, kRec);
   L.emrec = take((int64_t)caps.EM + 1, kRec);
@@ -308,6 +306,7 @@ PE_HD Arena carve(const Layout& L, uint8_t* base, int lane = 0) {
   a.b1 = base + (uint64_t)lane;
   a.b4 = base + (uint64_t)lane * 4;
   a.b8 = base + (uint64_t)lane * 8;
+  a.r16 = base + (uint64_t)lane * 16;
   a.r32 = base + (uint64_t)lane * kRec;
 #ifdef PE_BOUNDS_CHECK
   a.lo = base;
@@ -331,11 +330,18 @@ PE_HD double ddiv(double a, double b) { volatile double r = a / b; return r; }
 // Lowered view of one value (REF spmd.cc:42-51 `Lowered`): buffer, spec
 // word, acquired-in-loop mask (loops never nest, so acq is 0 or 1 per dim)
 // and global shape.
+//
+// In the arena the global shape is not stored (16-byte records): it is the
+// static shape of value gv with, per dim d, code (gx >> 2d) & 3 = 0 as is,
+// 1 divided by, 2 multiplied by the size of axis (gx >> 8) & 3 -- a
+// per-iteration copy divides its loop dim, an acquired sharded dim
+// multiplies back (lower_base), and no other shapes arise.
 struct Low {
   int32_t buf;
   uint32_t spec;
   uint32_t acq;
-  int32_t g[kMaxRank];
+  int32_t gv;
+  uint32_t gx;
 };
 
 struct Pull {
@@ -1131,9 +1137,15 @@ struct Cand {
   // when not divisible.  Branch-free (an unsharded dim divides by 1): after
   // a failure the candidate's outputs are discarded (finish), so only the
   // status matters, not the quotient returned alongside it.
+  // global dim d of a record, from its shape code (Low)
+  PE_HD uint32_t gdim(const Low& w, int d) const {
+    uint32_t x = (uint32_t)g.shape(w.gv)[d], c = (w.gx >> (2 * d)) & 3u;
+    uint32_t ax1 = ((w.gx >> 8) & 3u) + 1u;
+    return c == 0 ? x : c == 1 ? g.quo1(x, ax1) : x * g.axis_sz32[ax1];
+  }
   PE_HD int64_t local_dim(const Low& w, int d) {
     uint32_t ax1 = spec_axis(w.spec, d);
-    uint32_t x = (uint32_t)w.g[d];
+    uint32_t x = gdim(w, d);
     uint32_t q = g.quo1(x, ax1);
     if (x != q * g.axis_sz32[ax1]) fail(PE_CAND_INTERNAL);
     return q;
@@ -1145,9 +1157,9 @@ struct Cand {
 #pragma unroll
     for (int d = 0; d < kMaxRank; ++d) {
       uint32_t ax1 = spec_axis(w.spec, d);
-      uint32_t x = (uint32_t)w.g[d];
-      uint32_t q = g.quo1(x, ax1);
       bool in = d < r;
+      uint32_t x = in ? gdim(w, d) : 0u;
+      uint32_t q = g.quo1(x, ax1);
       rem |= in ? x - q * g.axis_sz32[ax1] : 0u;
       e *= in ? (int64_t)q : 1;
     }
@@ -1157,7 +1169,7 @@ struct Cand {
   PE_HD int64_t global_bytes(const Low& w) const {
     int64_t e = 4;
     int r = rank_of_spec(w.spec);
-    for (int d = 0; d < r; ++d) e *= w.g[d];
+    for (int d = 0; d < r; ++d) e *= gdim(w, d);
     return e;
   }
   PE_HD Low load(int32_t v) const {
@@ -1165,21 +1177,18 @@ struct Cand {
     LowHead h = a.lo_h()[v];
     w.buf = h.buf;
     w.spec = h.spec;
-    w.acq = h.acq;
-    G4 gg = a.lo_g()[v];
-    for (int d = 0; d < kMaxRank; ++d) w.g[d] = gg.v[d];
+    w.acq = h.aux & 0xFu;
+    w.gx = h.aux >> 4;
+    w.gv = h.gv;
     return w;
   }
   PE_HD void store(int32_t v, const Low& w) {
     LowHead h;
     h.buf = w.buf;
     h.spec = w.spec;
-    h.acq = w.acq;
-    h.pad = 0;
+    h.aux = w.acq | (w.gx << 4);
+    h.gv = w.gv;
     a.lo_h()[v] = h;
-    G4 gg;
-    for (int d = 0; d < kMaxRank; ++d) gg.v[d] = w.g[d];
-    a.lo_g()[v] = gg;
   }
   // register_type (REF spmd.cc): the buffer's final DistType.  Only the
   // parity trace reads it: collective_stats takes each operand's type at
@@ -1299,10 +1308,11 @@ struct Cand {
     Low r;
     int32_t xv = g.A + o;
     int rank = g.vrank[xv];
-    for (int d = 0; d < kMaxRank; ++d) r.g[d] = g.shape(xv)[d];
+    r.gv = xv;
+    r.gx = 0;
     if (l >= 0) {
       int32_t dd = (a.vaux()[v] & 7) - 1;
-      if (dd >= 0) r.g[dd] = (int32_t)g.aquo((uint32_t)r.g[dd], lax);
+      if (dd >= 0) r.gx = (1u << (2 * dd)) | ((uint32_t)lax << 8);
     }
     r.spec = (uint32_t)rank << 24;
     r.acq = 0;
@@ -1336,7 +1346,9 @@ struct Cand {
       if (kind == kReshape) {
         int64_t in[kMaxRank];
         for (int d = 0; d < wr; ++d) in[d] = local_dim(w, d);
-        rr = reshape_rule(in, wr, r.g, rank);
+        int32_t pit[kMaxRank];
+        for (int d = 0; d < kMaxRank; ++d) pit[d] = (int32_t)gdim(r, d);
+        rr = reshape_rule(in, wr, pit, rank);
         if (rr.error) {
           fail(PE_CAND_INTERNAL);
           return;
@@ -1385,12 +1397,17 @@ struct Cand {
 #pragma unroll
     for (int d = 0; d < kMaxRank; ++d) {
       if (d >= rank) break;
-      out_elems *= r.g[d];
+      out_elems *= gdim(r, d);
       uint32_t ax1 = spec_axis(r.spec, d);
       if (ax1) {
         int64_t sz = asz(ax1 - 1);
-        r.g[d] = (int32_t)(r.g[d] * sz);
         gmul *= sz;
+        // shape code: a divided dim is restored, any other multiplied; one
+        // axis per code (inside a loop every sharded dim is by its axis)
+        uint32_t c = (r.gx >> (2 * d)) & 3u;
+        if ((r.gx & 0xFFu) != 0 && ((r.gx >> 8) & 3u) != ax1 - 1) fail(PE_CAND_CAPACITY);
+        r.gx = (r.gx & ~(3u << (2 * d)) & 0xFFu) | ((c == 1 ? 0u : 2u) << (2 * d)) |
+               ((ax1 - 1) << 8);
       }
     }
     int32_t j = new_op(kind, -1, -1, n, n > 0 ? a.lo_buf()[a.opnd()[base]] : -1, 4 * out_elems);
@@ -1488,7 +1505,8 @@ struct Cand {
         fail(PE_CAND_INTERNAL);
         return;
       }
-      for (int d = 0; d < kMaxRank; ++d) w.g[d] = g.shape(lt)[d];
+      w.gv = lt;
+      w.gx = 0;
       int rk = rank_of_spec(w.spec);
       for (int d = 0; d < rk; ++d)
         if (local_dim(w, d) != local_dim(yv, d)) {
@@ -1504,7 +1522,8 @@ struct Cand {
           w.spec = spec_set_axis(w.spec, d, 0);
           w.acq &= ~(1u << d);
         }
-      for (int d = 0; d < kMaxRank; ++d) w.g[d] = g.shape(lt)[d];
+      w.gv = lt;
+      w.gx = 0;
     }
     // both kinds register the loop's result type (one inlined copy; its
     // local shape must exist, REF mesh.cc:110-124); a reduce loop then
@@ -1532,14 +1551,15 @@ struct Cand {
     for (int32_t x = 0; x < g.A; ++x) {
       Low w;
       int rank = g.vrank[x];
-      for (int d = 0; d < kMaxRank; ++d) w.g[d] = g.shape(x)[d];
+      w.gv = x;
+      w.gx = 0;
       w.spec = (uint32_t)rank << 24;
       w.acq = 0;
       w.buf = x;
       int32_t direct = a.uses()[x] - a.slcnt()[x] - (result_ref == x ? 1 : 0);
       if (direct == 0 && a.aslice()[x] >= 0) {
         int d = a.aslice()[x] & 7, ax = a.aslice()[x] >> 3;
-        if (g.amod((uint32_t)w.g[d], ax) == 0) w.spec = spec_set_axis(w.spec, d, (uint32_t)(ax + 1));
+        if (g.amod((uint32_t)g.shape(x)[d], ax) == 0) w.spec = spec_set_axis(w.spec, d, (uint32_t)(ax + 1));
       }
       store(x, w);
       int64_t lb = 4 * local_elems(w);
