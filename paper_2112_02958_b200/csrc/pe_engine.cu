@@ -106,6 +106,7 @@ struct pe_engine {
   // main rollout launch timing (pe_engine_set_kernel_timing): an event pair
   // around each main launch on its stream
   bool ktiming = false;
+  uint32_t small_block = 32;  // block size of launches below full occupancy
   std::vector<cudaEvent_t> kev, kev_free;
 };
 
@@ -820,6 +821,8 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   e->layout = pe::make_layout(v, /*tight=*/true);
   e->big_layout = pe::make_layout(v, /*tight=*/false);
   if (const char* sd = std::getenv("PE_SCHED_DEPTH")) e->sched_depth = std::atoi(sd);
+  if (const char* sb = std::getenv("PE_SMALL_BLOCK"))  // experiment knob (32 .. 128)
+    e->small_block = (uint32_t)std::min(128, std::max(32, std::atoi(sb) / 32 * 32));
   if (const char* sm = std::getenv("PE_SCHED_MIN_BATCH")) e->sched_min_batch = (uint32_t)std::atoi(sm);
   if (const char* sn = std::getenv("PE_SCHED_MAX_NODES")) e->sched_max_nodes = std::atoi(sn);
   if (const char* sg = std::getenv("PE_SCHED_SNAP_GB")) e->snap_budget_gb = std::atof(sg);
@@ -1152,11 +1155,11 @@ pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* 
   // arenas keep: traced batches run there (the main pass has nothing to do)
   const bool full = d_trace != nullptr && trace_words > 0;
   uint32_t ms = full ? std::min<uint32_t>(e->big_slots, n) : slots;
-  pe_eval_kernel<false><<<(ms + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+  pe_eval_kernel<false><<<(ms + e->small_block - 1) / e->small_block, e->small_block, 0, st>>>(
       e->dview, full ? e->big_layout : e->layout, full ? e->d_big_arena : e->d_arena, ms, d_acts,
       d_off, n, e->cp, e->baseline, d_out, d_trace, trace_words, d_flags, e->d_ctr);
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
-  pe_eval_kernel<true><<<(bs + kBlock - 1) / kBlock, kBlock, 0, st>>>(
+  pe_eval_kernel<true><<<(bs + e->small_block - 1) / e->small_block, e->small_block, 0, st>>>(
       e->dview, e->big_layout, e->d_big_arena, bs, d_acts, d_off, n, e->cp, e->baseline, d_out,
       d_trace, trace_words, d_flags, nullptr);
   e->launches += 2;
@@ -1470,10 +1473,14 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
   if (ce != cudaSuccess) return ce;
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
   uint32_t threads = slots * kThreadsPerSlot;
+  // a launch with fewer slots than the resident threads (small batches: MCTS
+  // leaf batches, config 4's arena-limited slots) runs one-warp blocks, so
+  // the block scheduler spreads its warps over every SM (128-thread blocks
+  // left SMs idle: 8,192 candidates = 64 blocks on 148 SMs)
   uint32_t blk = threads % PE_SM_THREADS == 0 && threads >= (uint32_t)e->sm_count * PE_SM_THREADS
-                     ? PE_SM_THREADS : kBlock;
+                     ? PE_SM_THREADS : e->small_block;
   uint32_t grid = (threads + blk - 1) / blk;
-  uint32_t bgrid = (bs * kThreadsPerSlot + kBlock - 1) / kBlock;
+  uint32_t bgrid = (bs * kThreadsPerSlot + e->small_block - 1) / e->small_block;
   // (the stuck-resurfacing instantiation only when the worklist uses it)
   auto launch = [&](auto main_k, auto retry_k) {
     // (experiment PE_L2_PERSIST: the graph image as a persisting L2 window)
@@ -1514,7 +1521,7 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
     // the retry launch reads the statuses the main launch writes: never
     // queue it behind a main launch that failed to start
     if (le != cudaSuccess) return le;
-    retry_k<<<bgrid, kBlock, 0, st>>>(gv, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff,
+    retry_k<<<bgrid, e->small_block, 0, st>>>(gv, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff,
                                       d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts,
                                       d_out, d_legal, lw, nullptr, nullptr, SchedView(),
                                       CacheView(), max_acts);
