@@ -117,6 +117,17 @@ def _max_over_ranks(dist, x: float, device=None) -> float:
 
 
 # ------------------------------------------------------------- CPU baseline
+def _cpu_model() -> str:
+    """The host CPU the reference arm ran on (state it)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference(text, n_cand, seed0, threads):
     """The reference's own CPU path (oracle/_ref: patched REF propagate /
     lower_to_spmd / collective_stats + SPEC cost/rollout restatement) on
@@ -154,7 +165,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": _config(per_step, {"parallelism": f"{threads} host threads"}),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "cpu": _cpu_model(), "kind": "reference",
                              "sample": f"{args.steps} x {per_step} rollouts of the bench workload"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -353,7 +364,7 @@ def run_engine(args):
             threads = os.cpu_count() or 1
             n_cpu = 48 * threads  # ~12 s of reference CPU work on this path
             v_cpu, dt = cpu_reference(text, n_cpu, 30_000_000, threads)
-            cpu = {"value": v_cpu, "unit": UNIT, "cores": threads, "kind": "reference",
+            cpu = {"value": v_cpu, "unit": UNIT, "cores": threads, "cpu": _cpu_model(), "kind": "reference",
                    "sample": f"{n_cpu} rollouts of the bench workload ({dt:.1f} s)"}
 
     if rank == 0:
@@ -449,7 +460,7 @@ def run_search(args):
                 "dtype": "int64", "data": "synthetic",
                 "config": _search_config(args, lb, budget), "megatron_found": bool(ok),
                 "plan": search.plan_actions(p), "search_s_full_budget": t_budget,
-                "cpu_baseline": {"value": t, "unit": "s", "cores": threads, "kind": "reference",
+                "cpu_baseline": {"value": t, "unit": "s", "cores": threads, "cpu": _cpu_model(), "kind": "reference",
                                  "sample": f"the full search to the plan ({budget} episodes)"},
                 "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -499,7 +510,7 @@ def run_search(args):
             cp_plan = search.run_mcts(ev, len(ords) - 1, ords, episodes=budget, seed=args.seed,
                                       leaf_batch=lb)
             tc = time.perf_counter() - t0
-            cpu = {"value": tc, "unit": "s", "cores": threads, "kind": "reference",
+            cpu = {"value": tc, "unit": "s", "cores": threads, "cpu": _cpu_model(), "kind": "reference",
                    "sample": f"the same search ({budget} episodes, leaf batch {lb})",
                    "plan_identical": search.plan_actions(cp_plan) == search.plan_actions(plan)}
     if comm is not None:
@@ -685,7 +696,7 @@ def run_sweep(args):
         if os.path.exists(H.ORACLE_SO):
             threads = os.cpu_count() or 1
             done, dt = cpu_capped(text, args.cpu_cap_s, threads, 90_000_000)
-            cpu = {"value": done / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            cpu = {"value": done / dt, "unit": UNIT, "cores": threads, "cpu": _cpu_model(), "kind": "reference",
                    "sample": f"root rollouts, one stream per core, stopped hard at "
                              f"{args.cpu_cap_s:.0f} s: {done} completed in {dt:.0f} s",
                    "completed": done, "note": "an upper bound when 0 completed; see "

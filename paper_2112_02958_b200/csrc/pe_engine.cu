@@ -12,6 +12,7 @@
 // There is no CPU fallback: without a device every entry point fails with
 // PE_ERR_NO_DEVICE.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -119,6 +120,12 @@ struct pe_state {
 };
 
 namespace {
+
+// NVTX range over an engine call (nsys / ncu timelines; header-only NVTX 3)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 void set_err(pe_error* err, int code, const std::string& msg, int line = 0, int col = 0) {
   if (!err) return;
@@ -1113,6 +1120,7 @@ pe_status pe_eval_batch(pe_engine* e, const pe_action* acts, const uint32_t* seq
 pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* seq_off,
                            uint32_t n, pe_result* out, int32_t* trace, uint32_t trace_words,
                            uint8_t* argflags, uint32_t flags, void* stream, pe_error* err) {
+  NvtxRange nvtx_("pe_eval_batch");
   if (!e || !seq_off || !out) {
     set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
     return PE_ERR_INVALID_ARGUMENT;
@@ -1360,6 +1368,7 @@ bool sched_upload(pe_engine* e, cudaStream_t st, pe_error* err) {
 // device permutation, or nullptr (identity) when scheduling is off.
 bool sched_perm(pe_engine* e, uint32_t n, const uint64_t* d_seeds, int32_t maxd,
                 cudaStream_t st, const uint32_t** perm, SchedView* sv, pe_error* err) {
+  NvtxRange nvtx_("sched_perm");
   *perm = nullptr;
   *sv = SchedView();
   int32_t depth = std::min(e->sched_depth, maxd);
@@ -1608,6 +1617,7 @@ int64_t ag_total(const pe_result& r) {
 // sequence of `seqs` (each = the state InferRest is applied to).
 bool ir_expand_batch(pe_engine* e, std::vector<std::vector<pe_action>*>& seqs, cudaStream_t st,
                      pe_error* err) {
+  NvtxRange nvtx_("ir_expand_batch");
   const pe::HostGraph& g = e->graph->g;
   const int32_t A = (int32_t)g.args.size();
   const pe_action marker{0, 0, 0, PE_ACT_INFER_REST, PE_ACT_FLAG_EXPANDED};
@@ -1767,6 +1777,7 @@ struct RolloutIo {
 // pause again.  The caller's outputs end up exactly as an uninterrupted
 // rollout would have written them.
 pe_status ir_resolve(pe_engine* e, const RolloutIo& io, cudaStream_t st, pe_error* err) {
+  NvtxRange nvtx_("ir_resolve");
   const int32_t maxd = (int32_t)e->cfg.max_decisions;
   const int32_t lw = (int32_t)pe_engine_legal_words(e);
   const uint64_t kGamma = 0x9E3779B97F4A7C15ull;
@@ -2093,6 +2104,7 @@ pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix, const uint32_t
                            const uint64_t* seeds, uint32_t n, pe_action* acts_out,
                            uint32_t* n_acts_out, pe_result* out, uint64_t* legal_out,
                            uint32_t flags, void* stream, pe_error* err) {
+  NvtxRange nvtx_("pe_rollout_batch");
   if (!e || !prefix_off || !seeds || !acts_out || !n_acts_out || !out) {
     set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
     return PE_ERR_INVALID_ARGUMENT;
@@ -2234,6 +2246,7 @@ void pe_engine_prefix_cache_stats(const pe_engine* e, uint64_t* hits, uint64_t* 
 
 pe_status pe_state_create(pe_engine* e, const pe_action* acts, uint32_t n, pe_state** out,
                           pe_error* err) {
+  NvtxRange nvtx_("pe_state_create");
   if (!e || !out || (n && !acts)) {
     set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
     return PE_ERR_INVALID_ARGUMENT;
@@ -2326,6 +2339,7 @@ pe_status pe_state_specs(const pe_state* s, uint32_t* arg_specs, uint32_t* resul
 pe_status pe_eval_from_states(pe_engine* e, const pe_state* const* parents, const pe_action* acts,
                               const uint32_t* seq_off, uint32_t n, pe_result* out, void* stream,
                               pe_error* err) {
+  NvtxRange nvtx_("pe_eval_from_states");
   if (!e || !parents || !seq_off || !out || (seq_off[n] && !acts)) {
     set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
     return PE_ERR_INVALID_ARGUMENT;
@@ -2402,6 +2416,7 @@ int engine_rollout_eval(void* user, const pe_action* prefix, const uint32_t* pof
 extern "C" pe_status pe_search(pe_engine* e, const pe_search_config* cfg, uint32_t merge_every,
                                uint32_t rank, pe_merge_fn merge, void* merge_user,
                                pe_plan* out, pe_error* err) {
+  NvtxRange nvtx_("pe_search");
   if (!e || !out) {
     set_err(err, PE_ERR_INVALID_ARGUMENT, "null argument");
     return PE_ERR_INVALID_ARGUMENT;
