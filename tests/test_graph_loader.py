@@ -97,3 +97,39 @@ def test_arrays_graph_evaluates_identically():
         rb, sb, lb = b.rollout_batch([[]] * 512, seeds, legal=True)
         assert sa == sb and la == lb
         assert all(not H.compare_results(x, y) for x, y in zip(ra, rb))
+
+
+def test_reader_accepts_the_grammar_variants():
+    # comments, free whitespace, empty lists and attribute blocks, reals in
+    # every spelling, scalar tensors, names with digits / dots / slashes
+    text = """// leading comment
+mesh {   "a"=2 ,"b" = 3 }   // trailing comment
+func @f.v2 (%x0: f32[4,6] {scope="layer_0/in"}, %w/1: f32[6]) -> f32[4,6] {
+  %c = constant() {value=-1.5e-3} : f32[]
+  %cb = broadcast_in_dim(%c) {map=[]} : f32[4,6]
+  %wb = broadcast_in_dim(%w/1) {map=[1]} : f32[4,6]
+  %y = add(%x0, %cb) {} : f32[4,6]
+  %z = mul(%y,%wb) : f32[4,6]
+  return %z
+}
+"""
+    g = engine.Graph(text)
+    assert g.n_args == 2 and g.n_ops == 5 and g.axis_names == ["a", "b"]
+    assert g.shapes[g.value_index("c")] == [] and g.scopes[0] == "layer_0/in"
+    h = engine.Graph.from_arrays(*pir_arrays.to_arrays(text.replace("// leading comment\n", "")))
+    assert h.names == g.names
+
+
+@pytest.mark.parametrize("bad", [
+    'mesh { "a" = 2 }\nfunc @f(%x: f32[4]) -> f32[4] { %y = neg(%x) : f32[4,] return %y }',
+    'func @f(%x: f32[4]) -> f32[4] { %y = slice(%x) {start=[0], limit=[1.0]} : f32[1] return %y }',
+    'func @f(%x: f32[4]) -> f32[4] { %y = neg(%x : f32[4] return %y }',
+    'func @f(%x: f32[4]) -> f32[4] { %y = neg(%x) : f32[4] return y }',
+    'func @f(%x: f32[4]) -> f32[4] { %y = neg(%x) : f32[99999999999999999999] return %y }',
+    'func @f(%x: f32[4]) -> f32[4] { %y = constant() {value=} : f32[4] return %y }',
+    'func @f(%x: f32[4] -> f32[4] { return %x }',
+    'mesh { "a = 2 }',
+])
+def test_reader_rejects_malformed_text(bad):
+    with pytest.raises(engine.ParseError):
+        engine.Graph(bad)

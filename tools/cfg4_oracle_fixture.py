@@ -19,7 +19,9 @@ import helpers as H  # noqa: E402
 from paper_2112_02958_b200 import capi, engine, modelgen  # noqa: E402
 
 CANDS = {"w2": ("l47_w2", 0, "model", False), "x0": ("x0", 0, "batch", False),
-         "qgrp": ("l0_wq", 1, "model", True), "g1grp": ("l23_g1", 0, "batch", True)}
+         "qgrp": ("l0_wq", 1, "model", True), "g1grp": ("l23_g1", 0, "batch", True),
+         "w1_47": ("l47_w1", 1, "model", False), "w2_45": ("l45_w2", 0, "model", False),
+         "wo_47": ("l47_wo", 0, "model", False), "g2_47": ("l47_g2", 0, "model", False)}
 OUT = os.path.join(ROOT, "tests", "golden", "cfg4_oracle.json")
 
 
@@ -35,9 +37,12 @@ def main():
     r, _ = H.eval_batch("oracle", text, [seq], cfg=cfg)
     rec = {"name": name, "seq": seq, "oracle_seconds": time.time() - t0,
            "result": capi.result_dict(r[0])}
-    data = json.load(open(OUT)) if os.path.exists(OUT) else {"graph": "config 4", "cands": []}
-    data["cands"] = [c for c in data["cands"] if c["name"] != name] + [rec]
-    json.dump(data, open(OUT, "w"), indent=1)
+    if os.environ.get("FIXTURE_PART_DIR"):  # concurrent runs: one file each, merged later
+        json.dump(rec, open(os.path.join(os.environ["FIXTURE_PART_DIR"], name + ".json"), "w"))
+    else:
+        data = json.load(open(OUT)) if os.path.exists(OUT) else {"graph": "config 4", "cands": []}
+        data["cands"] = [c for c in data["cands"] if c["name"] != name] + [rec]
+        json.dump(data, open(OUT, "w"), indent=1)
     print(json.dumps(rec))
 
 
