@@ -108,6 +108,7 @@ struct pe_engine {
   // around each main launch on its stream
   bool ktiming = false;
   uint32_t small_block = 32;  // block size of launches below full occupancy
+  uint32_t cpw_force = 0;     // PE_CPW: cap on candidates per warp (experiments)
   std::vector<cudaEvent_t> kev, kev_free;
 };
 
@@ -141,10 +142,9 @@ bool cuda_ok(cudaError_t e, pe_error* err, const char* what) {
   return false;
 }
 
-#ifndef PE_SOLO
-#define PE_SOLO 0
-#endif
-constexpr uint32_t kThreadsPerSlot = PE_SOLO ? 32 : 1;
+// (round 1's PE_SOLO experiment -- one candidate per warp -- is now the
+// runtime threads-per-slot choice of enqueue_rollouts)
+constexpr uint32_t kThreadsPerSlot = 1;
 #ifndef PE_MIN_BLOCKS
 #define PE_MIN_BLOCKS 8
 #endif
@@ -213,8 +213,10 @@ pe_eval_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant__ 
                uint8_t* arena, uint32_t slots,
                const pe_action* acts, const uint32_t* off, uint32_t n, pe_cost_params cp,
                int64_t baseline, pe_result* out, int32_t* trace, uint32_t trace_words,
-               uint8_t* argflags, uint32_t* ctr) {
-  uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+               uint8_t* argflags, uint32_t* ctr, uint32_t tps) {
+  // tps = threads per slot (pe_rollout_kernel; threads_per_slot)
+  if (threadIdx.x % tps) return;
+  uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) / tps;
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
   for (uint32_t i = slot; i < n; i = next_cand<RETRY>(i, slots, ctr)) {
@@ -260,14 +262,13 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                   pe_action* acts_out, uint32_t* n_out, pe_result* out, uint64_t* legal_out,
                   int32_t legal_words, uint32_t* ctr, const uint32_t* perm,
                   const __grid_constant__ SchedView sv, const __grid_constant__ CacheView cv,
-                  uint32_t* max_acts) {
-#if PE_SOLO
-  // experiment: one active lane per warp (no SIMT divergence across candidates)
-  if (threadIdx.x % 32) return;
-  uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-#else
-  uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
-#endif
+                  uint32_t tps, uint32_t* max_acts) {
+  // tps = threads per slot: one lane in every tps runs a candidate, so a
+  // warp holds 32 / tps candidates (enqueue_rollouts picks it per launch:
+  // the lanes of a warp serialise their divergent paths, so a batch that
+  // does not need every lane runs with fewer candidates per warp)
+  if (threadIdx.x % tps) return;
+  uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) / tps;
   if (slot >= slots) return;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
   // k = schedule position; perm (prefix-trie scheduling) maps it to the
@@ -322,7 +323,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
     // columns of acts_out back)
     if (max_acts) atomicMax(max_acts, n_out[i]);
   };
-  if (RETRY || PE_SOLO) {
+  if (RETRY) {
     for (uint32_t k = slot; k < n; k += slots) run(k);
   } else {
     // Warp-chunked dynamic schedule: the first wave is position `slot`;
@@ -510,6 +511,22 @@ bool ensure_io(pe_engine* e, size_t bytes, pe_error* err) {
 }
 
 uint32_t launch_slots(const pe_engine* e, uint32_t n) { return std::min<uint32_t>(e->slots, n); }
+
+// Candidates per warp of a launch, as threads per slot (32 / candidates per
+// warp).  A lane's candidate waits for the other lanes' divergent paths
+// (config 3: one candidate alone takes 7.5 ms, 1,024 candidates 46 ms at 32
+// per warp but 11.4 ms at 1 per warp), so a launch that does not need every
+// lane of the resident warps runs the fewest candidates per warp that still
+// fit them in one wave: below 4 x the resident warps (the gain measured up
+// to 3.5x; at 7x equal, at 14x 32 per warp wins by 5 %).  PE_CPW forces it.
+uint32_t threads_per_slot(const pe_engine* e, uint32_t slots) {
+  const uint32_t warps = (uint32_t)e->sm_count * PE_SM_THREADS / 32;
+  uint32_t cpw = 32;
+  if ((uint64_t)slots <= 4ull * warps)
+    while (cpw > 1 && (uint64_t)(cpw / 2) * warps >= slots) cpw /= 2;
+  if (e->cpw_force) cpw = std::min<uint32_t>(32, e->cpw_force);
+  return 32 / cpw;
+}
 
 bool ir_expand_batch(pe_engine* e, std::vector<std::vector<pe_action>*>& seqs, cudaStream_t st,
                      pe_error* err);
@@ -828,6 +845,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   e->layout = pe::make_layout(v, /*tight=*/true);
   e->big_layout = pe::make_layout(v, /*tight=*/false);
   if (const char* sd = std::getenv("PE_SCHED_DEPTH")) e->sched_depth = std::atoi(sd);
+  if (const char* cw = std::getenv("PE_CPW")) e->cpw_force = (uint32_t)std::max(0, std::atoi(cw));
   if (const char* sb = std::getenv("PE_SMALL_BLOCK"))  // experiment knob (32 .. 128)
     e->small_block = (uint32_t)std::min(128, std::max(32, std::atoi(sb) / 32 * 32));
   if (const char* sm = std::getenv("PE_SCHED_MIN_BATCH")) e->sched_min_batch = (uint32_t)std::atoi(sm);
@@ -1163,13 +1181,15 @@ pe_status pe_eval_batch_ex(pe_engine* e, const pe_action* acts, const uint32_t* 
   // arenas keep: traced batches run there (the main pass has nothing to do)
   const bool full = d_trace != nullptr && trace_words > 0;
   uint32_t ms = full ? std::min<uint32_t>(e->big_slots, n) : slots;
-  pe_eval_kernel<false><<<(ms + e->small_block - 1) / e->small_block, e->small_block, 0, st>>>(
+  const uint32_t tps = threads_per_slot(e, ms);
+  pe_eval_kernel<false><<<(ms * tps + e->small_block - 1) / e->small_block, e->small_block, 0,
+                          st>>>(
       e->dview, full ? e->big_layout : e->layout, full ? e->d_big_arena : e->d_arena, ms, d_acts,
-      d_off, n, e->cp, e->baseline, d_out, d_trace, trace_words, d_flags, e->d_ctr);
+      d_off, n, e->cp, e->baseline, d_out, d_trace, trace_words, d_flags, e->d_ctr, tps);
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
   pe_eval_kernel<true><<<(bs + e->small_block - 1) / e->small_block, e->small_block, 0, st>>>(
       e->dview, e->big_layout, e->d_big_arena, bs, d_acts, d_off, n, e->cp, e->baseline, d_out,
-      d_trace, trace_words, d_flags, nullptr);
+      d_trace, trace_words, d_flags, nullptr, 1u);
   e->launches += 2;
   if (!cuda_ok(cudaGetLastError(), err, "pe_eval_kernel launch")) return PE_ERR_CUDA;
   if (!(flags & PE_MEM_DEVICE)) {
@@ -1249,7 +1269,7 @@ bool sched_probe(pe_engine* e, const std::vector<std::vector<pe_action>>& prefix
         e->dview, e->big_layout, e->d_big_arena, bs, (const pe_action*)buf[0],
         (const uint32_t*)buf[1], (const uint64_t*)buf[2], n, maxd, e->cp, e->baseline,
         (pe_action*)buf[3], (uint32_t*)buf[4], (pe_result*)buf[5], (uint64_t*)buf[6], lw,
-        nullptr, nullptr, SchedView(), CacheView(), nullptr);
+        nullptr, nullptr, SchedView(), CacheView(), 1u, nullptr);
     e->launches += 2;
     ok = cuda_ok(cudaGetLastError(), err, "probe launch") &&
          cuda_ok(cudaMemcpyAsync(lg.data(), buf[6], sizes[6], cudaMemcpyDeviceToHost, st), err,
@@ -1481,7 +1501,8 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
   cudaError_t ce = cudaMemsetAsync(e->d_ctr + 1, 0, sizeof(uint32_t), st);
   if (ce != cudaSuccess) return ce;
   uint32_t bs = std::min<uint32_t>(e->big_slots, n);
-  uint32_t threads = slots * kThreadsPerSlot;
+  const uint32_t tps = threads_per_slot(e, slots);
+  uint32_t threads = slots * tps;
   // a launch with fewer slots than the resident threads (small batches: MCTS
   // leaf batches, config 4's arena-limited slots) runs one-warp blocks, so
   // the block scheduler spreads its warps over every SM (128-thread blocks
@@ -1521,7 +1542,7 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
     cudaError_t le = cudaLaunchKernelEx(&lc, main_k, gv, e->layout, e->d_arena, slots, d_prefix,
                                         d_poff, d_seeds, n, maxd, e->cp, e->baseline, d_acts,
                                         d_nacts, d_out, d_legal, lw, e->d_ctr + 1, perm, sv,
-                                        cv, max_acts);
+                                        cv, tps, max_acts);
     if (e->ktiming && k0 && k1) {
       cudaEventRecord(k1, st);
       e->kev.push_back(k0);
@@ -1533,7 +1554,7 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
     retry_k<<<bgrid, e->small_block, 0, st>>>(gv, e->big_layout, e->d_big_arena, bs, d_prefix, d_poff,
                                       d_seeds, n, maxd, e->cp, e->baseline, d_acts, d_nacts,
                                       d_out, d_legal, lw, nullptr, nullptr, SchedView(),
-                                      CacheView(), max_acts);
+                                      CacheView(), 1u, max_acts);
     return cudaGetLastError();
   };
   // the instantiation with only the features this launch needs (the
