@@ -587,14 +587,45 @@ struct Cand {
   // lower(); after a whole propagate the dirty bits are clear and the
   // pending-slice list is empty.  (Engines with stuck resurfacing do not
   // schedule, so rs / rsb need no snapshot.)
+  // A saved state is a DELTA against init(): the value records that
+  // differ from their initial ones, every slot added after them, the loop
+  // and argument records, the operand slots that were redirected, the front
+  // stack and the carry bits.  Loading = init() + the delta, so starting
+  // from a saved state never costs more than init() itself (a full copy of
+  // a 52K-op state read ~3 MB per candidate and lost to replaying two
+  // decisions).
   PE_HD static uint64_t snap_bytes(const GraphView& g, const Caps& caps) {
-    return 16ull * (1 + 2ull * caps.V + 2ull * caps.L + (uint64_t)g.A) +
-           4ull * ((uint64_t)g.E + caps.FS + (uint64_t)(g.A >> 5) + 1);
+    return 16ull * (2 + 3ull * (uint64_t)(g.A + g.N) + 2ull * caps.V + 2ull * caps.L +
+                    (uint64_t)g.A) +
+           4ull * (2ull * (uint64_t)g.E + caps.FS + (uint64_t)(g.A >> 5) + 1);
+  }
+  PE_HD void init_records(int32_t v, V4& r0, V4& r1) const {
+    if (v < g.A) {
+      r0 = V4{VK_ARG, v, 0, g.init_uses[v]};
+      r1 = V4{0, -1, -1, 0};
+    } else {
+      r0 = V4{VK_TOP, v - g.A, -1, g.init_uses[v]};
+      r1 = V4{0, -1, -1, 2 * (v - g.A)};
+    }
+  }
+  PE_HD static bool same(const V4& x, const V4& y) {
+    return x.x == y.x && x.y == y.y && x.z == y.z && x.w == y.w;
   }
   PE_HD void save(uint8_t* dst) const {
     V4* p = reinterpret_cast<V4*>(dst);
-    *p++ = V4{nslots, nloops, nfs, result_ref};
-    for (int32_t v = 0; v < nslots; ++v) {
+    V4* head = p;
+    p += 2;
+    int32_t nch = 0;
+    for (int32_t v = 0; v < g.A + g.N; ++v) {
+      V4 r0 = a.vr0()[v], r1 = a.vr1()[v], i0, i1;
+      init_records(v, i0, i1);
+      if (same(r0, i0) && same(r1, i1)) continue;
+      *p++ = V4{v, 0, 0, 0};
+      *p++ = r0;
+      *p++ = r1;
+      ++nch;
+    }
+    for (int32_t v = g.A + g.N; v < nslots; ++v) {
       *p++ = a.vr0()[v];
       *p++ = a.vr1()[v];
     }
@@ -604,17 +635,27 @@ struct Cand {
     }
     for (int32_t x = 0; x < g.A; ++x) *p++ = a.ar0()[x];
     int32_t* q = reinterpret_cast<int32_t*>(p);
-    for (int32_t s = 0; s < g.E; ++s) *q++ = a.opnd()[s];
+    int32_t nop = 0;
+    for (int32_t s = 0; s < g.E; ++s) {
+      int32_t u = a.opnd()[s];
+      if (u == g.oopnd[s]) continue;
+      *q++ = s;
+      *q++ = u;
+      ++nop;
+    }
     for (int32_t i = 0; i < nfs; ++i) *q++ = a.fs()[i];
     for (int32_t w = 0; w <= (g.A >> 5); ++w) *q++ = (int32_t)a.carry()[w];
+    head[0] = V4{nslots, nloops, nfs, result_ref};
+    head[1] = V4{nch, nop, 0, 0};
   }
   // init() for a candidate that starts from a saved prefix state; a state
   // saved from a full-size arena may not fit a tight one (CAPACITY: the
   // retry kernel loads it into a full-size arena)
   PE_HD void load(const uint8_t* src) {
     const V4* p = reinterpret_cast<const V4*>(src);
-    V4 h = *p++;
-    status = PE_CAND_OK;
+    V4 h = p[0], h2 = p[1];
+    p += 2;
+    init();
     if (h.x > caps.V || h.y > caps.L || h.z > caps.FS) {
       fail(PE_CAND_CAPACITY);
       return;
@@ -623,7 +664,13 @@ struct Cand {
     nloops = h.y;
     nfs = h.z;
     result_ref = h.w;
-    for (int32_t v = 0; v < nslots; ++v) {
+    for (int32_t k = 0; k < h2.x; ++k) {
+      int32_t v = p->x;
+      a.vr0()[v] = p[1];
+      a.vr1()[v] = p[2];
+      p += 3;
+    }
+    for (int32_t v = g.A + g.N; v < nslots; ++v) {
       a.vr0()[v] = *p++;
       a.vr1()[v] = *p++;
     }
@@ -633,10 +680,9 @@ struct Cand {
     }
     for (int32_t x = 0; x < g.A; ++x) a.ar0()[x] = *p++;
     const int32_t* q = reinterpret_cast<const int32_t*>(p);
-    for (int32_t s = 0; s < g.E; ++s) a.opnd()[s] = *q++;
+    for (int32_t k = 0; k < h2.y; ++k, q += 2) a.opnd()[q[0]] = q[1];
     for (int32_t i = 0; i < nfs; ++i) a.fs()[i] = *q++;
     for (int32_t w = 0; w <= (g.A >> 5); ++w) a.carry()[w] = (uint32_t)*q++;
-    for (int32_t w = 0; w <= (g.N >> 5); ++w) a.dirty()[w] = 0;
     nrs = 0;
     pend = -1;
     nem = 0;
