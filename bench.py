@@ -41,7 +41,8 @@ def _config(batch, extra=None):
     c = {"workload": WORKLOAD, "graph": "24-layer GPT-2-medium forward (1032 ops, 145 args)",
          "mesh": "[batch=4, model=2]", "candidates_per_step": batch,
          "candidate": "SPEC rollout from root: uniform legal TileValue, Stop w=2 after 1st, <=32",
-         "auto_axes": ["batch", "model"], "group_scopes": True}
+         "auto_axes": ["batch", "model"], "group_scopes": True,
+         "infer_rest_in_action_space": False, "rng": "splitmix64 per candidate (both arms)"}
     if extra:
         c.update(extra)
     return c
