@@ -1838,23 +1838,26 @@ pe_status ir_resolve(pe_engine* e, const RolloutIo& io, cudaStream_t st, pe_erro
       return fail(PE_ERR_CUDA);
     if (m == 0) break;
     std::vector<uint32_t> list(m);
-    if (!cuda_ok(cudaMemcpy(list.data(), d_list, (size_t)m * 4, cudaMemcpyDeviceToHost), err, "D2H ir"))
-      return fail(PE_ERR_CUDA);
+    // (all copies on the call's stream: a pageable cudaMemcpy may return
+    // before its DMA lands, and a non-blocking stream does not wait for it)
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      return cuda_ok(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), err, "D2H ir") &&
+             cuda_ok(cudaStreamSynchronize(st), err, "ir sync");
+    };
+    if (!d2h(list.data(), d_list, (size_t)m * 4)) return fail(PE_ERR_CUDA);
     std::sort(list.begin(), list.end());
-    if (!cuda_ok(cudaMemcpy(d_list, list.data(), (size_t)m * 4, cudaMemcpyHostToDevice), err, "H2D ir"))
+    if (!cuda_ok(cudaMemcpyAsync(d_list, list.data(), (size_t)m * 4, cudaMemcpyHostToDevice, st),
+                 err, "H2D ir") ||
+        !cuda_ok(cudaStreamSynchronize(st), err, "ir sync"))
       return fail(PE_ERR_CUDA);
     if (!have_host) {
       hpoff.assign(io.n + 1, 0);
       hseeds.assign(io.n, 0);
-      bool ok = io.d_poff == nullptr ||
-                cuda_ok(cudaMemcpy(hpoff.data(), io.d_poff, (size_t)(io.n + 1) * 4, cudaMemcpyDeviceToHost),
-                        err, "D2H ir");
-      ok = ok && cuda_ok(cudaMemcpy(hseeds.data(), io.d_seeds, (size_t)io.n * 8, cudaMemcpyDeviceToHost),
-                         err, "D2H ir");
+      bool ok = io.d_poff == nullptr || d2h(hpoff.data(), io.d_poff, (size_t)(io.n + 1) * 4);
+      ok = ok && d2h(hseeds.data(), io.d_seeds, (size_t)io.n * 8);
       if (ok && io.d_prefix && hpoff[io.n]) {
         hp.resize(hpoff[io.n]);
-        ok = cuda_ok(cudaMemcpy(hp.data(), io.d_prefix, hp.size() * sizeof(pe_action),
-                                cudaMemcpyDeviceToHost), err, "D2H ir");
+        ok = d2h(hp.data(), io.d_prefix, hp.size() * sizeof(pe_action));
       }
       if (!io.d_prefix) std::fill(hpoff.begin(), hpoff.end(), 0u);
       if (!ok) return fail(PE_ERR_CUDA);
