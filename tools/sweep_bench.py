@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Config 4 (BASELINE.json configs[3]): batched candidate-evaluation sweep on
-the 48-layer training-step graph (13,757 ops, 1,153 arguments), mesh
+the 48-layer training-step graph (52,154 ops, 1,156 arguments), mesh
 [batch=4, model=2], grouped worklist; batches of rollouts of increasing size,
 device-timed, with the algorithmic-bytes roofline fraction.
 
