@@ -20,6 +20,9 @@
 #include "partir/ir.h"
 #include "partir/parser.h"
 #include "partir/printer.h"
+#include "partir/propagate.h"
+#include "partir/rewrite.h"
+#include "partir/spmd.h"
 #include "pe.h"
 
 // ---- the binding (INTEGRATION.md "Without the print / re-parse round trip")
@@ -81,6 +84,64 @@ pe_graph* graph_from_program(const partir::Program& p) {
   return g;
 }
 
+// ---- drop-in evaluation (needs a GPU): the reference's own apply_tile_action
+// + propagate + lower_to_spmd + collective_stats next to pe_eval_batch on the
+// same Program, in one process, through the C-ABI.  argv: file "eval" then
+// action sequences "value:dim:axis[,value:dim:axis...]".
+int eval_mode(const partir::Program& p, pe_graph* g, int n, char** seqs) {
+  pe_engine* e = nullptr;
+  pe_error err{};
+  if (pe_engine_create(g, nullptr, nullptr, 0, &e, &err) != PE_OK) {
+    std::fprintf(stderr, "pe_engine_create: %s\n", err.message);
+    return 3;
+  }
+  std::vector<pe_action> acts;
+  std::vector<uint32_t> off{0};
+  std::vector<partir::CollectiveStats> ref;
+  for (int c = 0; c < n; ++c) {
+    partir::Program q = p;
+    std::stringstream in(seqs[c]);
+    std::string item;
+    while (std::getline(in, item, ',')) {
+      std::string v = item.substr(0, item.find(':'));
+      std::string rest = item.substr(item.find(':') + 1);
+      int dim = std::stoi(rest.substr(0, rest.find(':')));
+      std::string axis = rest.substr(rest.find(':') + 1);
+      q = partir::propagate(partir::apply_tile_action(q, v, dim, axis)).program;
+      acts.push_back(pe_action{(uint32_t)pe_graph_value_index(g, v.c_str()), (uint8_t)dim,
+                               (uint8_t)pe_graph_axis_index(g, axis.c_str()), PE_ACT_TILE, 0});
+    }
+    off.push_back((uint32_t)acts.size());
+    ref.push_back(partir::collective_stats(partir::lower_to_spmd(q)));
+  }
+  std::vector<pe_result> out(n);
+  if (pe_eval_batch(e, acts.data(), off.data(), (uint32_t)n, out.data(), nullptr, 0, 0, nullptr,
+                    &err) != PE_OK) {
+    std::fprintf(stderr, "pe_eval_batch: %s\n", err.message);
+    return 3;
+  }
+  int bad = 0;
+  for (int c = 0; c < n; ++c) {
+    for (int a = 0; a < (int)p.mesh.axes.size(); ++a) {
+      const std::string& ax = p.mesh.axes[a].name;
+      auto get = [&](const std::map<std::string, partir::CollectiveStats::PerAxis>& m, bool bytes) {
+        auto it = m.find(ax);
+        return it == m.end() ? (int64_t)0 : (bytes ? it->second.bytes : it->second.count);
+      };
+      bad |= get(ref[c].all_reduce, false) != out[c].ar_cnt[a];
+      bad |= get(ref[c].all_reduce, true) != out[c].ar_bytes[a];
+      bad |= get(ref[c].all_gather, false) != out[c].ag_cnt[a];
+      bad |= get(ref[c].all_gather, true) != out[c].ag_bytes[a];
+      bad |= get(ref[c].slice_by_coord, false) != out[c].sbc_cnt[a];
+    }
+    std::printf("%s %s ar=%lld ag=%lld\n", seqs[c], out[c].status == 0 ? "ok" : "status!=0",
+                (long long)ref[c].all_reduce_bytes(), (long long)ref[c].all_gather_bytes());
+  }
+  pe_engine_destroy(e);
+  std::printf("%s\n", bad ? "MISMATCH" : "EVAL OK");
+  return bad ? 1 : 0;
+}
+
 // ---- the check
 int main(int argc, char** argv) {
   if (argc < 2) return 2;
@@ -112,6 +173,7 @@ int main(int argc, char** argv) {
   std::printf("%s args=%d ops=%d operands=%d groups=%d\n", bad ? "MISMATCH" : "OK",
               pe_graph_num_args(a), pe_graph_num_ops(a), pe_graph_num_operands(a),
               pe_graph_num_groups(a));
+  if (!bad && argc > 3 && std::strcmp(argv[2], "eval") == 0) bad = eval_mode(p, a, argc - 3, argv + 3);
   pe_graph_destroy(a);
   pe_graph_destroy(b);
   return bad ? 1 : 0;

@@ -40,3 +40,21 @@ def test_reference_program_through_the_array_binding(oracle_lib, tmp_path, cfgno
     r = subprocess.run([EXE, str(f)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout, r.stderr)
     assert r.stdout.startswith("OK")
+
+
+@pytest.mark.gpu
+def test_drop_in_evaluation_matches_the_reference_in_process(oracle_lib, tmp_path):
+    # the reference's apply_tile_action + propagate + lower_to_spmd +
+    # collective_stats and pe_eval_batch, side by side in one C++ process
+    if not os.path.isdir(REF_INC):
+        pytest.skip("reference headers not available")
+    src = os.path.join(ROOT, "tests", "native", "binding_example.cc")
+    if not os.path.exists(EXE) or os.path.getmtime(EXE) < os.path.getmtime(src):
+        _build()
+    f = tmp_path / "p.pir"
+    f.write_text(modelgen.build_transformer(2, mesh=(("batch", 2), ("model", 2)), **modelgen.TOY))
+    seqs = ["l0_wq:1:model", "l0_wq:1:model,l0_w1:1:model", "x:0:batch",
+            "l1_w2:0:model,l0_wk:2:model", "l0_wo:0:model,x:2:batch"]
+    r = subprocess.run([EXE, str(f), "eval", *seqs], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout, r.stderr)
+    assert "EVAL OK" in r.stdout
