@@ -240,10 +240,29 @@ def emit_plan(engine, plan: PePlan) -> str:
             actions.append({"tile_group": members, "dim": a.dim, "axis": axes[a.axis]})
         elif a.kind == capi.PE_ACT_TILE:
             actions.append({"tile": g.names[a.value], "dim": a.dim, "axis": axes[a.axis]})
+        elif a.kind == capi.PE_ACT_INFER_REST:
+            actions.append({"infer_rest": True})
     d = {"args": args, "output": _spec_json(out_word, (out_word >> 24) & 7, axes),
          "actions": actions, "cost": capi.result_dict(res, g.n_axes), "seed": plan.seed,
          "episodes": plan.episodes, "found_at_episode": plan.found_at_episode}
     return json.dumps(d, sort_keys=True)
+
+
+def plan_actions_from_json(engine, text: str) -> list:
+    """The action sequence of an emitted plan (SPEC: "replayable"): the
+    inverse of emit_plan's "actions" list, for pe_eval_batch."""
+    g = engine.graph
+    out = []
+    for a in json.loads(text)["actions"]:
+        if "infer_rest" in a:
+            out.append(PeAction(0, 0, 0, capi.PE_ACT_INFER_REST, 0))
+        elif "tile_group" in a:
+            grp = g.group_of(g.value_index(a["tile_group"][0]))
+            out.append(PeAction(grp, a["dim"], g.axis_index(a["axis"]), capi.PE_ACT_TILE_GROUP, 0))
+        else:
+            out.append(PeAction(g.value_index(a["tile"]), a["dim"], g.axis_index(a["axis"]),
+                                capi.PE_ACT_TILE, 0))
+    return out
 
 
 def megatron_signature(res, model_axis: int, layers: int) -> bool:

@@ -121,3 +121,23 @@ def test_search_with_infer_rest_equals_oracle_search(oracle_lib):
                          episodes=256, seed=11, leaf_batch=32)
     assert search.plan_actions(gp) == search.plan_actions(op)
     assert not H.compare_results(gp.result, op.result)
+
+
+def test_emitted_plan_with_infer_rest_replays(oracle_lib):
+    # SPEC emit_plan: the plan file is replayable; an InferRest decision is
+    # kept as a decision and re-expanded on replay
+    text = PROGRAMS["t2"]()
+    cfg = capi.default_search_config(group_scopes=1, infer_rest_action=1)
+    eng = engine.Engine(engine.Graph(text), device=0, cfg=cfg)
+    res, seqs, _ = eng.rollout_batch([[]] * 256, list(range(256)))
+    k = next(i for i, sq in enumerate(seqs) if any(a[3] == capi.PE_ACT_INFER_REST for a in sq))
+    plan = capi.PePlan()
+    plan.n_actions = len(seqs[k])
+    for i, a in enumerate(seqs[k]):
+        plan.actions[i] = capi.PeAction(*a, 0)
+    plan.result = res[k]
+    import json
+    d = search.emit_plan(eng, plan)
+    assert any("infer_rest" in a for a in json.loads(d)["actions"])
+    again = eng.eval_batch([search.plan_actions_from_json(eng, d)])[0]
+    assert not H.compare_results(again, res[k])
