@@ -365,6 +365,26 @@ struct Pull {
 constexpr int kFInferRest = 1;
 constexpr int kFResume = 2;
 constexpr int kFAll = kFInferRest | kFResume;
+// kFCoop: a whole warp runs ONE candidate (launches with one candidate per
+// warp): every lane executes the sequential rewrite / lowering chain in
+// lockstep on the same data (no divergence, broadcast loads, identical
+// stores), and the data-parallel phases -- init(), the legal-set scan, the
+// liveness sweep and its sums -- are split across the lanes (warp ballots,
+// shuffle scans and reductions).
+constexpr int kFCoop = 4;
+
+PE_HD int32_t pe_lane() {
+#ifdef __CUDA_ARCH__
+  return (int32_t)(threadIdx.x & 31);
+#else
+  return 0;
+#endif
+}
+PE_HD void pe_syncwarp() {
+#ifdef __CUDA_ARCH__
+  __syncwarp();
+#endif
+}
 
 struct Resume {
   const uint8_t* snap = nullptr;
@@ -548,23 +568,26 @@ struct Cand {
   }
 
   // ------------------------------------------------------------ init
-  PE_HD void init() {
+  // (ln, nl): this lane and the lanes sharing the candidate (kFCoop), or
+  // (0, 1) for one lane per candidate
+  PE_HD void init(int32_t ln = 0, int32_t nl = 1) {
     int32_t A = g.A, N = g.N;
-    for (int32_t v = 0; v < A; ++v) {
+    for (int32_t v = ln; v < A; v += nl) {
       a.vr0()[v] = V4{VK_ARG, v, 0, g.init_uses[v]};
       a.vr1()[v] = V4{0, -1, -1, 0};
       a.ar0()[v] = V4{0, -1, 0, 0};  // adirect, aslice, awrapped (+aspec0)
     }
-    for (int32_t o = 0; o < N; ++o) {
+    for (int32_t o = ln; o < N; o += nl) {
       int32_t v = A + o;
       a.vr0()[v] = V4{VK_TOP, o, -1, g.init_uses[v]};  // vaux: odd slot empty
       a.vr1()[v] = V4{0, -1, -1, 2 * o};
     }
-    for (int32_t s = 0; s < g.E; ++s) a.opnd()[s] = g.oopnd[s];
-    for (int32_t w = 0; w <= (A >> 5); ++w) a.carry()[w] = 0;
-    for (int32_t w = 0; w <= (N >> 5); ++w) a.dirty()[w] = 0;
+    for (int32_t s = ln; s < g.E; s += nl) a.opnd()[s] = g.oopnd[s];
+    for (int32_t w = ln; w <= (A >> 5); w += nl) a.carry()[w] = 0;
+    for (int32_t w = ln; w <= (N >> 5); w += nl) a.dirty()[w] = 0;
     if (g.resurface)
-      for (int32_t w = 0; w <= (N >> 5); ++w) a.rsb()[w] = 0;
+      for (int32_t w = ln; w <= (N >> 5); w += nl) a.rsb()[w] = 0;
+    if (nl > 1) pe_syncwarp();
     nrs = 0;
     pend = -1;
     nslots = A + N;
@@ -651,11 +674,11 @@ struct Cand {
   // init() for a candidate that starts from a saved prefix state; a state
   // saved from a full-size arena may not fit a tight one (CAPACITY: the
   // retry kernel loads it into a full-size arena)
-  PE_HD void load(const uint8_t* src) {
+  PE_HD void load(const uint8_t* src, int32_t ln = 0, int32_t nl = 1) {
     const V4* p = reinterpret_cast<const V4*>(src);
     V4 h = p[0], h2 = p[1];
     p += 2;
-    init();
+    init(ln, nl);
     if (h.x > caps.V || h.y > caps.L || h.z > caps.FS) {
       fail(PE_CAND_CAPACITY);
       return;
@@ -1665,7 +1688,7 @@ struct Cand {
 
   // ------------------------------------------------------------ scoring
   PE_HD void score(const pe_cost_params& cp, int64_t baseline, int32_t steps,
-                   pe_result& r) {
+                   pe_result& r, int32_t ln = 0, int32_t nl = 1) {
     // collective_stats (REF spmd.cc:405-434), accumulated at emission
     for (int x = 0; x < PE_MAX_AXES; ++x) {
       r.ar_bytes[x] = a.st8()[x];
@@ -1681,7 +1704,44 @@ struct Cand {
     // the same pass.
     if (result_buf >= g.A) a.em_last()[result_buf - g.A] = nem - 1;
     a.delta()[nem] = 0;
-    int64_t run = 0, best = 0;
+    int64_t run = 0, best = 0, base = 0;
+#ifdef __CUDA_ARCH__
+    if (nl > 1) {
+      // the warp's lanes (kFCoop): every -lb[j] lands first (atomics: two
+      // buffers may end at the same op), then a shuffle scan per 32 ops
+      // carries the running sum and a warp max keeps its peak
+      pe_syncwarp();
+      for (int32_t j = ln; j < nem; j += nl) {
+        V4 q = a.em_q0()[j];
+        int64_t lb = a.em_q1()[j].x;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&a.delta()[q.z + 1]),
+                  (unsigned long long)(-lb));
+      }
+      __syncwarp();
+      int64_t carry = 0;
+      for (int32_t c = 0; c < nem; c += 32) {
+        int32_t j = c + ln;
+        int64_t d = j < nem ? a.em_q1()[j].y : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          int64_t t = __shfl_up_sync(0xFFFFFFFFu, d, off);
+          if (ln >= off) d += t;
+        }
+        int64_t m = j < nem ? carry + d : 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          int64_t t = __shfl_xor_sync(0xFFFFFFFFu, m, off);
+          m = t > m ? t : m;
+        }
+        best = m > best ? m : best;
+        carry += __shfl_sync(0xFFFFFFFFu, d, 31);
+      }
+      for (int32_t x = ln; x < g.A; x += nl) base += a.alb0()[x];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) base += __shfl_xor_sync(0xFFFFFFFFu, base, off);
+      __syncwarp();
+    } else
+#endif
     for (int32_t j = 0; j < nem; ++j) {
       V4 q = a.em_q0()[j];  // head, op0, last, operand offset
       I64x2 q1 = a.em_q1()[j];  // local bytes, liveness delta
@@ -1692,8 +1752,8 @@ struct Cand {
       a.delta()[q.z + 1] -= lb;
 #endif
     }
-    int64_t base = 0;
-    for (int32_t x = 0; x < g.A; ++x) base += a.alb0()[x];
+    if (nl == 1)
+      for (int32_t x = 0; x < g.A; ++x) base += a.alb0()[x];
     r.peak_bytes = base + best;
     r.flops = flops;
     r.n_spmd_ops = nem;
@@ -1758,19 +1818,20 @@ struct Cand {
   // resurfacing kernel); otherwise the stuck analysis rides on lowering
   PE_HD void finish(const pe_cost_params& cp, int64_t baseline, int32_t steps,
                     bool propagated, pe_result& r, int32_t* trace, uint32_t trace_words,
-                    bool separate = false) {
+                    bool separate = false, int32_t ln = 0, int32_t nl = 1) {
     tick(5);
     nstk = 0;
     if (separate && !bad() && propagated) analyze();
     tick(6);
     if (!bad()) lower(!separate && propagated);
     tick(7);
-    finish_result(cp, baseline, steps, propagated, r, trace, trace_words);
+    finish_result(cp, baseline, steps, propagated, r, trace, trace_words, ln, nl);
     clear_seen();
     tick(8);
   }
   PE_HD void finish_result(const pe_cost_params& cp, int64_t baseline, int32_t steps,
-                           bool propagated, pe_result& r, int32_t* trace, uint32_t trace_words) {
+                           bool propagated, pe_result& r, int32_t* trace, uint32_t trace_words,
+                           int32_t ln = 0, int32_t nl = 1) {
     if (bad()) {
       int32_t st = status;
       for (int x = 0; x < PE_MAX_AXES; ++x) {
@@ -1790,7 +1851,7 @@ struct Cand {
       return;
     }
     int32_t fs = r.fail_step;
-    score(cp, baseline, steps, r);
+    score(cp, baseline, steps, r, ln, nl);
     r.n_stuck = propagated ? nstk : 0;
     r.status = status;
     r.fail_step = fs;
@@ -1913,6 +1974,27 @@ struct Cand {
     r.reserved = draws;
     r.n_steps = steps;
   }
+#ifdef __CUDA_ARCH__
+  // build_legal<false> with the warp's lanes splitting the ordinals: a
+  // ballot per 32 ordinals keeps the list in ordinal order (kFCoop)
+  PE_HD int32_t build_legal_coop(int32_t ln) {
+    int32_t n = 0;
+    for (int32_t base = 0; base < g.n_ord; base += 32) {
+      int32_t o = base + ln;
+      bool ok = false;
+      if (o < g.n_ord)
+        for (int32_t i = g.ord_off[o]; i < g.ord_off[o + 1] && !ok; ++i) {
+          int32_t m = g.ord_mem[i];
+          ok = !((a.carry()[m >> 5] >> (m & 31)) & 1u);
+        }
+      unsigned b = __ballot_sync(0xFFFFFFFFu, ok);
+      if (ok) a.lg()[n + __popc(b & ((1u << ln) - 1u))] = o;
+      n += __popc(b);
+    }
+    __syncwarp();
+    return n;
+  }
+#endif
   PE_HD pe_action ordinal_action(int32_t ord) const {
     pe_action x;
     int32_t na = g.n_auto;
@@ -1957,14 +2039,16 @@ struct Cand {
     int32_t steps = 0, nacts = 0;
     bool propagated = false, terminal = false;
     constexpr bool IR = (F & kFInferRest) != 0, RES = (F & kFResume) != 0;
+    constexpr bool COOP = (F & kFCoop) != 0;
+    const int32_t ln = COOP ? pe_lane() : 0, nln = COOP ? 32 : 1;
     if (RES && rs.snap) {
-      load(rs.snap);
+      load(rs.snap, ln, nln);
       for (int32_t k = 0; k < rs.done && k < maxd; ++k) acts_out[k] = rs.path[k];
       steps = nacts = rs.done;
       propagated = rs.done > 0;
       terminal = rs.stop;
     } else {
-      init();
+      init(ln, nln);
     }
     tick(0);
     r.fail_step = -1;
@@ -2032,7 +2116,11 @@ struct Cand {
     }
     if (!bad() && status == PE_CAND_OK) {
       if (legal_out) {
+#ifdef __CUDA_ARCH__
+        int32_t nl = COOP ? build_legal_coop(ln) : build_legal<RS>();
+#else
         int32_t nl = build_legal<RS>();
+#endif
         for (int32_t i = 0; i < nl; ++i) legal_out[a.lg()[i] >> 6] |= 1ull << (a.lg()[i] & 63);
         if (IR && g.ir_ord >= 0 && infer_rest_legal())
           legal_out[g.ir_ord >> 6] |= 1ull << (g.ir_ord & 63);
@@ -2043,7 +2131,11 @@ struct Cand {
       while (!terminal) {
         if (steps >= maxd) break;
         tick(4);
+#ifdef __CUDA_ARCH__
+        int32_t nl = COOP ? build_legal_coop(ln) : build_legal<RS>();
+#else
         int32_t nl = build_legal<RS>();
+#endif
         // InferRest follows the TileValue actions (SPEC legal_actions order)
         int32_t ir = IR && g.ir_ord >= 0 && infer_rest_legal() ? 1 : 0;
         if (nl + ir == 0) break;
@@ -2078,7 +2170,7 @@ struct Cand {
       }
     }
     *n_out = (uint32_t)(nacts < maxd ? nacts : maxd);
-    finish(cp, baseline, steps, propagated, r, nullptr, 0);
+    finish(cp, baseline, steps, propagated, r, nullptr, 0, false, ln, nln);
   }
 };
 

@@ -109,6 +109,7 @@ struct pe_engine {
   bool ktiming = false;
   uint32_t small_block = 32;  // block size of launches below full occupancy
   uint32_t cpw_force = 0;     // PE_CPW: cap on candidates per warp (experiments)
+  bool coop = true;           // one-candidate-per-warp launches run warp-cooperatively
   std::vector<cudaEvent_t> kev, kev_free;
 };
 
@@ -267,9 +268,12 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
   // warp holds 32 / tps candidates (enqueue_rollouts picks it per launch:
   // the lanes of a warp serialise their divergent paths, so a batch that
   // does not need every lane runs with fewer candidates per warp)
-  if (threadIdx.x % tps) return;
+  // (kFCoop: tps = 32 and every lane of the warp runs its one candidate)
+  constexpr bool COOP = (F & pe::kFCoop) != 0;
+  if (!COOP && threadIdx.x % tps) return;
   uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) / tps;
   if (slot >= slots) return;
+  const bool writer = !COOP || (threadIdx.x & 31) == 0;
   pe::Cand c(g, L, arena + (uint64_t)(slot / pe::kLanes) * L.bytes, slot % pe::kLanes);
   // k = schedule position; perm (prefix-trie scheduling) maps it to the
   // candidate, so lanes of a warp run candidates that share their first
@@ -309,7 +313,7 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
                            cp, baseline, acts_out + (uint64_t)i * maxd, n_out + i, r,
                            legal_out ? legal_out + (uint64_t)i * legal_words : nullptr,
                            legal_words, rs);
-    out[i] = r;
+    if (writer) out[i] = r;
 #if defined(PE_CAND_TIMES) && defined(__CUDA_ARCH__)
     if (!RETRY && k < kCandTimesCap) {
       g_cand_times[2 * k] = t_begin;
@@ -321,9 +325,9 @@ pe_rollout_kernel(const __grid_constant__ pe::GraphView g, const __grid_constant
 #endif
     // longest action list of the batch (host mode copies only that many
     // columns of acts_out back)
-    if (max_acts) atomicMax(max_acts, n_out[i]);
+    if (max_acts && writer) atomicMax(max_acts, n_out[i]);
   };
-  if (RETRY) {
+  if (RETRY || COOP) {
     for (uint32_t k = slot; k < n; k += slots) run(k);
   } else {
     // Warp-chunked dynamic schedule: the first wave is position `slot`;
@@ -845,6 +849,7 @@ pe_status pe_engine_create(const pe_graph* graph, const pe_search_config* cfg,
   e->layout = pe::make_layout(v, /*tight=*/true);
   e->big_layout = pe::make_layout(v, /*tight=*/false);
   if (const char* sd = std::getenv("PE_SCHED_DEPTH")) e->sched_depth = std::atoi(sd);
+  if (const char* co = std::getenv("PE_COOP")) e->coop = std::atoi(co) != 0;
   if (const char* cw = std::getenv("PE_CPW")) e->cpw_force = (uint32_t)std::max(0, std::atoi(cw));
   if (const char* sb = std::getenv("PE_SMALL_BLOCK"))  // experiment knob (32 .. 128)
     e->small_block = (uint32_t)std::min(128, std::max(32, std::atoi(sb) / 32 * 32));
@@ -1562,8 +1567,15 @@ cudaError_t enqueue_rollouts(pe_engine* e, const pe::GraphView& gv, const pe_act
   // resurfacing engines never use saved states
   const bool ir = gv.ir_ord >= 0 || gv.ir_pause;
   const bool res = (sv.keys && sv.snap) || cv.from;
+  // one candidate per warp: the whole warp runs it (kFCoop)
+  const bool coop = tps == 32 && e->coop && !ir && !e->wl.resurface;
   cudaError_t lerr;
-  if (e->wl.resurface)
+  if (coop)
+    lerr = res ? launch(pe_rollout_kernel<false, false, pe::kFCoop | pe::kFResume>,
+                        pe_rollout_kernel<true, false, 0>)
+               : launch(pe_rollout_kernel<false, false, pe::kFCoop>,
+                        pe_rollout_kernel<true, false, 0>);
+  else if (e->wl.resurface)
     lerr = ir ? launch(pe_rollout_kernel<false, true, pe::kFInferRest>,
                        pe_rollout_kernel<true, true, pe::kFInferRest>)
               : launch(pe_rollout_kernel<false, true, 0>, pe_rollout_kernel<true, true, 0>);
