@@ -99,3 +99,24 @@ def test_gpu_searched_plan_preserves_semantics(oracle_lib):
     p = search.mcts_search(eng, episodes=500, seed=4, leaf_batch=64)
     ok, diff, _ = H.oracle_check_equivalence(text, search.plan_actions(p), trials=3)
     assert ok, diff
+
+
+def test_config1_mlp_search_seeds_equal_the_reference_search(oracle_lib):
+    # BASELINE.json configs[0] / SURVEY.md §8(d) config 1: the 2-layer MLP on
+    # {model=8}, MCTS with the SPEC defaults (memory + comm cost model, budget
+    # 500 episodes), seeds 0-19 on the GPU engine; the same searches driven by
+    # the reference CPU path (oracle evaluator) return identical plans
+    text = modelgen.config_program(1)
+    g = engine.Graph(text)
+    cfg = capi.default_search_config(group_scopes=0)
+    cp = capi.default_cost_params()
+    ords = search.ordinal_actions(g, cfg)
+    lw = (len(ords) - 1 + 63) // 64
+    eng = _engine(text, cfg, cp)
+    plans = [search.mcts_search(eng, episodes=500, seed=s, leaf_batch=64) for s in range(20)]
+    assert all(p.result.status == capi.PE_CAND_OK and p.episodes == 500 for p in plans)
+    for s in range(0, 20, 5):
+        op = search.run_mcts(evaluator("oracle", text, cfg, cp, lw), len(ords) - 1, ords,
+                             episodes=500, seed=s, leaf_batch=64)
+        assert search.plan_actions(plans[s]) == search.plan_actions(op)
+        assert not H.compare_results(plans[s].result, op.result)
