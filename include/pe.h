@@ -56,7 +56,8 @@ enum {
                             (REF rewrite.cc:61-113, propagate.cc:459-482)      */
   PE_ACT_TILE_GROUP = 1, /* the same on every member of a scope group, one
                             propagate (grouping SPEC:568)            */
-  PE_ACT_INFER_REST = 2, /* infer_rest (REF propagate.cc:484-544) — reserved   */
+  PE_ACT_INFER_REST = 2, /* infer_rest (REF propagate.cc:484-544) over the auto
+                            axes; a decision                    */
   PE_ACT_STOP = 3        /* terminal                                           */
 };
 
@@ -73,8 +74,9 @@ typedef struct pe_action {
  * INFER_REST marker before it is). */
 #define PE_ACT_FLAG_INFERRED 1u
 /* An INFER_REST marker whose inferred tile actions follow it (output of
- * pe_infer_rest).  Unexpanded INFER_REST actions are expanded by the host
- * entry points; the kernels only accept expanded markers. */
+ * pe_infer_rest).  Unexpanded INFER_REST actions are expanded by the entry
+ * points: pe_eval_batch (host buffers) and pe_rollout_batch expand every
+ * candidate's next one in the same batched evaluation. */
 #define PE_ACT_FLAG_EXPANDED 2u
 
 /* ---- per-candidate result record ---- */
@@ -307,9 +309,17 @@ pe_status pe_infer_rest(pe_engine* e, const pe_action* prefix, uint32_t n_prefix
  * pe_engine_legal_words() uint64 words, may be NULL), then samples actions
  * with the rollout policy (uniform, Stop weight 2 after the first decision,
  * at most max_decisions) from a splitmix64 stream seeded with seeds[c], and
- * scores the terminal state.  acts_out receives prefix + sampled actions
+ * scores the terminal state.  acts_out receives the candidate's DECISIONS --
+ * the prefix's and the sampled ones; an InferRest decision as its unexpanded
+ * marker, its inferred tiles omitted, so replaying the row re-derives them
  * (row stride max_decisions per candidate; entries past a candidate's
- * n_acts_out are unspecified), n_acts_out the count. */
+ * n_acts_out are unspecified), n_acts_out the count.  With infer_rest_action
+ * (or an unexpanded InferRest in a host prefix) a candidate that reaches an
+ * InferRest decision pauses; all paused candidates are expanded together
+ * (each inference round's trials in one batched evaluation) and resume with
+ * their RNG streams advanced by the draws they consumed.  A launch runs 32
+ * candidates per warp when it needs every resident lane, fewer otherwise,
+ * and one candidate per warp warp-cooperatively. */
 pe_status pe_rollout_batch(pe_engine* e, const pe_action* prefix,
                            const uint32_t* prefix_off, const uint64_t* seeds,
                            uint32_t n_cand, pe_action* acts_out,
