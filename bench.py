@@ -266,6 +266,26 @@ def run_engine(args):
     total_ms = _max_over_ranks(dist, sum(step_ms), dev)
     value = ws * K * B / (total_ms / 1e3)
 
+    # the round-1 step size, same timing rules, device-timed only: keeps the
+    # number comparable across rounds (DESIGN.md §8 batch-size table)
+    also = None
+    B2 = args.also_batch
+    if 0 < B2 < B:
+        poff2 = poff[:B2 + 1]
+        ms2 = []
+        for i in range(W + K):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.rollout_batch_device(None, poff2.data_ptr(), seeds[i].data_ptr(), B2,
+                                     acts_out.data_ptr(), nacts.data_ptr(), res.data_ptr(), stream=sp)
+            e1.record(stream)
+            ms2.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        t2 = _max_over_ranks(dist, sum(a.elapsed_time(b) for a, b in ms2[W:]), dev)
+        also = {"candidates_per_step": B2, "value": ws * K * B2 / (t2 / 1e3), "ms_per_step": t2 / K,
+                "note": "round-1 step size; device-timed, L2 flushed between steps"}
+
     # sanity: every candidate evaluated OK (numpy views of the pe_result
     # fields; no per-candidate Python objects, whose garbage collection
     # could land in the e2e timing below)
@@ -389,7 +409,8 @@ def run_engine(args):
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
                 "cpu_baseline": cpu,
                 "parity_sample": parity,
-                "clocks": clk.summary()}
+                "clocks": clk.summary(),
+                "also_measured": also}
         print(json.dumps(line))
     if dist:
         dist.barrier()
@@ -730,7 +751,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     # >= the engine's resident slots (148 SMs x 32 warps x 32 lanes = 151,552)
-    ap.add_argument("--batch", type=int, default=262144)
+    ap.add_argument("--batch", type=int, default=1048576,
+                    help="rollouts per step (about 7 waves of the config-3 slots)")
+    ap.add_argument("--also-batch", type=int, default=262144,
+                    help="also time this step size (round 1's), device-timed; 0 = off")
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity-sample", action="store_true")
