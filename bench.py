@@ -266,26 +266,6 @@ def run_engine(args):
     total_ms = _max_over_ranks(dist, sum(step_ms), dev)
     value = ws * K * B / (total_ms / 1e3)
 
-    # the round-1 step size, same timing rules, device-timed only: keeps the
-    # number comparable across rounds (DESIGN.md §8 batch-size table)
-    also = None
-    B2 = args.also_batch
-    if 0 < B2 < B:
-        poff2 = poff[:B2 + 1]
-        ms2 = []
-        for i in range(W + K):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            eng.rollout_batch_device(None, poff2.data_ptr(), seeds[i].data_ptr(), B2,
-                                     acts_out.data_ptr(), nacts.data_ptr(), res.data_ptr(), stream=sp)
-            e1.record(stream)
-            ms2.append((e0, e1))
-        torch.cuda.synchronize(dev)
-        t2 = _max_over_ranks(dist, sum(a.elapsed_time(b) for a, b in ms2[W:]), dev)
-        also = {"candidates_per_step": B2, "value": ws * K * B2 / (t2 / 1e3), "ms_per_step": t2 / K,
-                "note": "round-1 step size; device-timed, L2 flushed between steps"}
-
     # sanity: every candidate evaluated OK (numpy views of the pe_result
     # fields; no per-candidate Python objects, whose garbage collection
     # could land in the e2e timing below)
@@ -309,6 +289,27 @@ def run_engine(args):
     if rank == 0 and not args.no_parity_sample:
         parity = _parity_sample(text, cfg, seeds[K - 1].cpu().numpy(), acts_out, nacts, res, B,
                                 maxd, args.parity_n)
+    # the round-1 step size, same timing rules, device-timed only (after the
+    # parity sample: it overwrites the output buffers): keeps the
+    # number comparable across rounds (DESIGN.md §8 batch-size table)
+    also = None
+    B2 = args.also_batch
+    if 0 < B2 < B:
+        poff2 = poff[:B2 + 1]
+        ms2 = []
+        for i in range(W + K):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.rollout_batch_device(None, poff2.data_ptr(), seeds[i].data_ptr(), B2,
+                                     acts_out.data_ptr(), nacts.data_ptr(), res.data_ptr(), stream=sp)
+            e1.record(stream)
+            ms2.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        t2 = _max_over_ranks(dist, sum(a.elapsed_time(b) for a, b in ms2[W:]), dev)
+        also = {"candidates_per_step": B2, "value": ws * K * B2 / (t2 / 1e3), "ms_per_step": t2 / K,
+                "note": "round-1 step size; device-timed, L2 flushed between steps"}
+
     gc.collect()
 
     # e2e: the public C-ABI with HOST buffers (pinned), copies inside the region

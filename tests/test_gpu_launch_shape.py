@@ -1,13 +1,13 @@
 """GPU parity of the exact launch shape bench.py times.
 
-A bench step is 262,144 root rollouts, more than the engine's resident slots
-(148 SMs x 1024 = 151,552).  That launch takes paths small batches never
-reach: SM-wide 1024-thread blocks (pe_engine.cu launch geometry), the
-warp-chunked second wave claimed from the work counter (__activemask +
-__shfl_sync), and arena reuse by a second candidate inside one launch.  Every
-candidate of such a launch must equal the same seed evaluated in a
-single-wave launch (8,192 candidates: one candidate per thread, 128-thread
-blocks), and a strided sample must equal the oracle (the patched reference's
+A bench step is 1,048,576 root rollouts (round 1: 262,144), about seven
+times the engine's resident slots (148 SMs x 1024 = 151,552).  That launch
+takes paths small batches never reach: SM-wide 1024-thread blocks at 32
+candidates per warp (pe_engine.cu launch geometry), the warp-chunked later
+waves claimed from the work counter (__activemask + __shfl_sync), and arena
+reuse by later candidates inside one launch.  Every candidate of such a launch
+must equal the same seed evaluated in single-wave launches (8,192 candidates:
+two per warp, one-warp blocks), and a strided sample must equal the oracle (the patched reference's
 propagate / lower_to_spmd / collective_stats + the SPEC cost and rollout
 restatement) bit-exactly on every integer field.
 """
@@ -21,7 +21,7 @@ from paper_2112_02958_b200 import capi, engine, modelgen
 
 pytestmark = pytest.mark.gpu
 
-N_FULL = 262144
+N_FULL = 1048576  # bench.py --batch default
 WAVE = 8192
 
 
